@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark: move evaluations/s (and tabu iterations/s) of the B200 engine.
+
+Default workload = BASELINE.json configs[2], the batched multi-start config the
+1e10 moves/s target is quoted on: 4096 independent tabu runs of a
+20-vehicle / 100-mission instance, 1000 iterations each, on one GPU (SURVEY
+§8.0 C3).  One step = one `as_batch_run` call over the whole batch (every §8(a)
+row: decode, gather, delta, feasibility, tabu/aspiration, key reduction,
+on-device apply, loop control, per-run kick).  Under torchrun each rank runs its
+own 4096 runs (seeds offset by rank): weak scaling, no data-path collective.
+
+Contract keys: see the task statement; `--impl reference` times the CPU oracle
+(the reference arm of this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2002_11710_b200 import instgen  # noqa: E402
+
+METRIC = "move evals/sec and tabu iters/sec per B200 (1/2/4/8 GPU), % roofline"
+UNIT = "move evals/s"
+
+# Algorithmic integer operations per scored move: the
+# adds/compares/selects the formulas of §8(a) a3-a6 require per (m,t) pair or
+# per swap pair, with the per-row removal part amortised.
+OPS_RELOCATE = 18
+OPS_SWAP = 34
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload(name):
+    cfg = instgen.CONFIGS[name]
+    inst = instgen.generate(name)
+    return cfg, inst
+
+
+def cpu_oracle_leg(inst, cfg, start, runs, iters, threads):
+    """The oracle as it stands, on `threads` host threads (ctypes releases the GIL)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    O = oracle.Oracle(inst)
+    p, m = start
+
+    def one(seed):
+        r = O.search(p, m, mode=1, tenure=cfg.tenure, max_iters=iters, seed=seed, kick=cfg.kick, trace=False)
+        return r["iters_done"]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        done = list(ex.map(one, range(1, runs + 1)))
+    dt = time.perf_counter() - t0
+    return sum(done), dt
+
+
+def valid_moves(inst):
+    n, V = inst.n_missions, inst.n_vehicles
+    return n * (n + V - 2) + n * (n - 1) // 2
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg, inst = workload(args.workload)
+    import oracle
+    O = oracle.Oracle(inst)
+    st, start, _, _ = O.greedy()
+    if st != 0:
+        start = (inst.planted_ptr, inst.planted_missions)
+    cores = os.cpu_count() or 1
+    runs, iters = cores * args.ref_runs_per_core, args.ref_iters
+    for _ in range(args.warmup):
+        cpu_oracle_leg(inst, cfg, start, max(1, cores), 5, cores)
+    tot_it, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        it, dt = cpu_oracle_leg(inst, cfg, start, runs, iters, cores)
+        tot_it += it
+        tot_t += dt
+    value = tot_it * valid_moves(inst) / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"C3 batched ({args.workload})", "runs_per_step": runs, "iters_per_run": iters,
+                       "n_missions": inst.n_missions, "n_vehicles": inst.n_vehicles},
+            "tabu_iters_per_s": tot_it / tot_t,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{runs} runs x {iters} TS iterations of the C3 instance per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2002_11710_b200 import airsched as A
+
+    cfg, inst = workload(args.workload)
+    R = args.runs or cfg.n_runs
+    iters = args.iters or cfg.max_iters
+    h = A.Instance(inst)
+    stream = torch.cuda.current_stream(dev)
+    ctx = A.Ctx(local, stream.cuda_stream)
+    ctx.upload(h)
+    p, m, nrep = A.as_init_greedy(ctx, h)
+    start = (p, m)
+    prm = A.params(mode=A.AS_MODE_TABU, tenure=cfg.tenure, max_iters=iters, kick=cfg.kick, trace_level=0)
+    seeds_np = np.arange(1 + rank * R, 1 + (rank + 1) * R, dtype=np.uint64)
+    # device-resident inputs and outputs for the kernel-timed value
+    tp = torch.from_numpy(p).to(dev)
+    tm = torch.from_numpy(m).to(dev)
+    ts = torch.from_numpy(seeds_np.view(np.int64)).to(dev)
+    tres = torch.zeros((R, 40), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        A.as_batch_run(ctx, h, R, tp, tm, prm, ts, shared_start=True, results=tres)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    sampler = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters_total = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for k in range(args.steps):
+        flush.zero_()                      # L2 flush between timed steps (outside the events)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.kernel_launches - launches0
+    res = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(R)
+    iters_total = int(res["iters_done"].sum()) * args.steps
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        it_t = torch.tensor([iters_total], dtype=torch.int64, device=dev)
+        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+        iters_all = int(it_t.item())
+    else:
+        iters_all = iters_total
+    VM = valid_moves(inst)
+    value = iters_all * VM / (t_ms / 1e3)
+    # best over all runs of all ranks: (best_obj << 32 | global run) min
+    gbest = int(np.min((res["best_obj"].astype(np.int64) << 20) | (np.arange(R) + rank * R)))
+    if world > 1:
+        gb = torch.tensor([gbest], dtype=torch.int64, device=dev)
+        dist.all_reduce(gb, op=dist.ReduceOp.MIN)
+        gbest = int(gb.item())
+
+    # ---- e2e: the same call with pinned HOST buffers (H2D/D2H inside the timed region)
+    hp = torch.from_numpy(p).pin_memory()
+    hm = torch.from_numpy(m).pin_memory()
+    hs = torch.from_numpy(seeds_np.view(np.int64)).pin_memory()
+    hres = torch.zeros((R, 40), dtype=torch.uint8).pin_memory()
+    e2e_ms = []
+    for k in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A.as_batch_run(ctx, h, R, hp, hm, prm, hs, shared_start=True, results=hres)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_iters = int(hres.numpy().view(A.RESULT_DTYPE)["iters_done"].sum())
+    e2e_value = e2e_iters * VM / (float(np.mean(e2e_ms)) / 1e3) * world
+    h2d = p.nbytes + m.nbytes + seeds_np.nbytes
+    d2h = R * 40
+
+    # ---- roofline of the dominant kernel (k_search = the whole step)
+    ops = (inst.n_missions * (inst.n_missions + inst.n_vehicles - 2) * OPS_RELOCATE +
+           inst.n_missions * (inst.n_missions - 1) // 2 * OPS_SWAP)
+    f_mhz = clocks.get("sm_mhz") or 1965.0
+    peak_gops = 148 * 128 * f_mhz * 1e6 / 1e9
+    achieved_gops = (iters_total * ops) / (t_ms / 1e3) / 1e9 if world == 1 else (iters_all * ops) / (t_ms / 1e3) / world / 1e9
+    roof = {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
+            "frac": achieved_gops / peak_gops, "traffic": args.traffic,
+            "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle  # noqa: F401  (cpu_baseline leg only)
+        cores = os.cpu_count() or 1
+        runs_cpu, iters_cpu = cores * 4, 100
+        it_cpu, dt_cpu = cpu_oracle_leg(inst, cfg, start, runs_cpu, iters_cpu, cores)
+        cpu = {"value": it_cpu * VM / dt_cpu, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{runs_cpu} runs x {iters_cpu} TS iterations (seeds 1..{runs_cpu}, kick {cfg.kick}) of the same instance"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"C3 batched: {R} tabu runs/GPU of a {inst.n_vehicles}-vehicle/"
+                                   f"{inst.n_missions}-mission instance, {iters} iters, tenure {cfg.tenure}, kick {cfg.kick}",
+                       "runs_per_gpu": R, "iters_per_run": iters, "valid_moves_per_iter": VM,
+                       "instance_seed": inst.seed, "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"runs sharded over {world} GPU(s)"},
+            "tabu_iters_per_s": iters_all / (t_ms / 1e3),
+            "best_objective_s": gbest >> 20,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
+            "step_ms": step_ms}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--workload", default="batched")
+    ap.add_argument("--runs", type=int, default=0)
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-runs-per-core", type=int, default=2)
+    ap.add_argument("--ref-iters", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None, help="dram bytes/launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

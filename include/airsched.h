@@ -1,0 +1,219 @@
+/*
+ * airsched.h -- C ABI of the B200-native move-evaluation and selection engine
+ * for arXiv 2002.11710 ("air-EMS fleet scheduling": neighbourhood search and
+ * tabu search over mission-to-vehicle routes).
+ *
+ * Citations: "P:n" = line n of the paper's text (/root/reference/PAPER.md,
+ * not needed at run time); "reading #k" = DESIGN.md's ambiguity ledger.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns as_status; outputs are written only on AS_OK.  No C++
+ *    exception crosses the ABI.  as_last_error() returns a thread-local message
+ *    for the last non-OK status of the calling thread.
+ *  - Inputs are copied; the caller keeps its buffers.  Handles are destroyed
+ *    explicitly by the caller.
+ *  - Array arguments marked "(host or device)" may point to host memory or to
+ *    device memory of the context's device (for example a torch CUDA tensor's
+ *    data_ptr()); the library classifies them with cudaPointerGetAttributes.
+ *    Host outputs are complete when the call returns; a call whose array
+ *    outputs are all device pointers only enqueues work on the context's
+ *    stream (callers synchronise the stream themselves).
+ *  - Schedules cross the boundary in CSR form: route_ptr[V+1] (route_ptr[0] =
+ *    0, non-decreasing) and route_missions[route_ptr[V]], vehicle v flying
+ *    route_missions[route_ptr[v] .. route_ptr[v+1]) in order, base -> missions
+ *    -> the same base (Alg. 1 line 5 "Solution" matrix).
+ *  - Integer seconds everywhere; objective values are int64 seconds.
+ */
+#ifndef AIRSCHED_H
+#define AIRSCHED_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AS_OK = 0,
+    AS_ERR_INVALID_ARG = 1,      /* bad sizes, indices, ranges, null pointers */
+    AS_ERR_INFEASIBLE_START = 2, /* start schedule violates con6-con9 */
+    AS_ERR_INIT_FAILED = 3,      /* Alg. 1 found no schedule (O13) */
+    AS_ERR_DEVICE = 4,           /* CUDA error (message in as_last_error) */
+    AS_ERR_OOM = 5,              /* device allocation failed */
+    AS_ERR_COMM = 6,             /* NCCL error */
+    AS_ERR_UNSUPPORTED = 7       /* size outside what this build's kernels handle */
+} as_status;
+
+typedef struct as_instance as_instance; /* immutable after create; thread-safe */
+typedef struct as_ctx as_ctx;           /* one device + one CUDA stream; single-threaded */
+typedef struct as_comm as_comm;         /* NCCL communicator (multi-GPU); may be NULL */
+
+/* ---------------------------------------------------------------- instance --
+ * The paper's problem statement (§3): bases with a vehicle class
+ * and location, missions <pickup, delivery, rho> with a
+ * deadline w_n, the flight limit p and the 24 h return limit
+ * (P:148).  Travel times are an input matrix of integer seconds per class
+ * (the paper's d built from Eq. e1; BASELINE north_star).  Several
+ * vehicles may share a base (reading #12).  All arrays are host memory and
+ * are copied.
+ */
+typedef struct {
+    int32_t n_locations;            /* NL >= 1: facilities and base sites */
+    int32_t n_classes;              /* NC in [1, 4]: matrix layers l (paper: 2) */
+    const int32_t *travel_s;        /* [NC][NL][NL] row-major, 0 <= T < 2^26, T[c][a][a] == 0 */
+    const uint8_t *class_is_heli;   /* [NC] 1 = helicopter class (may serve rho=1 missions, con9) */
+    int32_t n_bases;                /* >= 1 */
+    const int32_t *base_location;   /* [n_bases] in [0, NL) */
+    int32_t n_vehicles;             /* V >= 1 */
+    const int32_t *vehicle_base;    /* [V] in [0, n_bases) */
+    const int32_t *vehicle_class;   /* [V] in [0, NC)  (l = b_k) */
+    int32_t n_missions;             /* n >= 0 */
+    const int32_t *pickup_loc;      /* [n] in [0, NL) */
+    const int32_t *delivery_loc;    /* [n] in [0, NL) */
+    const int32_t *deadline_s;      /* [n] w_n in [1, day_length_s] */
+    const uint8_t *heli_only;       /* [n] rho: 1 = helicopter required */
+    int32_t flight_limit_s;         /* p > 0 (36000 = 10 h) */
+    int32_t day_length_s;           /* >= flight_limit_s (86400) */
+} as_instance_desc;
+
+/* Validates and copies desc (AS_ERR_INVALID_ARG names the violated rule).
+ * Limits: n + V < 2^20, the move-space size n(n+V)+n^2 < 2^32 - 1. */
+as_status as_instance_create(const as_instance_desc *desc, as_instance **out);
+void as_instance_destroy(as_instance *inst);
+
+/* Canonical move space (O5): relocate block
+ * idx = m*(n+V) + t (remove mission m, insert it before mission t, or at the
+ * end of route t-n for t >= n), then swap block idx = n(n+V) + m1*n + m2. */
+int64_t as_move_space_size(const as_instance *inst);
+/* Valid indices per iteration for a complete schedule with every move kind
+ * enabled: n(n+V-2) + n(n-1)/2 (state-independent). */
+int64_t as_valid_moves_per_iter(const as_instance *inst);
+
+/* Host-side check of a complete or partial CSR schedule against the model
+ * (Eq. obj_s, con1-con9).  feasible: 1 iff complete and feasible.  objective:
+ * total flight seconds (Eq. obj_s).  Pointers: host. */
+as_status as_schedule_check(const as_instance *inst, const int32_t *route_ptr, const int32_t *route_missions,
+                            int32_t *feasible, int64_t *objective);
+
+/* ----------------------------------------------------------------- context --
+ * device: CUDA ordinal.  cuda_stream: a cudaStream_t (e.g. torch's current
+ * stream); NULL = the legacy default stream. */
+as_status as_ctx_create(int32_t device, void *cuda_stream, as_ctx **out);
+as_status as_ctx_set_stream(as_ctx *ctx, void *cuda_stream);
+void as_ctx_destroy(as_ctx *ctx);
+/* Upload (and cache on ctx) the instance's device copy.  Optional: every call
+ * below uploads on first use; call this to keep the upload out of a timed
+ * region. */
+as_status as_instance_upload(as_ctx *ctx, const as_instance *inst);
+
+/* ------------------------------------------------------- Algorithm 1 (O13) --
+ * Greedy initialisation: helicopter-only missions first, each
+ * phase by ascending (deadline, id); the vehicle with the smallest cost
+ * increase wins (ties: lower id); insert_mode 0 = TAIL (route end, reading
+ * #23), 1 = SORTED (deadline-sorted slot).  When no vehicle fits, one
+ * neighbourhood-search iteration runs on the device over the assigned missions
+ * and the mission is retried once (reading #22).
+ * Outputs (host or device): route_ptr_out[V+1], route_missions_out[n]. */
+as_status as_init_greedy(as_ctx *ctx, const as_instance *inst, int32_t insert_mode, int32_t max_repairs,
+                         int32_t *route_ptr_out, int32_t *route_missions_out, int32_t *n_repairs_out);
+
+/* ----------------------------------------------------------- evaluation --- */
+enum { AS_MODE_NS = 0, AS_MODE_TABU = 1 };
+enum { AS_FLAG_VALID = 1, AS_FLAG_FEASIBLE = 2, AS_FLAG_TABU = 4, AS_FLAG_ADMISSIBLE = 8,
+       AS_FLAG_BYDEFAULT = 16 };
+enum { AS_MOVE_INTER_RELOCATE = 1, AS_MOVE_INTRA_RELOCATE = 2, AS_MOVE_INTER_SWAP = 4,
+       AS_MOVE_INTRA_SWAP = 8, AS_MOVE_ALL = 15 };
+
+/* Selection key of a move (O9): (class << 63) | ((delta + 2^30) << 32) | idx,
+ * class 0 = admissible, 1 = feasible but not admissible (by-default);
+ * AS_KEY_NONE = invalid or infeasible.  The minimum key is the selected move:
+ * smallest delta, ties to the lowest index (reading #26). */
+#define AS_KEY_NONE 0xFFFFFFFFFFFFFFFFull
+
+/* Score every canonical index of one schedule: delta (Eq. obj_s difference,
+ * defined for every valid index), FEASIBLE (con6-con9 of the moved schedule),
+ * TABU (some (mission, vehicle) the move places into has tabu_expiry >= iter),
+ * ADMISSIBLE (TS: feasible and (not tabu or cur+delta < best_obj);
+ * NS: feasible and delta < 0), BYDEFAULT (feasible, not admissible).
+ * Invalid indices get delta 0, flags 0.  The schedule (host) must be feasible
+ * (AS_ERR_INFEASIBLE_START otherwise); it may be partial (unlisted missions
+ * are unassigned; every move touching them is invalid).
+ * tabu_expiry: [n][V] int32 (host or device) or NULL (nothing tabu).
+ * delta_out [N] int32, flags_out [N] uint8 (host or device, nullable),
+ * best_key_out (host, nullable).  N = as_move_space_size. */
+as_status as_eval_moves(as_ctx *ctx, const as_instance *inst, const int32_t *route_ptr,
+                        const int32_t *route_missions, int32_t mode, const int32_t *tabu_expiry, int32_t iter,
+                        int64_t best_obj, uint32_t move_mask, int32_t *delta_out, uint8_t *flags_out,
+                        uint64_t *best_key_out);
+
+/* --------------------------------------------------------------- search --- */
+typedef struct {
+    int32_t mode;             /* AS_MODE_NS (Alg. 2) or AS_MODE_TABU (Alg. 3) */
+    int32_t tenure;           /* TabuCounter: a move applied at it is tabu during it+1..it+tenure */
+    int32_t max_iters;        /* iterations (one iteration = full neighbourhood + one applied move) */
+    int32_t kick;             /* relocates of the seeded kick (O12); used when seed != 0 */
+    uint32_t move_mask;       /* AS_MOVE_* bits; AS_MOVE_INTER_RELOCATE alone = the paper's move set */
+    int32_t strict_tabu_stop; /* TS: stop (reason 2) instead of the by-default move */
+    int32_t trace_level;      /* 0 none, 1 per-iteration records, 2 + tabu-list digest */
+    uint64_t seed;            /* run seed; 0 = start unchanged */
+} as_run_params;
+
+enum { AS_STOP_MAX_ITERS = 0, AS_STOP_LOCAL_OPT = 1, AS_STOP_NO_MOVE = 2, AS_STOP_INFEASIBLE_START = 3 };
+
+typedef struct {
+    int64_t best_obj, final_obj, start_obj;
+    int32_t best_iter;        /* -1 if the start was never improved */
+    int32_t iters_done, stop_reason, kicks_applied;
+} as_run_result;              /* 40 bytes */
+
+typedef struct {
+    int64_t cur, best;        /* objective after the move; best so far */
+    uint32_t idx;             /* applied canonical move index */
+    int32_t delta;
+    int32_t cls;              /* 0 admissible, 1 by-default */
+    int32_t it;
+} as_trace_rec;               /* 32 bytes */
+
+/* One NS/TS run (O10/O11) from a complete feasible start (host).  Outputs:
+ * result (host), best schedule CSR (host or device, nullable), trace
+ * [max_iters] (host or device, nullable, trace_level >= 1), digest [max_iters]
+ * FNV-1a-64 of the tabu list after each iteration (trace_level 2), tabu_out
+ * [n][V] final expiry matrix (nullable).  comm: NULL = one GPU. */
+as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, const int32_t *start_ptr,
+                      const int32_t *start_missions, const as_run_params *params, as_run_result *result,
+                      int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out,
+                      uint64_t *digest_out, int32_t *tabu_out);
+/* as_tabu_run with params->mode forced to AS_MODE_NS (Alg. 2). */
+as_status as_nbhd_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, const int32_t *start_ptr,
+                      const int32_t *start_missions, const as_run_params *params, as_run_result *result,
+                      int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out);
+
+/* n_runs independent runs of one instance (multi-start), one after its own
+ * seeded kick (seeds[r]; params->seed is ignored).  Starts (host or device):
+ * start_ptr [n_runs][V+1], start_missions [n_runs][n], or a single shared
+ * start when shared_start != 0.  Outputs (host or device, nullable):
+ * results [n_runs], best_ptr_out [n_runs][V+1], best_missions_out
+ * [n_runs][n], trace_out [n_runs][max_iters] (trace_level >= 1).
+ * best_run_out (host, nullable): run with the smallest (best_obj, run) over
+ * all ranks of comm.  A run whose start is infeasible reports stop_reason
+ * AS_STOP_INFEASIBLE_START; the call still succeeds. */
+as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, int32_t n_runs,
+                       const int32_t *start_ptr, const int32_t *start_missions, int32_t shared_start,
+                       const as_run_params *params, const uint64_t *seeds, as_run_result *results,
+                       int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out,
+                       int64_t *best_run_out);
+
+/* Device time of the last search/eval call's kernels on ctx's stream (ms),
+ * measured with CUDA events around the launches. */
+float as_ctx_last_kernel_ms(const as_ctx *ctx);
+/* Number of kernels the library launched on ctx since creation. */
+int64_t as_ctx_kernel_launches(const as_ctx *ctx);
+
+const char *as_last_error(void);
+const char *as_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -159,6 +159,18 @@ class Oracle:
                             int(bool(full)), _p(delta), _p(flags), C.byref(bc), C.byref(bd), C.byref(bi))
         return delta, flags, (bc.value, bd.value, bi.value)
 
+    def eval_indices(self, ptr, ms, idx, mode=MODE_TABU, E=None, it=0, best_obj=None, mask=0xF):
+        length, r = self.to_lists(ptr, ms)
+        idx = np.ascontiguousarray(idx, np.int64)
+        delta = np.zeros(len(idx), np.int32)
+        flags = np.zeros(len(idx), np.uint8)
+        if best_obj is None:
+            best_obj = self.objective(ptr, ms)
+        Ec = None if E is None else np.ascontiguousarray(E, np.int32)
+        lib().or_eval_index_list(self.ref, _p(length), _p(r), int(mode), _p(Ec), int(it), C.c_int64(int(best_obj)),
+                                 C.c_uint32(int(mask)), C.c_int64(len(idx)), _p(idx), _p(delta), _p(flags))
+        return delta, flags
+
     # ---- O10-O12 ---------------------------------------------------------------
     def search(self, ptr, ms, mode=MODE_TABU, tenure=10, max_iters=100, seed=0, kick=0, mask=0xF,
                strict_tabu_stop=False, digest=False, trace=True):

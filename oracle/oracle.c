@@ -380,6 +380,37 @@ void or_eval_moves(const or_inst *I, const int32_t *len, const int32_t *r, int32
     evalctx_free(&X);
 }
 
+/* The same per-index values for a list of indices (large instances, sampled). */
+void or_eval_index_list(const or_inst *I, const int32_t *len, const int32_t *r, int32_t mode, const int32_t *E,
+                        int32_t it, int64_t best_obj, uint32_t mask, int64_t count, const int64_t *idx,
+                        int32_t *delta_out, uint8_t *flags_out) {
+    evalctx X;
+    evalctx_init(&X, I, len, r);
+    for (int64_t k = 0; k < count; k++) {
+        move_t mv;
+        int64_t delta = 0;
+        int32_t feas = 0;
+        uint8_t flags = 0;
+        if (eval_one(&X, len, r, idx[k], mask, 0, &mv, &delta, &feas)) {
+            int32_t admissible;
+            flags |= OR_FLAG_VALID;
+            if (feas) flags |= OR_FLAG_FEASIBLE;
+            if (mode == OR_MODE_TABU) {
+                int32_t tabu = is_tabu(I, &mv, E, it);
+                if (tabu) flags |= OR_FLAG_TABU;
+                admissible = feas && (!tabu || X.cur + delta < best_obj);
+            } else {
+                admissible = feas && delta < 0;
+            }
+            if (admissible) flags |= OR_FLAG_ADMISSIBLE;
+            else if (feas) flags |= OR_FLAG_BYDEFAULT;
+        }
+        delta_out[k] = (int32_t)delta;
+        flags_out[k] = flags;
+    }
+    evalctx_free(&X);
+}
+
 /* ------------------------------------------------------------------ O12 -- */
 /* SplitMix64 (Steele, Lea & Flood 2014) -- the run seed's generator. */
 uint64_t or_splitmix64_next(uint64_t *state) {

@@ -66,6 +66,11 @@ void or_eval_moves(const or_inst *I, const int32_t *len, const int32_t *r, int32
                    int32_t *delta_out, uint8_t *flags_out,
                    int32_t *best_cls, int32_t *best_delta, int64_t *best_idx);
 
+/* or_eval_moves' per-index delta/flags for idx[0..count) only. */
+void or_eval_index_list(const or_inst *I, const int32_t *len, const int32_t *r, int32_t mode, const int32_t *E,
+                        int32_t it, int64_t best_obj, uint32_t mask, int64_t count, const int64_t *idx,
+                        int32_t *delta_out, uint8_t *flags_out);
+
 typedef struct {
     int32_t mode, tenure, max_iters, kick, strict_tabu_stop, want_digest;
     uint32_t mask;

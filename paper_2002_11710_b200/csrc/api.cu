@@ -1,0 +1,789 @@
+// api.cu -- the C ABI (include/airsched.h): validation, host<->device
+// marshalling, launch policy.  Every step of the search path runs in the
+// kernels of kernels.cu; host code here only validates inputs, copies buffers
+// and (for Alg. 1, as_init_greedy) makes the deadline-ordered placement
+// decisions, delegating its repair iteration to the device evaluator.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "airsched.h"
+#include "engine.cuh"
+#include "launch.h"
+
+using namespace airsched;
+
+static thread_local std::string g_err;
+
+static as_status fail(as_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            return fail(_e == cudaErrorMemoryAllocation ? AS_ERR_OOM : AS_ERR_DEVICE, "%s: %s (%s:%d)", \
+                        #expr, cudaGetErrorString(_e), __FILE__, __LINE__);                         \
+    } while (0)
+
+// ----------------------------------------------------------------- instance --
+struct as_instance {
+    uint64_t uid;
+    int32_t NL, NC, V, n, n_bases, P, DAY;
+    std::vector<int32_t> T, base_loc, vbase, vcls, vloc, pick, del, w;
+    std::vector<uint8_t> cls_heli, heli;
+};
+
+static uint64_t g_uid = 1;
+
+extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance **out) {
+    if (!d || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    const int64_t NL = d->n_locations, NC = d->n_classes, V = d->n_vehicles, n = d->n_missions, B = d->n_bases;
+    if (NL < 1 || NC < 1 || NC > 4) return fail(AS_ERR_INVALID_ARG, "need n_locations >= 1 and 1 <= n_classes <= 4");
+    if (V < 1 || B < 1 || n < 0) return fail(AS_ERR_INVALID_ARG, "need n_vehicles >= 1, n_bases >= 1, n_missions >= 0");
+    if (n + V >= (1 << 20)) return fail(AS_ERR_INVALID_ARG, "n + V must be < 2^20");
+    if (n * (n + V) + n * n >= 0xFFFFFFFFll) return fail(AS_ERR_INVALID_ARG, "move space must be < 2^32 - 1");
+    if (NC * NL * NL > (int64_t)1 << 31) return fail(AS_ERR_INVALID_ARG, "travel matrix too large");
+    if (!d->travel_s || !d->class_is_heli || !d->base_location || !d->vehicle_base || !d->vehicle_class)
+        return fail(AS_ERR_INVALID_ARG, "null array");
+    if (n > 0 && (!d->pickup_loc || !d->delivery_loc || !d->deadline_s || !d->heli_only))
+        return fail(AS_ERR_INVALID_ARG, "null mission array");
+    if (d->flight_limit_s <= 0 || d->day_length_s < d->flight_limit_s)
+        return fail(AS_ERR_INVALID_ARG, "need flight_limit_s > 0 and day_length_s >= flight_limit_s (SPEC S:117)");
+    std::unique_ptr<as_instance> I(new (std::nothrow) as_instance());
+    if (!I) return fail(AS_ERR_OOM, "host allocation");
+    I->NL = (int32_t)NL; I->NC = (int32_t)NC; I->V = (int32_t)V; I->n = (int32_t)n; I->n_bases = (int32_t)B;
+    I->P = d->flight_limit_s; I->DAY = d->day_length_s;
+    I->T.assign(d->travel_s, d->travel_s + NC * NL * NL);
+    for (int64_t c = 0; c < NC; c++)
+        for (int64_t a = 0; a < NL; a++)
+            for (int64_t b = 0; b < NL; b++) {
+                int32_t t = I->T[(c * NL + a) * NL + b];
+                if (t < 0 || t >= (1 << 26)) return fail(AS_ERR_INVALID_ARG, "travel_s[%lld][%lld][%lld] = %d outside [0, 2^26)", (long long)c, (long long)a, (long long)b, t);
+                if (a == b && t != 0) return fail(AS_ERR_INVALID_ARG, "travel_s diagonal must be 0 (S:35)");
+            }
+    I->cls_heli.assign(d->class_is_heli, d->class_is_heli + NC);
+    I->base_loc.assign(d->base_location, d->base_location + B);
+    for (auto x : I->base_loc)
+        if (x < 0 || x >= NL) return fail(AS_ERR_INVALID_ARG, "base_location out of range");
+    I->vbase.assign(d->vehicle_base, d->vehicle_base + V);
+    I->vcls.assign(d->vehicle_class, d->vehicle_class + V);
+    I->vloc.resize(V);
+    for (int64_t v = 0; v < V; v++) {
+        if (I->vbase[v] < 0 || I->vbase[v] >= B) return fail(AS_ERR_INVALID_ARG, "vehicle_base[%lld] out of range", (long long)v);
+        if (I->vcls[v] < 0 || I->vcls[v] >= NC) return fail(AS_ERR_INVALID_ARG, "vehicle_class[%lld] out of range", (long long)v);
+        I->vloc[v] = I->base_loc[I->vbase[v]];
+    }
+    if (n > 0) {
+        I->pick.assign(d->pickup_loc, d->pickup_loc + n);
+        I->del.assign(d->delivery_loc, d->delivery_loc + n);
+        I->w.assign(d->deadline_s, d->deadline_s + n);
+        I->heli.assign(d->heli_only, d->heli_only + n);
+    }
+    for (int64_t m = 0; m < n; m++) {
+        if (I->pick[m] < 0 || I->pick[m] >= NL || I->del[m] < 0 || I->del[m] >= NL)
+            return fail(AS_ERR_INVALID_ARG, "mission %lld location out of range", (long long)m);
+        if (I->w[m] < 1 || I->w[m] > d->day_length_s)
+            return fail(AS_ERR_INVALID_ARG, "deadline of mission %lld outside [1, day_length] (S:111)", (long long)m);
+        if (I->heli[m] > 1) return fail(AS_ERR_INVALID_ARG, "heli_only must be 0/1");
+    }
+    I->uid = __atomic_fetch_add(&g_uid, 1, __ATOMIC_RELAXED);
+    *out = I.release();
+    return AS_OK;
+}
+
+extern "C" void as_instance_destroy(as_instance *inst) { delete inst; }
+
+extern "C" int64_t as_move_space_size(const as_instance *I) {
+    if (!I) return -1;
+    int64_t n = I->n, V = I->V;
+    return n * (n + V) + n * n;
+}
+
+extern "C" int64_t as_valid_moves_per_iter(const as_instance *I) {
+    if (!I) return -1;
+    int64_t n = I->n, V = I->V;
+    return n > 0 ? n * (n + V - 2) + n * (n - 1) / 2 : 0;
+}
+
+// Host view of a CSR schedule: per-vehicle mission lists.
+struct HostSched {
+    std::vector<std::vector<int32_t>> routes;
+};
+
+static as_status parse_csr(const as_instance *I, const int32_t *ptr, const int32_t *ms, bool allow_partial,
+                           HostSched &S) {
+    if (!ptr) return fail(AS_ERR_INVALID_ARG, "null route_ptr");
+    if (ptr[0] != 0) return fail(AS_ERR_INVALID_ARG, "route_ptr[0] must be 0");
+    int32_t total = ptr[I->V];
+    if (total < 0 || total > I->n) return fail(AS_ERR_INVALID_ARG, "route_ptr[V] out of range");
+    if (!allow_partial && total != I->n) return fail(AS_ERR_INVALID_ARG, "schedule must list every mission once");
+    if (total > 0 && !ms) return fail(AS_ERR_INVALID_ARG, "null route_missions");
+    std::vector<char> seen(I->n, 0);
+    S.routes.assign(I->V, {});
+    for (int v = 0; v < I->V; v++) {
+        if (ptr[v + 1] < ptr[v]) return fail(AS_ERR_INVALID_ARG, "route_ptr must be non-decreasing");
+        for (int i = ptr[v]; i < ptr[v + 1]; i++) {
+            int32_t m = ms[i];
+            if (m < 0 || m >= I->n) return fail(AS_ERR_INVALID_ARG, "mission id %d out of range", m);
+            if (seen[m]) return fail(AS_ERR_INVALID_ARG, "mission %d listed twice (con1/con2)", m);
+            seen[m] = 1;
+            S.routes[v].push_back(m);
+        }
+    }
+    return AS_OK;
+}
+
+// Host arithmetic for validation and Alg. 1 placement (not the search path).
+static inline int64_t hT(const as_instance *I, int c, int a, int b) {
+    return I->T[((int64_t)c * I->NL + a) * I->NL + b];
+}
+static inline int32_t h_end(const as_instance *I, int v, int x) { return x >= 0 ? I->del[x] : I->vloc[v]; }
+static inline int64_t h_dm(const as_instance *I, int v, int x, int m) {   // d(x -> mission m), class of v
+    int c = I->vcls[v];
+    return hT(I, c, h_end(I, v, x), I->pick[m]) + hT(I, c, I->pick[m], I->del[m]);
+}
+static inline int64_t h_db(const as_instance *I, int v, int x) { return hT(I, I->vcls[v], h_end(I, v, x), I->vloc[v]); }
+
+static void route_eval(const as_instance *I, int v, const std::vector<int32_t> &r, int64_t *cost, bool *feas) {
+    if (r.empty()) { *cost = 0; *feas = true; return; }
+    int64_t c = 0, dep = 0;
+    bool ok = true;
+    int prev = -1;
+    for (int32_t m : r) {
+        int64_t d = h_dm(I, v, prev, m);
+        if (dep + d > I->w[m]) ok = false;
+        if (I->heli[m] && !I->cls_heli[I->vcls[v]]) ok = false;
+        c += d;
+        dep = I->w[m];
+        prev = m;
+    }
+    int64_t d = h_db(I, v, prev);
+    if (dep + d > I->DAY) ok = false;
+    c += d;
+    if (c > I->P) ok = false;
+    *cost = c;
+    *feas = ok;
+}
+
+extern "C" as_status as_schedule_check(const as_instance *I, const int32_t *ptr, const int32_t *ms, int32_t *feasible,
+                                       int64_t *objective) {
+    if (!I) return fail(AS_ERR_INVALID_ARG, "null instance");
+    HostSched S;
+    as_status st = parse_csr(I, ptr, ms, true, S);
+    if (st != AS_OK) return st;
+    int64_t total = 0;
+    bool ok = ptr[I->V] == I->n;
+    for (int v = 0; v < I->V; v++) {
+        int64_t c;
+        bool f;
+        route_eval(I, v, S.routes[v], &c, &f);
+        total += c;
+        ok = ok && f;
+    }
+    if (feasible) *feasible = ok ? 1 : 0;
+    if (objective) *objective = total;
+    return AS_OK;
+}
+
+// ------------------------------------------------------------------ context --
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+struct InstDev {
+    uint64_t uid = 0;
+    DevInst d{};
+    std::vector<void *> allocs;
+};
+
+struct as_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int n_sm = 148;
+    size_t max_smem = 0;
+    std::map<const as_instance *, InstDev> insts;
+    std::map<std::string, DevBuf> scratch;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;
+    float last_ms = 0.f;
+    int64_t launches = 0;
+};
+
+struct as_comm {
+    int nranks = 1, rank = 0;
+};
+
+static as_status set_device(as_ctx *ctx) {
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    return AS_OK;
+}
+
+extern "C" as_status as_ctx_create(int32_t device, void *stream, as_ctx **out) {
+    if (!out) return fail(AS_ERR_INVALID_ARG, "null out");
+    int count = 0;
+    CUDA_TRY(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(AS_ERR_INVALID_ARG, "device %d not present (%d devices)", device, count);
+    std::unique_ptr<as_ctx> c(new as_ctx());
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(AS_ERR_DEVICE, "this build targets sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
+    c->n_sm = prop.multiProcessorCount;
+    c->max_smem = prop.sharedMemPerBlockOptin;
+    CUDA_TRY(cudaEventCreate(&c->ev0));
+    CUDA_TRY(cudaEventCreate(&c->ev1));
+    *out = c.release();
+    return AS_OK;
+}
+
+extern "C" as_status as_ctx_set_stream(as_ctx *ctx, void *stream) {
+    if (!ctx) return fail(AS_ERR_INVALID_ARG, "null ctx");
+    ctx->stream = (cudaStream_t)stream;
+    return AS_OK;
+}
+
+extern "C" void as_ctx_destroy(as_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &kv : ctx->insts)
+        for (void *p : kv.second.allocs) cudaFree(p);
+    for (auto &kv : ctx->scratch) cudaFree(kv.second.p);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    delete ctx;
+}
+
+extern "C" float as_ctx_last_kernel_ms(const as_ctx *ctx) {
+    if (!ctx || !ctx->timed) return -1.f;
+    as_ctx *c = const_cast<as_ctx *>(ctx);
+    if (cudaEventSynchronize(c->ev1) != cudaSuccess) return -1.f;
+    float ms = -1.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    return ms;
+}
+
+extern "C" int64_t as_ctx_kernel_launches(const as_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
+static as_status scratch(as_ctx *ctx, const char *name, size_t bytes, void **out) {
+    DevBuf &b = ctx->scratch[name];
+    if (b.cap < bytes) {
+        if (b.p) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(b.p);
+            b.p = nullptr;
+            b.cap = 0;
+        }
+        size_t cap = std::max<size_t>(bytes, 256);
+        CUDA_TRY(cudaMalloc(&b.p, cap));
+        b.cap = cap;
+    }
+    *out = b.p;
+    return AS_OK;
+}
+
+template <class Tp>
+static as_status dev_copy(InstDev &D, const std::vector<Tp> &v, const Tp **out, cudaStream_t st) {
+    void *p = nullptr;
+    size_t bytes = std::max<size_t>(v.size() * sizeof(Tp), 16);
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    D.allocs.push_back(p);
+    if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(Tp), cudaMemcpyHostToDevice, st));
+    *out = (const Tp *)p;
+    return AS_OK;
+}
+
+static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst **out) {
+    auto it = ctx->insts.find(I);
+    if (it != ctx->insts.end() && it->second.uid == I->uid) {
+        *out = &it->second.d;
+        return AS_OK;
+    }
+    if (it != ctx->insts.end()) {
+        for (void *p : it->second.allocs) cudaFree(p);
+        ctx->insts.erase(it);
+    }
+    InstDev D;
+    D.uid = I->uid;
+    as_status st;
+    cudaStream_t s = ctx->stream;
+    if ((st = dev_copy(D, I->T, &D.d.T, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->vloc, &D.d.vloc, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->vcls, &D.d.vcls, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->cls_heli, &D.d.cls_heli, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->pick, &D.d.pick, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->del, &D.d.del, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->w, &D.d.w, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->heli, &D.d.heli, s)) != AS_OK) return st;
+    void *svc = nullptr;
+    CUDA_TRY(cudaMalloc(&svc, std::max<size_t>((size_t)I->NC * I->n * 4, 16)));
+    D.allocs.push_back(svc);
+    CUDA_TRY(launch_svc(D.d.T, D.d.pick, D.d.del, (int32_t *)svc, I->n, I->NL, I->NC, s));
+    ctx->launches += I->n > 0;
+    D.d.svc = (const int32_t *)svc;
+    D.d.n = I->n; D.d.V = I->V; D.d.NL = I->NL; D.d.NC = I->NC; D.d.P = I->P; D.d.DAY = I->DAY;
+    auto &slot = ctx->insts[I];
+    slot = std::move(D);
+    *out = &slot.d;
+    return AS_OK;
+}
+
+extern "C" as_status as_instance_upload(as_ctx *ctx, const as_instance *I) {
+    if (!ctx || !I) return fail(AS_ERR_INVALID_ARG, "null argument");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const DevInst *d;
+    return get_dev_inst(ctx, I, &d);
+}
+
+// Pointer classification: device memory of any kind counts as "device".
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Input array -> device pointer (copies host arrays into named scratch).
+static as_status dev_in(as_ctx *ctx, const char *name, const void *p, size_t bytes, const void **out) {
+    if (!p || is_device_ptr(p)) {
+        *out = p;
+        return AS_OK;
+    }
+    void *d;
+    as_status st = scratch(ctx, name, bytes, &d);
+    if (st != AS_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *out = d;
+    return AS_OK;
+}
+
+// Output array: device pointer to write into; *host_dst set when a D2H copy is needed.
+struct OutBuf {
+    void *dev = nullptr;
+    void *host = nullptr;
+    size_t bytes = 0;
+};
+static as_status dev_out(as_ctx *ctx, const char *name, void *p, size_t bytes, OutBuf &o) {
+    o.bytes = bytes;
+    if (!p) return AS_OK;
+    if (is_device_ptr(p)) {
+        o.dev = p;
+        return AS_OK;
+    }
+    as_status st = scratch(ctx, name, bytes, &o.dev);
+    if (st != AS_OK) return st;
+    o.host = p;
+    return AS_OK;
+}
+static as_status finish_out(as_ctx *ctx, std::initializer_list<OutBuf *> outs) {
+    bool any = false;
+    for (OutBuf *o : outs)
+        if (o->host && o->bytes) {
+            CUDA_TRY(cudaMemcpyAsync(o->host, o->dev, o->bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            any = true;
+        }
+    if (any) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return AS_OK;
+}
+
+// ------------------------------------------------------------ eval (dump) ---
+struct GState {
+    RunViewG g;
+};
+
+static as_status alloc_gstate(as_ctx *ctx, const as_instance *I, bool with_E, RunViewG &G) {
+    const size_t S = (size_t)I->n + I->V;
+    void *p;
+    size_t words = 10 * S + (size_t)I->V + (with_E ? (size_t)I->n * I->V : 0) + 16;
+    as_status st = scratch(ctx, "gstate", words * 4, &p);
+    if (st != AS_OK) return st;
+    int32_t *b = (int32_t *)p;
+    G.succ = b; b += S;
+    G.pred = b; b += S;
+    G.veh = b; b += S;
+    G.endc = b; b += S;
+    G.depc = b; b += S;
+    G.inc = b; b += S;
+    G.svco = b; b += S;
+    G.pick_s = b; b += S;
+    G.w_s = b; b += S;
+    G.F = b; b += I->V;
+    G.E = with_E ? b : nullptr;
+    return AS_OK;
+}
+
+// Internal eval used by as_eval_moves and the greedy repair.
+static as_status eval_core(as_ctx *ctx, const as_instance *I, const DevInst *D, const HostSched &S, int mode,
+                           const int32_t *tabu_expiry, int it, int64_t cur, int64_t best, uint32_t mask,
+                           int32_t *delta_out, uint8_t *flags_out, uint64_t *best_key) {
+    std::vector<int32_t> ptr(I->V + 1, 0), ms;
+    for (int v = 0; v < I->V; v++) {
+        ms.insert(ms.end(), S.routes[v].begin(), S.routes[v].end());
+        ptr[v + 1] = (int32_t)ms.size();
+    }
+    const void *dptr, *dms;
+    as_status st;
+    if ((st = dev_in(ctx, "eval_ptr", ptr.data(), ptr.size() * 4, &dptr)) != AS_OK) return st;
+    if ((st = dev_in(ctx, "eval_ms", ms.empty() ? nullptr : ms.data(), ms.size() * 4, &dms)) != AS_OK) return st;
+    RunViewG G;
+    bool tabu = mode == AS_MODE_TABU && tabu_expiry;
+    if ((st = alloc_gstate(ctx, I, tabu, G)) != AS_OK) return st;
+    if (tabu) {
+        const void *dE;
+        size_t eb = (size_t)I->n * I->V * 4;
+        if ((st = dev_in(ctx, "eval_E", tabu_expiry, eb, &dE)) != AS_OK) return st;
+        if (dE != G.E) CUDA_TRY(cudaMemcpyAsync(G.E, dE, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CUDA_TRY(launch_build_state(*D, (const int32_t *)dptr, (const int32_t *)dms, G, ctx->stream));
+    ctx->launches++;
+    const uint64_t N = (uint64_t)as_move_space_size(I);
+    OutBuf od, of, ok;
+    if ((st = dev_out(ctx, "eval_delta", delta_out, N * 4, od)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "eval_flags", flags_out, N, of)) != AS_OK) return st;
+    void *dkey;
+    if ((st = scratch(ctx, "eval_key", 8, &dkey)) != AS_OK) return st;
+    CUDA_TRY(cudaMemsetAsync(dkey, 0xFF, 8, ctx->stream));
+    if (!tabu) G.E = nullptr;
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    if (N > 0) {
+        CUDA_TRY(launch_eval_dump(*D, G, mode == AS_MODE_TABU ? 1 : 0, it, cur, best, mask, (int32_t *)od.dev,
+                                  (uint8_t *)of.dev, (unsigned long long *)dkey, N, ctx->n_sm, ctx->stream));
+        ctx->launches++;
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timed = true;
+    ok.dev = dkey;
+    ok.host = best_key;
+    ok.bytes = best_key ? 8 : 0;
+    return finish_out(ctx, {&od, &of, &ok});
+}
+
+extern "C" as_status as_eval_moves(as_ctx *ctx, const as_instance *I, const int32_t *ptr, const int32_t *ms,
+                                   int32_t mode, const int32_t *tabu_expiry, int32_t iter, int64_t best_obj,
+                                   uint32_t move_mask, int32_t *delta_out, uint8_t *flags_out, uint64_t *best_key_out) {
+    if (!ctx || !I) return fail(AS_ERR_INVALID_ARG, "null ctx/instance");
+    if (mode != AS_MODE_NS && mode != AS_MODE_TABU) return fail(AS_ERR_INVALID_ARG, "mode must be NS or TABU");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    HostSched S;
+    if ((st = parse_csr(I, ptr, ms, true, S)) != AS_OK) return st;
+    int64_t cur = 0;
+    for (int v = 0; v < I->V; v++) {
+        int64_t c;
+        bool f;
+        route_eval(I, v, S.routes[v], &c, &f);
+        if (!f) return fail(AS_ERR_INFEASIBLE_START, "route %d of the schedule is infeasible", v);
+        cur += c;
+    }
+    const DevInst *D;
+    if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+    return eval_core(ctx, I, D, S, mode, tabu_expiry, iter, cur, best_obj, move_mask, delta_out, flags_out,
+                     best_key_out);
+}
+
+// --------------------------------------------------------------- search -----
+static as_status pick_layout(as_ctx *ctx, const as_instance *I, bool tabu, int *T_smem, int *E_smem, size_t *smem) {
+    const size_t lim = ctx->max_smem;
+    const int n = I->n, V = I->V, NL = I->NL, NC = I->NC;
+    struct Opt { bool t, e; } opts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
+    for (auto o : opts) {
+        bool e = o.e && tabu;
+        size_t b = search_smem_bytes(n, V, NL, NC, o.t, e);
+        if (b <= lim) {
+            *T_smem = o.t;
+            *E_smem = e;
+            *smem = b;
+            return AS_OK;
+        }
+    }
+    return fail(AS_ERR_UNSUPPORTED, "instance too large for the per-CTA persistent kernel (n=%d, V=%d)", n, V);
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *s = getenv(name);
+    return s ? atoi(s) : dflt;
+}
+
+static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, const int32_t *start_ptr,
+                          const int32_t *start_ms, int32_t shared_start, const as_run_params *P,
+                          const uint64_t *seeds, as_run_result *results, int32_t *best_ptr, int32_t *best_ms,
+                          as_trace_rec *trace, uint64_t *digest, int32_t *tabu_out, bool single) {
+    if (!P) return fail(AS_ERR_INVALID_ARG, "null params");
+    if (P->mode != AS_MODE_NS && P->mode != AS_MODE_TABU) return fail(AS_ERR_INVALID_ARG, "mode must be NS or TABU");
+    if (P->max_iters < 0 || P->tenure < 0 || P->kick < 0) return fail(AS_ERR_INVALID_ARG, "negative parameter");
+    if (n_runs < 1) return fail(AS_ERR_INVALID_ARG, "n_runs must be >= 1");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const DevInst *D;
+    if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+    const bool tabu = P->mode == AS_MODE_TABU;
+    const int n = I->n, V = I->V;
+    int T_smem, E_smem;
+    size_t smem;
+    if ((st = pick_layout(ctx, I, tabu, &T_smem, &E_smem, &smem)) != AS_OK) return st;
+    const int force_T = env_int("AIRSCHED_T_SMEM", -1);
+    if (force_T == 0 && T_smem) {
+        T_smem = 0;
+        smem = search_smem_bytes(n, V, I->NL, I->NC, false, E_smem);
+    }
+    SearchArgs A;
+    memset(&A, 0, sizeof(A));
+    A.inst = *D;
+    const size_t nst = shared_start ? 1 : (size_t)n_runs;
+    const void *dp, *dm, *ds = nullptr;
+    if ((st = dev_in(ctx, "start_ptr", start_ptr, nst * (V + 1) * 4, &dp)) != AS_OK) return st;
+    if ((st = dev_in(ctx, "start_ms", start_ms, std::max<size_t>(nst * n * 4, 4), &dm)) != AS_OK) return st;
+    if (seeds && (st = dev_in(ctx, "seeds", seeds, (size_t)n_runs * 8, &ds)) != AS_OK) return st;
+    A.start_ptr = (const int32_t *)dp;
+    A.start_ms = (const int32_t *)dm;
+    A.shared_start = shared_start;
+    A.seeds = (const uint64_t *)ds;
+    A.seed = P->seed;
+    A.kick = P->kick;
+    A.tenure = P->tenure;
+    A.max_iters = P->max_iters;
+    A.strict_tabu_stop = P->strict_tabu_stop;
+    A.mask = P->move_mask;
+    A.T_smem = T_smem;
+    A.E_smem = E_smem;
+    if (tabu && !E_smem) {
+        void *e;
+        if ((st = scratch(ctx, "E_global", (size_t)n_runs * n * V * 4 + 4, &e)) != AS_OK) return st;
+        A.E_global = (int32_t *)e;
+    }
+    OutBuf o_res, o_bp, o_bm, o_tr, o_dg, o_tb;
+    as_run_result *res_dev_needed = results;
+    if ((st = dev_out(ctx, "o_res", res_dev_needed, (size_t)n_runs * sizeof(as_run_result), o_res)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_bp", best_ptr, (size_t)n_runs * (V + 1) * 4, o_bp)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_bm", best_ms, std::max<size_t>((size_t)n_runs * n * 4, 4), o_bm)) != AS_OK) return st;
+    const bool want_trace = trace && P->trace_level >= 1 && P->max_iters > 0;
+    const bool want_digest = digest && tabu && P->trace_level >= 2 && P->max_iters > 0;
+    if ((st = dev_out(ctx, "o_tr", want_trace ? trace : nullptr, (size_t)n_runs * P->max_iters * sizeof(as_trace_rec), o_tr)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_dg", want_digest ? digest : nullptr, (size_t)n_runs * P->max_iters * 8, o_dg)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_tb", tabu ? tabu_out : nullptr, std::max<size_t>((size_t)n_runs * n * V * 4, 4), o_tb)) != AS_OK) return st;
+    if (best_ptr && !best_ms && n > 0) return fail(AS_ERR_INVALID_ARG, "best_ptr_out needs best_missions_out");
+    A.results = (as_run_result *)o_res.dev;
+    A.best_ptr = (int32_t *)o_bp.dev;
+    A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
+    A.trace = (as_trace_rec *)o_tr.dev;
+    A.digest = (uint64_t *)o_dg.dev;
+    A.tabu_out = (int32_t *)o_tb.dev;
+    // single-result call: results struct is host memory and required
+    int threads;
+    const int64_t N = as_move_space_size(I);
+    if (single) {
+        int64_t t = 64;
+        while (t < 1024 && t * 16 < N) t *= 2;
+        threads = (int)t;
+    } else {
+        threads = 256;
+    }
+    threads = env_int("AIRSCHED_THREADS", threads);
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(launch_search(A, tabu ? 1 : 0, n_runs, threads, smem, ctx->stream));
+    ctx->launches++;
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timed = true;
+    return finish_out(ctx, {&o_res, &o_bp, &o_bm, &o_tr, &o_dg, &o_tb});
+}
+
+extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
+                                 const int32_t *start_ms, const as_run_params *P, as_run_result *result,
+                                 int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, uint64_t *digest,
+                                 int32_t *tabu_out) {
+    if (!ctx || !I || !P || !result) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (comm && comm->nranks > 1) return fail(AS_ERR_UNSUPPORTED, "sharded single-instance runs are not built yet");
+    HostSched S;
+    as_status st = parse_csr(I, start_ptr, start_ms, false, S);
+    if (st != AS_OK) return st;
+    int32_t feas;
+    int64_t obj;
+    as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
+    if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
+    st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, digest, tabu_out, true);
+    if (st != AS_OK) return st;
+    if (result->stop_reason == AS_STOP_INFEASIBLE_START)
+        return fail(AS_ERR_INFEASIBLE_START, "device rejected the start schedule");
+    return AS_OK;
+}
+
+extern "C" as_status as_nbhd_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
+                                 const int32_t *start_ms, const as_run_params *P, as_run_result *result,
+                                 int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace) {
+    if (!P) return fail(AS_ERR_INVALID_ARG, "null params");
+    as_run_params q = *P;
+    q.mode = AS_MODE_NS;
+    return as_tabu_run(ctx, comm, I, start_ptr, start_ms, &q, result, best_ptr, best_ms, trace, nullptr, nullptr);
+}
+
+extern "C" as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *I, int32_t n_runs,
+                                  const int32_t *start_ptr, const int32_t *start_ms, int32_t shared_start,
+                                  const as_run_params *P, const uint64_t *seeds, as_run_result *results,
+                                  int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int64_t *best_run_out) {
+    if (!ctx || !I || !P) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (!start_ptr) return fail(AS_ERR_INVALID_ARG, "null start");
+    (void)comm;
+    as_status st = run_core(ctx, I, n_runs, start_ptr, start_ms, shared_start, P, seeds, results, best_ptr, best_ms,
+                            trace, nullptr, nullptr, false);
+    if (st != AS_OK) return st;
+    if (best_run_out) {
+        // smallest (best_obj, run) among feasible runs; needs the results on the host
+        std::vector<as_run_result> h(n_runs);
+        const as_run_result *src = results;
+        if (!results) return fail(AS_ERR_INVALID_ARG, "best_run_out needs results");
+        if (is_device_ptr(results)) {
+            CUDA_TRY(cudaMemcpyAsync(h.data(), results, n_runs * sizeof(as_run_result), cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            src = h.data();
+        }
+        int64_t best = -1;
+        for (int r = 0; r < n_runs; r++) {
+            if (src[r].stop_reason == AS_STOP_INFEASIBLE_START) continue;
+            if (best < 0 || src[r].best_obj < src[best].best_obj) best = r;
+        }
+        *best_run_out = best;
+    }
+    return AS_OK;
+}
+
+// ------------------------------------------------------------ Algorithm 1 ---
+extern "C" as_status as_init_greedy(as_ctx *ctx, const as_instance *I, int32_t insert_mode, int32_t max_repairs,
+                                    int32_t *route_ptr_out, int32_t *route_missions_out, int32_t *n_repairs_out) {
+    if (!ctx || !I || !route_ptr_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (insert_mode != 0 && insert_mode != 1) return fail(AS_ERR_INVALID_ARG, "insert_mode must be 0 (TAIL) or 1 (SORTED)");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const int n = I->n, V = I->V;
+    std::vector<int32_t> order;
+    for (int phase = 0; phase < 2; phase++) {
+        std::vector<int32_t> ph;
+        for (int m = 0; m < n; m++)
+            if ((phase == 0) == (I->heli[m] != 0)) ph.push_back(m);
+        std::stable_sort(ph.begin(), ph.end(), [&](int a, int b) { return I->w[a] < I->w[b] || (I->w[a] == I->w[b] && a < b); });
+        order.insert(order.end(), ph.begin(), ph.end());
+    }
+    HostSched S;
+    S.routes.assign(V, {});
+    std::vector<int64_t> F(V, 0);
+    int repairs = 0, assigned = 0;
+    auto try_place = [&](int m, int *bv, int *bat, int64_t *binc) {
+        *bv = -1;
+        for (int v = 0; v < V; v++) {
+            if (I->heli[m] && !I->cls_heli[I->vcls[v]]) continue;              // con9 (lines 10-12)
+            const auto &r = S.routes[v];
+            int at = (int)r.size();
+            if (insert_mode == 1) {
+                at = 0;
+                while (at < (int)r.size() && I->w[r[at]] <= I->w[m]) at++;
+            }
+            int prev = at > 0 ? r[at - 1] : -1;
+            int next = at < (int)r.size() ? r[at] : -1;
+            int64_t dep_prev = prev >= 0 ? I->w[prev] : 0;
+            int64_t d_in = h_dm(I, v, prev, m);
+            int64_t d_out = next >= 0 ? h_dm(I, v, m, next) : h_db(I, v, m);
+            int64_t d_old = next >= 0 ? h_dm(I, v, prev, next) : h_db(I, v, prev);
+            int64_t w_next = next >= 0 ? I->w[next] : I->DAY;
+            if (dep_prev + d_in > I->w[m]) continue;                           // lines 13-20
+            if (I->w[m] + d_out > w_next) continue;                            // lines 21-28
+            int64_t inc = r.empty() ? d_in + d_out : d_in + d_out - d_old;
+            if (F[v] + inc > I->P) continue;                                   // lines 29-31
+            if (*bv < 0 || inc < *binc) { *bv = v; *bat = at; *binc = inc; }   // lines 32-34
+        }
+        return *bv >= 0;
+    };
+    for (int i = 0; i < n; i++) {
+        int m = order[i], bv, bat;
+        int64_t binc;
+        if (!try_place(m, &bv, &bat, &binc)) {
+            if (assigned == 0 || repairs >= max_repairs)
+                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: no vehicle can take mission %d (P:166)", m);
+            // repair: one NS iteration on the device over the assigned missions
+            const DevInst *D;
+            if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+            int64_t cur = 0;
+            for (int v = 0; v < V; v++) cur += F[v];
+            uint64_t key = AS_KEY_NONE;
+            if ((st = eval_core(ctx, I, D, S, AS_MODE_NS, nullptr, 0, cur, cur, AS_MOVE_ALL, nullptr, nullptr, &key)) != AS_OK)
+                return st;
+            if (key == AS_KEY_NONE || key_cls(key) != 0)
+                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: repair found no improving move for mission %d", m);
+            uint32_t idx = key_idx(key);
+            const uint32_t Sn = (uint32_t)(n + V), Rb = (uint32_t)n * Sn;
+            auto locate = [&](int x, int *vv, int *pp) {
+                for (int v = 0; v < V; v++)
+                    for (int p = 0; p < (int)S.routes[v].size(); p++)
+                        if (S.routes[v][p] == x) { *vv = v; *pp = p; return; }
+                *vv = -1; *pp = -1;
+            };
+            if (idx < Rb) {
+                int mm = idx / Sn, t = idx % Sn, a, pa;
+                locate(mm, &a, &pa);
+                S.routes[a].erase(S.routes[a].begin() + pa);
+                if (t < n) {
+                    int b, pb;
+                    locate(t, &b, &pb);
+                    S.routes[b].insert(S.routes[b].begin() + pb, mm);
+                } else {
+                    S.routes[t - n].push_back(mm);
+                }
+            } else {
+                int m1 = (idx - Rb) / n, m2 = (idx - Rb) % n, a, pa, b, pb;
+                locate(m1, &a, &pa);
+                locate(m2, &b, &pb);
+                S.routes[a][pa] = m2;
+                S.routes[b][pb] = m1;
+            }
+            for (int v = 0; v < V; v++) {
+                bool f;
+                route_eval(I, v, S.routes[v], &F[v], &f);
+            }
+            repairs++;
+            if (!try_place(m, &bv, &bat, &binc))
+                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: mission %d still unplaceable after repair", m);
+        }
+        S.routes[bv].insert(S.routes[bv].begin() + bat, m);
+        F[bv] += binc;
+        assigned++;
+    }
+    std::vector<int32_t> ptr(V + 1, 0), ms;
+    for (int v = 0; v < V; v++) {
+        ms.insert(ms.end(), S.routes[v].begin(), S.routes[v].end());
+        ptr[v + 1] = (int32_t)ms.size();
+    }
+    if (is_device_ptr(route_ptr_out)) CUDA_TRY(cudaMemcpy(route_ptr_out, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice));
+    else memcpy(route_ptr_out, ptr.data(), ptr.size() * 4);
+    if (n > 0) {
+        if (!route_missions_out) return fail(AS_ERR_INVALID_ARG, "null route_missions_out");
+        if (is_device_ptr(route_missions_out)) CUDA_TRY(cudaMemcpy(route_missions_out, ms.data(), ms.size() * 4, cudaMemcpyHostToDevice));
+        else memcpy(route_missions_out, ms.data(), ms.size() * 4);
+    }
+    if (n_repairs_out) *n_repairs_out = repairs;
+    return AS_OK;
+}
+
+extern "C" const char *as_last_error(void) { return g_err.c_str(); }
+extern "C" const char *as_version(void) { return "airsched-b200 0.1 (sm_100a)"; }

@@ -1,0 +1,500 @@
+// kernels.cu -- sm_100a kernels of the move-evaluation and selection engine.
+//
+//   k_eval_dump     : as_eval_moves -- one thread per canonical index, writes
+//                     delta/flags and reduces the selection key (parity tool).
+//   k_search<TABU>  : persistent NS/TS loop, one run per CTA (as_tabu_run,
+//                     as_nbhd_run, as_batch_run).  Per iteration: every warp
+//                     scores tiles of moves (relocate rows: m warp-uniform,
+//                     lanes stride the target slot; swap rows paired so every
+//                     warp sees n items), reduces the packed 64-bit key by
+//                     warp shuffle then through shared memory, and one thread
+//                     applies the winner -- no host round-trip per iteration.
+//
+// DESIGN.md describes the layout and the roofline of each kernel.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.cuh"
+#include "launch.h"
+
+namespace airsched {
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t u = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+// ----------------------------------------------------------------------------
+// State construction from CSR (shared by the dump path; the persistent kernel
+// does the same in its prologue).  One CTA.
+__global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, int32_t *succ, int32_t *pred,
+                              int32_t *veh, int32_t *endc, int32_t *depc, int32_t *inc, int32_t *svco,
+                              int32_t *pick_s, int32_t *w_s, int32_t *F) {
+    const int n = I.n, V = I.V, S = n + V;
+    for (int x = threadIdx.x; x < S; x += blockDim.x) {
+        if (x < n) {
+            veh[x] = -1;
+            succ[x] = x;
+            pred[x] = x;
+            pick_s[x] = I.pick[x];
+            w_s[x] = I.w[x];
+        } else {
+            int v = x - n;
+            veh[x] = v;
+            pick_s[x] = I.vloc[v];
+            w_s[x] = I.DAY;
+        }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        int prev = n + v;
+        for (int i = ptr[v]; i < ptr[v + 1]; i++) {
+            int m = ms[i];
+            veh[m] = v;
+            succ[prev] = m;
+            pred[m] = prev;
+            prev = m;
+        }
+        succ[prev] = n + v;
+        pred[n + v] = prev;
+    }
+    __syncthreads();
+    MissionView M;
+    M.del = I.del; M.heli = nullptr; M.svc = I.svc; M.vcls = I.vcls; M.vloc = I.vloc; M.clsheli = nullptr;
+    M.T = I.T; M.n = n; M.V = V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
+    RunView R;
+    R.succ = succ; R.pred = pred; R.veh = veh; R.endc = endc; R.depc = depc; R.inc = inc; R.svco = svco;
+    R.pick_s = pick_s; R.w_s = w_s; R.F = F; R.E = nullptr;
+    for (int x = threadIdx.x; x < S; x += blockDim.x) {
+        if (x < n && veh[x] < 0) { endc[x] = depc[x] = inc[x] = svco[x] = 0; continue; }
+        refresh_slot(M, R, x);
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        int f = 0;
+        int x = succ[n + v];
+        while (x < n) { f += inc[x]; x = succ[x]; }
+        f += inc[n + v];
+        F[v] = f;
+    }
+}
+
+// One thread per canonical index.  delta/flags nullable; best key via atomicMin.
+template <bool TABU>
+__global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long long best, uint32_t mask,
+                            int32_t *delta_out, uint8_t *flags_out, unsigned long long *best_key, uint64_t N) {
+    MissionView M;
+    M.del = I.del; M.svc = I.svc; M.vcls = I.vcls; M.vloc = I.vloc; M.T = I.T;
+    M.n = I.n; M.V = I.V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
+    extern __shared__ int32_t sh_small[];
+    // heli flags / class flags as int in smem (tiny)
+    int32_t *heli_s = sh_small;
+    int32_t *ch_s = sh_small + I.n;
+    for (int i = threadIdx.x; i < I.n; i += blockDim.x) heli_s[i] = I.heli[i];
+    for (int i = threadIdx.x; i < I.NC; i += blockDim.x) ch_s[i] = I.cls_heli[i];
+    __syncthreads();
+    M.heli = heli_s;
+    M.clsheli = ch_s;
+    RunView R;
+    R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
+    R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = TABU ? G.E : nullptr;
+    uint64_t kmin = KEY_NONE;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < N;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        MoveEval e = eval_index(M, R, (uint32_t)idx, mask, it);
+        uint8_t fl = 0;
+        int cls = move_class<TABU>(e, cur, best);
+        if (e.valid) {
+            fl |= 1;
+            if (e.feasible) fl |= 2;
+            if (e.tabu) fl |= 4;
+            if (cls == 0) fl |= 8;
+            if (cls == 1) fl |= 16;
+        }
+        if (delta_out) delta_out[idx] = e.valid ? e.delta : 0;
+        if (flags_out) flags_out[idx] = fl;
+        if (cls >= 0) {
+            uint64_t k = make_key(cls, e.delta, (uint32_t)idx);
+            kmin = k < kmin ? k : kmin;
+        }
+    }
+    kmin = warp_min_u64(kmin);
+    if ((threadIdx.x & 31) == 0 && kmin != KEY_NONE) atomicMin(best_key, (unsigned long long)kmin);
+}
+
+// ----------------------------------------------------------------------------
+// Persistent search kernel: one run per CTA.
+struct SmemLayout {
+    // offsets in int32 words
+    int T, del, heli, svc, vcls, vloc, clsheli;
+    int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc;
+    int red;      // 64-bit aligned, 32 x u64
+    int ctrl;     // control words
+    int total;    // words
+};
+
+__host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
+    SmemLayout L;
+    int o = 0;
+    const int S = n + V;
+    L.T = T_smem ? o : -1;
+    o += T_smem ? NC * NL * NL : 0;
+    L.del = o; o += n;
+    L.heli = o; o += n;
+    L.svc = o; o += NC * n;
+    L.vcls = o; o += V;
+    L.vloc = o; o += V;
+    L.clsheli = o; o += NC;
+    L.succ = o; o += S;
+    L.pred = o; o += S;
+    L.veh = o; o += S;
+    L.endc = o; o += S;
+    L.depc = o; o += S;
+    L.inc = o; o += S;
+    L.svco = o; o += S;
+    L.pick_s = o; o += S;
+    L.w_s = o; o += S;
+    L.F = o; o += V;
+    L.bsucc = o; o += S;
+    L.E = E_smem ? o : -1;
+    o += E_smem ? n * V : 0;
+    o = (o + 1) & ~1;
+    L.red = o; o += 2 * 32;
+    L.ctrl = o; o += 16;
+    L.total = o;
+    return L;
+}
+
+size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
+    return (size_t)make_layout(n, V, NL, NC, T_smem, E_smem).total * 4;
+}
+
+template <bool TABU>
+__global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
+    extern __shared__ __align__(16) int32_t sm[];
+    const DevInst &I = A.inst;
+    const int n = I.n, V = I.V, S = n + V, NC = I.NC;
+    const int run = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const SmemLayout L = make_layout(n, V, I.NL, NC, A.T_smem, A.E_smem);
+
+    // ---- stage instance constants -----------------------------------------
+    if (A.T_smem) {
+        const int4 *src = reinterpret_cast<const int4 *>(I.T);
+        int4 *dst = reinterpret_cast<int4 *>(sm + L.T);
+        int nT = NC * I.NL * I.NL;
+        for (int i = tid; i < nT / 4; i += blockDim.x) dst[i] = src[i];
+        for (int i = (nT / 4) * 4 + tid; i < nT; i += blockDim.x) sm[L.T + i] = I.T[i];
+    }
+    for (int i = tid; i < n; i += blockDim.x) {
+        sm[L.del + i] = I.del[i];
+        sm[L.heli + i] = I.heli[i];
+    }
+    for (int i = tid; i < NC * n; i += blockDim.x) sm[L.svc + i] = I.svc[i];
+    for (int i = tid; i < V; i += blockDim.x) {
+        sm[L.vcls + i] = I.vcls[i];
+        sm[L.vloc + i] = I.vloc[i];
+    }
+    for (int i = tid; i < NC; i += blockDim.x) sm[L.clsheli + i] = I.cls_heli[i];
+
+    MissionView M;
+    M.del = sm + L.del; M.heli = sm + L.heli; M.svc = sm + L.svc; M.vcls = sm + L.vcls; M.vloc = sm + L.vloc;
+    M.clsheli = sm + L.clsheli; M.T = A.T_smem ? sm + L.T : I.T;
+    M.n = n; M.V = V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
+    int32_t *Eg = A.E_smem ? sm + L.E : (A.E_global ? A.E_global + (size_t)run * n * V : nullptr);
+    RunView R;
+    R.succ = sm + L.succ; R.pred = sm + L.pred; R.veh = sm + L.veh; R.endc = sm + L.endc; R.depc = sm + L.depc;
+    R.inc = sm + L.inc; R.svco = sm + L.svco; R.pick_s = sm + L.pick_s; R.w_s = sm + L.w_s; R.F = sm + L.F;
+    R.E = TABU ? Eg : nullptr;
+    int32_t *bsucc = sm + L.bsucc;
+    unsigned long long *red = reinterpret_cast<unsigned long long *>(sm + L.red);
+    int32_t *ctrl = sm + L.ctrl;   // 0: stop, 1: copy-best, 2: infeasible flag
+
+    // ---- start schedule (CSR) -> linked lists ------------------------------
+    const int32_t *ptr = A.start_ptr + (A.shared_start ? 0 : (size_t)run * (V + 1));
+    const int32_t *ms = A.start_ms + (A.shared_start ? 0 : (size_t)run * n);
+    for (int x = tid; x < S; x += blockDim.x) {
+        if (x < n) {
+            R.veh[x] = -1;
+            sm[L.pick_s + x] = I.pick[x];
+            sm[L.w_s + x] = I.w[x];
+        } else {
+            R.veh[x] = x - n;
+            sm[L.pick_s + x] = I.vloc[x - n];
+            sm[L.w_s + x] = I.DAY;
+        }
+    }
+    if (tid < 16) ctrl[tid] = 0;
+    if (Eg && TABU)
+        for (int i = tid; i < n * V; i += blockDim.x) Eg[i] = -1;
+    __syncthreads();
+    for (int v = tid; v < V; v += blockDim.x) {
+        int prev = n + v;
+        int bad = 0;
+        int lo = ptr[v], hi = ptr[v + 1];
+        if (lo < 0 || hi < lo || hi > n) bad = 1;
+        else
+            for (int i = lo; i < hi; i++) {
+                int m = ms[i];
+                if (m < 0 || m >= n) { bad = 1; break; }
+                if (atomicCAS(&R.veh[m], -1, v) != -1) { bad = 1; break; }
+                R.succ[prev] = m;
+                R.pred[m] = prev;
+                prev = m;
+            }
+        R.succ[prev] = n + v;
+        R.pred[n + v] = prev;
+        if (bad) atomicOr(&ctrl[2], 1);
+    }
+    __syncthreads();
+    for (int x = tid; x < S; x += blockDim.x) {
+        if (x < n && R.veh[x] < 0) { atomicOr(&ctrl[2], 1); continue; }
+        if (ctrl[2]) continue;
+        refresh_slot(M, R, x);
+        // con7/con8 of the incoming link, con9 compatibility
+        if (R.depc[x] + R.inc[x] > R.w_s[x]) atomicOr(&ctrl[2], 1);
+        if (x < n && M.heli[x] && !M.clsheli[M.vcls[R.veh[x]]]) atomicOr(&ctrl[2], 1);
+    }
+    __syncthreads();
+    if (!ctrl[2])
+        for (int v = tid; v < V; v += blockDim.x) {
+            int f = 0;
+            int x = R.succ[n + v];
+            while (x < n) { f += R.inc[x]; x = R.succ[x]; }
+            f += R.inc[n + v];
+            R.F[v] = f;
+            if (f > I.P) atomicOr(&ctrl[2], 1);   // con6
+        }
+    __syncthreads();
+
+    as_run_result *res = A.results ? A.results + run : nullptr;
+    if (ctrl[2]) {
+        if (tid == 0 && res) {
+            res->best_obj = res->final_obj = res->start_obj = -1;
+            res->best_iter = -1;
+            res->iters_done = 0;
+            res->stop_reason = AS_STOP_INFEASIBLE_START;
+            res->kicks_applied = 0;
+        }
+        if (tid == 0 && A.best_ptr) {
+            for (int v = 0; v <= V; v++) A.best_ptr[(size_t)run * (V + 1) + v] = 0;
+        }
+        return;
+    }
+
+    // ---- seeded kick (O12), one thread ---------------------------------------
+    __shared__ long long s_cur, s_best, s_start;
+    __shared__ int s_best_iter, s_kicks;
+    if (tid == 0) {
+        int kicks = 0;
+        uint64_t seed = A.seeds ? A.seeds[run] : A.seed;
+        if (seed != 0 && n > 0) {
+            uint64_t s = seed;
+            uint64_t Rb = (uint64_t)n * (uint64_t)S;
+            for (int k = 0; k < A.kick; k++) {
+                for (int tr = 0; tr < 64; tr++) {
+                    uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
+                    MoveEval e = eval_index(M, R, idx, 0xFu, 0);
+                    if (e.valid && e.feasible) {
+                        apply_move(M, R, idx, e, 0, 0, false);
+                        kicks++;
+                        break;
+                    }
+                }
+            }
+        }
+        long long c = 0;
+        for (int v = 0; v < V; v++) c += R.F[v];
+        s_cur = c;
+        s_best = c;
+        s_start = c;
+        s_best_iter = -1;
+        s_kicks = kicks;
+        ctrl[1] = 1;
+    }
+    __syncthreads();
+
+    // ---- main loop -----------------------------------------------------------
+    const uint32_t mask = A.mask;
+    const int nq = n / 2;   // swap row pairs (rows q and n-2-q)
+    int it = 0;
+    for (; it < A.max_iters; it++) {
+        if (ctrl[1]) {
+            for (int x = tid; x < S; x += blockDim.x) bsucc[x] = R.succ[x];
+        }
+        const long long cur = s_cur, best = s_best;
+        uint64_t kmin = KEY_NONE;
+        // relocate rows: m warp-uniform, lanes over target slots
+        for (int m = warp; m < n; m += nwarps) {
+            RelocRow r = reloc_row(M, R, m);
+            if (r.a < 0) continue;
+            const uint32_t base = (uint32_t)m * (uint32_t)S;
+            for (int t = lane; t < S; t += 32) {
+                MoveEval e = reloc_eval(M, R, r, m, t, mask, it);
+                int cls = move_class<TABU>(e, cur, best);
+                if (cls >= 0) {
+                    uint64_t k = make_key(cls, e.delta, base + t);
+                    kmin = k < kmin ? k : kmin;
+                }
+            }
+        }
+        // swap rows, paired: row q (n-1-q items) + row n-2-q (q+1 items)
+        const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+        for (int q = warp; q < nq; q += nwarps) {
+            const int qb = n - 2 - q;
+            const int lenA = n - 1 - q;
+            const int len = qb > q ? n : lenA;
+            for (int j = lane; j < len; j += 32) {
+                int m1, m2;
+                if (j < lenA) { m1 = q; m2 = q + 1 + j; }
+                else { m1 = qb; m2 = j; }
+                MoveEval e = swap_eval(M, R, m1, m2, mask, it);
+                int cls = move_class<TABU>(e, cur, best);
+                if (cls >= 0) {
+                    uint64_t k = make_key(cls, e.delta, Rb + (uint32_t)m1 * n + m2);
+                    kmin = k < kmin ? k : kmin;
+                }
+            }
+        }
+        kmin = warp_min_u64(kmin);
+        if (lane == 0) red[warp] = kmin;
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t k = red[0];
+            for (int w2 = 1; w2 < nwarps; w2++) k = red[w2] < k ? red[w2] : k;
+            int stop = 0;
+            if (k == KEY_NONE) stop = 2;                       // no feasible move
+            else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? 2 : 1;
+            ctrl[1] = 0;
+            if (stop) {
+                ctrl[0] = stop;
+            } else {
+                uint32_t idx = key_idx(k);
+                MoveEval e = eval_index(M, R, idx, mask, it);
+                apply_move(M, R, idx, e, it, A.tenure, TABU);
+                long long c = s_cur + e.delta;
+                s_cur = c;
+                if (c < s_best) {
+                    s_best = c;
+                    s_best_iter = it;
+                    ctrl[1] = 1;
+                }
+                if (A.trace) {
+                    as_trace_rec tr;
+                    tr.cur = c;
+                    tr.best = s_best;
+                    tr.idx = idx;
+                    tr.delta = e.delta;
+                    tr.cls = key_cls(k);
+                    tr.it = it;
+                    A.trace[(size_t)run * A.max_iters + it] = tr;
+                }
+                if (A.digest && TABU) {
+                    uint64_t h = 0xcbf29ce484222325ull;
+                    for (int mm = 0; mm < n; mm++)
+                        for (int v = 0; v < V; v++) {
+                            int ev = R.E[mm * V + v];
+                            if (ev < it + 1) continue;
+                            int trip[3] = {mm, v, ev};
+                            for (int q3 = 0; q3 < 3; q3++)
+                                for (int by = 0; by < 4; by++) {
+                                    h ^= (uint64_t)(((uint32_t)trip[q3] >> (8 * by)) & 0xFFu);
+                                    h *= 0x100000001b3ull;
+                                }
+                        }
+                    A.digest[(size_t)run * A.max_iters + it] = h;
+                }
+            }
+        }
+        __syncthreads();
+        if (ctrl[0]) break;
+    }
+    if (ctrl[1]) {
+        for (int x = tid; x < S; x += blockDim.x) bsucc[x] = R.succ[x];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (res) {
+            res->start_obj = s_start;
+            res->best_obj = s_best;
+            res->final_obj = s_cur;
+            res->best_iter = s_best_iter;
+            res->iters_done = it;
+            res->stop_reason = ctrl[0] ? ctrl[0] : AS_STOP_MAX_ITERS;
+            res->kicks_applied = s_kicks;
+        }
+        if (A.best_ptr) {
+            int32_t *bp = A.best_ptr + (size_t)run * (V + 1);
+            int32_t *bm = A.best_ms + (size_t)run * n;
+            int pos = 0;
+            for (int v = 0; v < V; v++) {
+                bp[v] = pos;
+                int x = bsucc[n + v];
+                while (x < n) { bm[pos++] = x; x = bsucc[x]; }
+            }
+            bp[V] = pos;
+        }
+    }
+    if (A.tabu_out && TABU && Eg) {
+        for (int i = tid; i < n * V; i += blockDim.x) A.tabu_out[(size_t)run * n * V + i] = Eg[i];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Host-side launchers (declared in launch.h).
+cudaError_t launch_build_state(const DevInst &I, const int32_t *ptr, const int32_t *ms, RunViewG &G,
+                               cudaStream_t st) {
+    k_build_state<<<1, 256, 0, st>>>(I, ptr, ms, G.succ, G.pred, G.veh, G.endc, G.depc, G.inc, G.svco, G.pick_s,
+                                     G.w_s, G.F);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int it, long long cur, long long best,
+                             uint32_t mask, int32_t *delta, uint8_t *flags, unsigned long long *best_key,
+                             uint64_t N, int n_sm, cudaStream_t st) {
+    int threads = 256;
+    uint64_t blocks64 = (N + threads - 1) / threads;
+    int blocks = (int)(blocks64 < (uint64_t)n_sm * 8 ? blocks64 : (uint64_t)n_sm * 8);
+    if (blocks < 1) blocks = 1;
+    size_t smem = (size_t)(I.n + I.NC) * 4;
+    if (mode == 1)
+        k_eval_dump<true><<<blocks, threads, smem, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
+    else
+        k_eval_dump<false><<<blocks, threads, smem, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st) {
+    cudaError_t err;
+    if (mode == 1) {
+        err = cudaFuncSetAttribute(k_search<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        k_search<true><<<n_runs, threads, smem, st>>>(A);
+    } else {
+        err = cudaFuncSetAttribute(k_search<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        k_search<false><<<n_runs, threads, smem, st>>>(A);
+    }
+    return cudaGetLastError();
+}
+
+__global__ void k_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * NC; i += gridDim.x * blockDim.x) {
+        int c = i / n, m = i % n;
+        svc[i] = T[((size_t)c * NL + pick[m]) * NL + del[m]];
+    }
+}
+
+cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
+                       cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_svc<<<(n * NC + 255) / 256, 256, 0, st>>>(T, pick, del, svc, n, NL, NC);
+    return cudaGetLastError();
+}
+
+}  // namespace airsched

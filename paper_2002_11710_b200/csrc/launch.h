@@ -1,0 +1,43 @@
+// launch.h -- host <-> kernel interface inside the library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "airsched.h"
+#include "engine.cuh"
+
+namespace airsched {
+
+// One run's state in global memory (dump path).
+struct RunViewG {
+    int32_t *succ, *pred, *veh, *endc, *depc, *inc, *svco, *pick_s, *w_s, *F, *E;
+};
+
+struct SearchArgs {
+    DevInst inst;
+    const int32_t *start_ptr, *start_ms;   // [R][V+1], [R][n] or shared
+    int32_t shared_start;
+    const uint64_t *seeds;                 // [R] or null -> seed
+    uint64_t seed;
+    int32_t kick, tenure, max_iters, strict_tabu_stop;
+    uint32_t mask;
+    int32_t T_smem, E_smem;
+    int32_t *E_global;                     // [R][n][V] when !E_smem
+    as_run_result *results;                // [R]
+    int32_t *best_ptr, *best_ms;           // [R][V+1], [R][n]
+    as_trace_rec *trace;                   // [R][max_iters]
+    uint64_t *digest;                      // [R][max_iters]
+    int32_t *tabu_out;                     // [R][n][V]
+};
+
+size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem);
+cudaError_t launch_build_state(const DevInst &I, const int32_t *ptr, const int32_t *ms, RunViewG &G, cudaStream_t st);
+cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int it, long long cur, long long best,
+                             uint32_t mask, int32_t *delta, uint8_t *flags, unsigned long long *best_key, uint64_t N,
+                             int n_sm, cudaStream_t st);
+cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st);
+cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
+                       cudaStream_t st);
+
+}  // namespace airsched

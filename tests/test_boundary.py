@@ -1,0 +1,92 @@
+"""C-ABI boundary tests that need no GPU: the library loads, exports every
+symbol include/airsched.h declares, validates instances, and its host-side
+schedule check agrees with the oracle.  (No compute calls without a GPU.)"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2002_11710_b200 import instgen
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2002_11710_b200 import _build
+    _build.build()
+    from paper_2002_11710_b200 import airsched
+    return airsched
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "airsched.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(as_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(A):
+    syms = header_symbols()
+    assert len(syms) >= 18
+    out = os.popen(f"nm -D --defined-only {A.LIB_PATH}").read()
+    exported = set(re.findall(r"\bT (as_[a-z0-9_]+)", out))
+    assert set(syms) <= exported, set(syms) - exported
+    assert set(A.SYMBOLS) == set(syms)
+    assert b"sm_100a" in A.lib.as_version()
+
+
+def test_sass_is_sm100a(A):
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {A.LIB_PATH}").read()
+    assert "sm_100a" in out
+
+
+def test_instance_validation(A):
+    inst = instgen.generate("tiny")
+    h = A.Instance(inst)
+    n, V = inst.n_missions, inst.n_vehicles
+    assert h.move_space_size == n * (n + V) + n * n == 152
+    assert h.valid_moves_per_iter == 100
+    bad = instgen.generate("tiny")
+    bad.travel_s = bad.travel_s.copy()
+    bad.travel_s[0, 1, 1] = 5
+    with pytest.raises(A.AirschedError) as e:
+        A.Instance(bad)
+    assert e.value.status == A.AS_ERR_INVALID_ARG and "diagonal" in str(e.value)
+    bad = instgen.generate("tiny")
+    bad.deadline_s = bad.deadline_s.copy()
+    bad.deadline_s[2] = 0
+    with pytest.raises(A.AirschedError):
+        A.Instance(bad)
+    bad = instgen.generate("tiny")
+    bad.vehicle_class = np.array([0, 0, 7], np.int32)
+    with pytest.raises(A.AirschedError):
+        A.Instance(bad)
+
+
+def test_schedule_check_matches_oracle(A, oracle_mod):
+    rng = np.random.default_rng(2)
+    for cfg in ("tiny", "ontario"):
+        inst = instgen.generate(cfg)
+        h = A.Instance(inst)
+        O = oracle_mod.Oracle(inst)
+        states = [(inst.planted_ptr, inst.planted_missions)]
+        n, V = inst.n_missions, inst.n_vehicles
+        for _ in range(30):
+            perm = rng.permutation(n).astype(np.int32)
+            cuts = np.sort(rng.integers(0, n + 1, V - 1))
+            states.append((np.concatenate([[0], cuts, [n]]).astype(np.int32), perm))
+        for p, m in states:
+            f, obj = h.check(p, m)
+            assert obj == O.objective(p, m) and f == O.feasible(p, m)
+    with pytest.raises(A.AirschedError):
+        h.check(np.array([0, 1] + [1] * (V - 1), np.int32), np.array([n + 5], np.int32))
+
+
+def test_ctx_without_gpu_fails_loudly(A):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(A.AirschedError) as e:
+        A.Ctx(0, 0)
+    assert e.value.status == A.AS_ERR_DEVICE

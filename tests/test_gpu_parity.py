@@ -1,0 +1,313 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Every comparison is element by element on seeded synthetic inputs
+(paper_2002_11710_b200/instgen.py).  Integer work => the bar is exact equality
+(BASELINE.json north_star: "bit-exact").  The selection key is compared by
+decoding (class, delta, idx) from the key and comparing with the oracle's
+selected move.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from e1 import e1_instance
+from paper_2002_11710_b200 import instgen
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "e1.json")))
+
+
+@pytest.fixture(scope="module")
+def A():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2002_11710_b200 import airsched
+    return airsched
+
+
+@pytest.fixture(scope="module")
+def ctx(A):
+    return A.Ctx(0)
+
+
+def decode_key(key):
+    if key == 0xFFFFFFFFFFFFFFFF:
+        return (-1, 0, -1)
+    return (key >> 63, int(((key >> 32) & 0x7FFFFFFF) - (1 << 30)), key & 0xFFFFFFFF)
+
+
+def routes_of(ptr, ms):
+    return [list(map(int, ms[ptr[v]:ptr[v + 1]])) for v in range(len(ptr) - 1)]
+
+
+def start_of(O, inst):
+    st, (p, m), _, _ = O.greedy()
+    if st != 0:
+        p, m = inst.planted_ptr, inst.planted_missions
+    return p, m
+
+
+def states_for(O, inst, n_ts=(5, 23), kicks=(3, 9)):
+    p, m = start_of(O, inst)
+    out = [(p, m)]
+    for it in n_ts:
+        out.append(O.search(p, m, mode=1, tenure=3, max_iters=it, trace=False)["final"])
+    for s in kicks:
+        out.append(O.kick(p, m, s, 12)[1])
+    return out
+
+
+# ----------------------------------------------------------------- E1 golden --
+def test_e1_eval_golden(A, ctx, oracle_mod):
+    I = e1_instance()
+    h = A.Instance(I)
+    ptr, ms = np.array([0, 3, 3], np.int32), np.array([0, 1, 2], np.int32)
+    d, f, key = A.as_eval_moves(ctx, h, ptr, ms, mode=A.AS_MODE_NS)
+    for k, mv in GOLD["moves"].items():
+        assert d[int(k)] == mv["delta"] and bool(f[int(k)] & 2) == mv["feasible"]
+    assert int((f & 1).sum()) == GOLD["valid_count"]
+    assert decode_key(key) == (0, -1160, 9)
+
+
+def test_e1_runs_golden(A, ctx):
+    I = e1_instance()
+    h = A.Instance(I)
+    ptr, ms = np.array([0, 3, 3], np.int32), np.array([0, 1, 2], np.int32)
+    g = GOLD["ts_tenure2"]
+    r = A.as_tabu_run(ctx, h, ptr, ms, A.params(mode=1, tenure=2, max_iters=4, trace_level=1), want_trace=True)
+    tr = r["trace"]
+    assert list(tr["idx"]) == g["idx"] and list(tr["delta"]) == g["delta"]
+    assert list(tr["cur"]) == g["cur"] and list(tr["best"]) == g["best"] and list(tr["cls"]) == g["cls"]
+    rn = A.as_nbhd_run(ctx, h, ptr, ms, A.params(mode=0, max_iters=10, trace_level=1), want_trace=True)
+    assert list(rn["trace"]["idx"]) == GOLD["ns"]["idx"] and rn["best_obj"] == 640 and rn["stop_reason"] == 1
+    rs = A.as_tabu_run(ctx, h, ptr, ms, A.params(mode=1, tenure=2, max_iters=8, strict_tabu_stop=1))
+    assert rs["iters_done"] == 2 and rs["stop_reason"] == 2
+    gp, gm, nrep = A.as_init_greedy(ctx, h)
+    assert routes_of(gp, gm) == GOLD["greedy_tail"]["routes"]
+
+
+# ------------------------------------------------------- as_eval_moves parity --
+@pytest.mark.parametrize("cfg", ["tiny", "ontario", "batched", "large"])
+def test_eval_moves_parity(A, ctx, oracle_mod, cfg):
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    rng = np.random.default_rng(11)
+    states = states_for(O, inst) if cfg != "large" else states_for(O, inst, n_ts=(3,), kicks=(5,))
+    for si, (p, m) in enumerate(states):
+        obj = O.objective(p, m)
+        for mode in (0, 1):
+            E = None
+            it = 0
+            best = obj
+            if mode == 1:
+                it = int(rng.integers(5, 40))
+                E = rng.integers(-1, it + 8, size=(inst.n_missions, inst.n_vehicles)).astype(np.int32)
+                best = obj - int(rng.integers(0, 2000))
+            od, of, (bc, bd, bi) = O.eval_moves(p, m, mode=mode, E=E, it=it, best_obj=best)
+            gd, gf, key = A.as_eval_moves(ctx, h, p, m, mode=mode, tabu_expiry=E, iter=it, best_obj=best)
+            assert (gf == of).all(), f"flags differ at {np.flatnonzero(gf != of)[:10]}"
+            assert (gd == od).all(), f"delta differs at {np.flatnonzero(gd != od)[:10]}"
+            assert decode_key(key) == (bc, bd, bi) if bc >= 0 else key == 0xFFFFFFFFFFFFFFFF
+
+
+def test_eval_moves_surge_sampled(A, ctx, oracle_mod):
+    """Full C5 size (n=4000, V=100, 32.4 M indices): GPU dump vs oracle on a
+    seeded sample of indices (every row touched), plus the selected key against
+    a full oracle scan."""
+    inst = instgen.generate("surge")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    p2, m2 = O.kick(p, m, 77, 40)[1]
+    rng = np.random.default_rng(5)
+    N = h.move_space_size
+    idx = np.unique(np.concatenate([rng.integers(0, N, 200000), np.arange(0, N, 4001)]))
+    E = rng.integers(-1, 30, size=(inst.n_missions, inst.n_vehicles)).astype(np.int32)
+    obj = O.objective(p2, m2)
+    od, of = O.eval_indices(p2, m2, idx, mode=1, E=E, it=20, best_obj=obj - 100)
+    gd, gf, key = A.as_eval_moves(ctx, h, p2, m2, mode=1, tabu_expiry=E, iter=20, best_obj=obj - 100)
+    assert (gf[idx] == of).all() and (gd[idx] == od).all()
+    assert int((gf & 1).sum()) == h.valid_moves_per_iter
+
+
+def test_partial_schedule_eval(A, ctx, oracle_mod):
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    keep = [x for x in m if x % 3 != 0]
+    routes = [[x for x in r if x in set(keep)] for r in routes_of(p, m)]
+    pp = np.zeros(len(routes) + 1, np.int32)
+    pp[1:] = np.cumsum([len(r) for r in routes])
+    mm = np.array([x for r in routes for x in r], np.int32)
+    od, of, ob = O.eval_moves(pp, mm, mode=0)
+    gd, gf, key = A.as_eval_moves(ctx, h, pp, mm, mode=0)
+    assert (gd == od).all() and (gf == of).all() and decode_key(key) == ob
+
+
+# ------------------------------------------------------------- run parity --
+def _compare_run(A, ctx, O, h, p, m, mode, tenure, iters, digest=False, seed=0, kick=0):
+    prm = A.params(mode=mode, tenure=tenure, max_iters=iters, trace_level=2 if digest else 1, seed=seed, kick=kick)
+    g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_digest=digest, want_tabu=(mode == 1))
+    o = O.search(p, m, mode=mode, tenure=tenure, max_iters=iters, digest=digest, seed=seed, kick=kick)
+    ot, gt = o["trace"], g["trace"]
+    assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+    assert (gt["idx"] == ot["idx"]).all(), f"first divergence at it {np.flatnonzero(gt['idx'] != ot['idx'])[:1]}"
+    assert (gt["delta"] == ot["delta"]).all() and (gt["cur"] == ot["cur"]).all()
+    assert (gt["best"] == ot["best"]).all() and (gt["cls"] == ot["cls"]).all()
+    if digest:
+        assert (g["digest"] == ot["digest"]).all()
+    if mode == 1:
+        assert (g["tabu"] == o["E"]).all()
+    assert g["best_obj"] == o["best_obj"] and g["final_obj"] == o["final_obj"] and g["best_iter"] == o["best_iter"]
+    assert g["start_obj"] == o["start_obj"] and g["kicks_applied"] == o["kicks_applied"]
+    assert routes_of(*g["best"]) == routes_of(*o["best"])
+    return g
+
+
+@pytest.mark.parametrize("cfg,iters,digest", [("tiny", 200, True), ("ontario", 5000, True), ("batched", 1000, False)])
+def test_tabu_run_parity(A, ctx, oracle_mod, cfg, iters, digest):
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, digest=digest)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+
+
+def test_large_run_parity_prefix(A, ctx, oracle_mod):
+    """C4 (n=500, V=40) at full size, the first iterations of TS and NS."""
+    inst = instgen.generate("large")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    _compare_run(A, ctx, O, h, p, m, 1, 10, 40)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, 40)
+
+
+def test_kicked_runs_parity(A, ctx, oracle_mod):
+    inst = instgen.generate("batched")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    for seed in (1, 2, 4096):
+        _compare_run(A, ctx, O, h, p, m, 1, 10, 300, seed=seed, kick=8)
+
+
+def test_batch_run_parity(A, ctx, oracle_mod):
+    """as_batch_run in the bench's launch configuration (shared start, per-run
+    seeds, kick 8), with sampled runs checked against the oracle."""
+    import torch
+    inst = instgen.generate("batched")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    c = instgen.CONFIGS["batched"]
+    p, m = start_of(O, inst)
+    R, iters = 512, 200
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
+    bm = np.zeros((R, inst.n_missions), np.int32)
+    tr = np.zeros((R, iters), A.TRACE_DTYPE)
+    prm = A.params(mode=1, tenure=c.tenure, max_iters=iters, kick=c.kick, trace_level=1)
+    best_run = A.as_batch_run(ctx, h, R, p, m, prm, seeds, shared_start=True, results=res, best_ptr_out=bp,
+                              best_missions_out=bm, trace_out=tr, want_best_run=True)
+    assert best_run == int(np.lexsort((np.arange(R), res["best_obj"]))[0])
+    for r in (0, 1, 77, 300, R - 1):
+        o = O.search(p, m, mode=1, tenure=c.tenure, max_iters=iters, seed=int(seeds[r]), kick=c.kick)
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == o["iters_done"]
+        assert res[r]["kicks_applied"] == o["kicks_applied"] and res[r]["best_iter"] == o["best_iter"]
+        assert (tr[r]["idx"][:o["iters_done"]] == o["trace"]["idx"]).all()
+        assert routes_of(bp[r], bm[r]) == routes_of(*o["best"])
+    # device-resident inputs/outputs (the bench's timed configuration)
+    dev = torch.device("cuda:0")
+    tp, tm = torch.from_numpy(p).to(dev), torch.from_numpy(m).to(dev)
+    ts = torch.from_numpy(seeds.view(np.int64)).to(dev)
+    tres = torch.zeros((R, 40), dtype=torch.uint8, device=dev)
+    A.as_batch_run(ctx, h, R, tp, tm, prm, ts, shared_start=True, results=tres)
+    torch.cuda.synchronize()
+    res2 = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(R)
+    assert (res2 == res).all()
+
+
+def test_greedy_parity(A, ctx, oracle_mod):
+    for cfg in instgen.CONFIGS:
+        inst = instgen.generate(cfg)
+        O = oracle_mod.Oracle(inst)
+        h = A.Instance(inst)
+        for mode in (0, 1):
+            st, (p, m), nrep, _ = O.greedy(insert_mode=mode)
+            if st != 0:
+                with pytest.raises(A.AirschedError):
+                    A.as_init_greedy(ctx, h, insert_mode=mode)
+                continue
+            gp, gm, gn = A.as_init_greedy(ctx, h, insert_mode=mode)
+            assert routes_of(gp, gm) == routes_of(p, m) and gn == nrep
+
+
+def test_greedy_repair_parity(A, ctx, oracle_mod):
+    """Instances where Alg. 1 needs its repair step -- found by seed scan."""
+    found = 0
+    for seed in range(400):
+        cfg = instgen.Config("r", 12, 2, 1, 1, 1, 8, "ontario", 4, 10, 3)
+        inst = instgen.generate(cfg, seed=seed)
+        O = oracle_mod.Oracle(inst)
+        st, (p, m), nrep, _ = O.greedy()
+        if nrep == 0:
+            continue
+        found += 1
+        h = A.Instance(inst)
+        if st != 0:
+            with pytest.raises(A.AirschedError):
+                A.as_init_greedy(ctx, h)
+        else:
+            gp, gm, gn = A.as_init_greedy(ctx, h)
+            assert routes_of(gp, gm) == routes_of(p, m) and gn == nrep
+        if found >= 5:
+            break
+
+
+# ------------------------------------------------------------- edge cases --
+def test_edge_cases(A, ctx, oracle_mod):
+    base = instgen.generate("tiny")
+    # zero missions
+    empty = instgen.Instance(base.travel_s, base.class_is_heli, base.base_location, base.vehicle_base,
+                             base.vehicle_class, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                             np.zeros(0, np.uint8))
+    h = A.Instance(empty)
+    p = np.zeros(base.n_vehicles + 1, np.int32)
+    r = A.as_tabu_run(ctx, h, p, np.zeros(0, np.int32), A.params(max_iters=10))
+    assert r["best_obj"] == 0 and r["stop_reason"] == A.AS_STOP_NO_MOVE and r["iters_done"] == 0
+    # one mission, one vehicle
+    one_cfg = instgen.Config("one", 1, 1, 0, 1, 0, 4, "ontario", 3, 10, 2)
+    one = instgen.generate(one_cfg, seed=3)
+    O = oracle_mod.Oracle(one)
+    h = A.Instance(one)
+    g = A.as_tabu_run(ctx, h, one.planted_ptr, one.planted_missions, A.params(max_iters=5))
+    o = O.search(one.planted_ptr, one.planted_missions, max_iters=5)
+    assert g["best_obj"] == o["best_obj"] and g["stop_reason"] == o["stop_reason"]
+    # infeasible start -> AS_ERR_INFEASIBLE_START
+    inst = instgen.generate("ontario")
+    h = A.Instance(inst)
+    bad_ptr = np.array([0] + [inst.n_missions] * inst.n_vehicles, np.int32)
+    bad_ms = np.argsort(inst.deadline_s)[::-1].astype(np.int32)   # everything on vehicle 0, reversed
+    with pytest.raises(A.AirschedError) as e:
+        A.as_tabu_run(ctx, h, bad_ptr, bad_ms, A.params(max_iters=5))
+    assert e.value.status == A.AS_ERR_INFEASIBLE_START
+    # paper-only move set (inter-route relocate only)
+    O = oracle_mod.Oracle(inst)
+    p, m = start_of(O, inst)
+    _compare_run_mask(A, ctx, O, A.Instance(inst), p, m)
+
+
+def _compare_run_mask(A, ctx, O, h, p, m):
+    prm = A.params(mode=1, tenure=10, max_iters=300, move_mask=A.AS_MOVE_INTER_RELOCATE, trace_level=1)
+    g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True)
+    o = O.search(p, m, mode=1, tenure=10, max_iters=300, mask=1)
+    assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and g["best_obj"] == o["best_obj"]
