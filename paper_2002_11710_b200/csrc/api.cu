@@ -46,7 +46,8 @@ struct as_instance {
     uint64_t uid;
     int32_t NL, NC, V, n, n_bases, P, DAY;
     std::vector<int32_t> T, base_loc, vbase, vcls, vloc, pick, del, w;
-    std::vector<uint8_t> cls_heli, heli;
+    std::vector<uint8_t> cls_heli, heli, vcls8;
+    int32_t maxT = 0;
 };
 
 static uint64_t g_uid = 1;
@@ -76,6 +77,7 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
                 int32_t t = I->T[(c * NL + a) * NL + b];
                 if (t < 0 || t >= (1 << 26)) return fail(AS_ERR_INVALID_ARG, "travel_s[%lld][%lld][%lld] = %d outside [0, 2^26)", (long long)c, (long long)a, (long long)b, t);
                 if (a == b && t != 0) return fail(AS_ERR_INVALID_ARG, "travel_s diagonal must be 0 (S:35)");
+                if (t > I->maxT) I->maxT = t;
             }
     I->cls_heli.assign(d->class_is_heli, d->class_is_heli + NC);
     I->base_loc.assign(d->base_location, d->base_location + B);
@@ -89,6 +91,7 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
         if (I->vcls[v] < 0 || I->vcls[v] >= NC) return fail(AS_ERR_INVALID_ARG, "vehicle_class[%lld] out of range", (long long)v);
         I->vloc[v] = I->base_loc[I->vbase[v]];
     }
+    I->vcls8.assign(I->vcls.begin(), I->vcls.end());
     if (n > 0) {
         I->pick.assign(d->pickup_loc, d->pickup_loc + n);
         I->del.assign(d->delivery_loc, d->delivery_loc + n);
@@ -329,6 +332,7 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
     if ((st = dev_copy(D, I->T, &D.d.T, s)) != AS_OK) return st;
     if ((st = dev_copy(D, I->vloc, &D.d.vloc, s)) != AS_OK) return st;
     if ((st = dev_copy(D, I->vcls, &D.d.vcls, s)) != AS_OK) return st;
+    if ((st = dev_copy(D, I->vcls8, &D.d.vcls8, s)) != AS_OK) return st;
     if ((st = dev_copy(D, I->cls_heli, &D.d.cls_heli, s)) != AS_OK) return st;
     if ((st = dev_copy(D, I->pick, &D.d.pick, s)) != AS_OK) return st;
     if ((st = dev_copy(D, I->del, &D.d.del, s)) != AS_OK) return st;
@@ -341,6 +345,7 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
     ctx->launches += I->n > 0;
     D.d.svc = (const int32_t *)svc;
     D.d.n = I->n; D.d.V = I->V; D.d.NL = I->NL; D.d.NC = I->NC; D.d.P = I->P; D.d.DAY = I->DAY;
+    D.d.maxT = I->maxT;
     auto &slot = ctx->insts[I];
     slot = std::move(D);
     *out = &slot.d;
@@ -593,18 +598,38 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     A.digest = (uint64_t *)o_dg.dev;
     A.tabu_out = (int32_t *)o_tb.dev;
     // single-result call: results struct is host memory and required
-    int threads;
+    A.n_runs = n_runs;
+    // launch policy: single runs -> one CTA per run (k_search); batches -> one run
+    // per warp with the instance shared per CTA (k_batch) when the compact layout fits.
     const int64_t N = as_move_space_size(I);
-    if (single) {
-        int64_t t = 64;
-        while (t < 1024 && t * 16 < N) t *= 2;
-        threads = (int)t;
-    } else {
-        threads = 256;
-    }
-    threads = env_int("AIRSCHED_THREADS", threads);
+    const int S = n + V;
+    const int tbytes = I->maxT <= 65535 ? 2 : 4;
+    const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
+    size_t sh_b = 0, run_b = 0;
+    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b);
+    int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
+    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !tabu_out;
+    const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
+    bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single));
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    CUDA_TRY(launch_search(A, tabu ? 1 : 0, n_runs, threads, smem, ctx->stream));
+    if (use_batch) {
+        int rpc = (int)std::min<int64_t>(28, std::min<int64_t>(rpc_fit, (n_runs + ctx->n_sm - 1) / ctx->n_sm));
+        rpc = std::max(1, env_int("AIRSCHED_RPC", rpc));
+        rpc = std::min(rpc, std::min(28, rpc_fit));
+        size_t smem_b = sh_b + (size_t)rpc * run_b;
+        CUDA_TRY(launch_batch(A, tabu ? 1 : 0, rpc, tbytes, ebytes, smem_b, ctx->stream));
+    } else {
+        int threads;
+        if (single) {
+            int64_t t = 64;
+            while (t < 1024 && t * 16 < N) t *= 2;
+            threads = (int)t;
+        } else {
+            threads = 256;
+        }
+        threads = env_int("AIRSCHED_THREADS", threads);
+        CUDA_TRY(launch_search(A, tabu ? 1 : 0, n_runs, threads, smem, ctx->stream));
+    }
     ctx->launches++;
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->timed = true;

@@ -20,6 +20,13 @@
 
 namespace airsched {
 
+__device__ __forceinline__ MissionView global_view(const DevInst &I) {
+    MissionView M;
+    M.T = I.T; M.del = I.del; M.heli = I.heli; M.svc = I.svc; M.vcls = I.vcls8; M.vloc = I.vloc;
+    M.clsheli = I.cls_heli; M.n = I.n; M.V = I.V; M.NL = I.NL; M.NLp = I.NL; M.P = I.P; M.DAY = I.DAY;
+    return M;
+}
+
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -64,9 +71,7 @@ __global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, 
         pred[n + v] = prev;
     }
     __syncthreads();
-    MissionView M;
-    M.del = I.del; M.heli = nullptr; M.svc = I.svc; M.vcls = I.vcls; M.vloc = I.vloc; M.clsheli = nullptr;
-    M.T = I.T; M.n = n; M.V = V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
+    MissionView M = global_view(I);
     RunView R;
     R.succ = succ; R.pred = pred; R.veh = veh; R.endc = endc; R.depc = depc; R.inc = inc; R.svco = svco;
     R.pick_s = pick_s; R.w_s = w_s; R.F = F; R.E = nullptr;
@@ -88,18 +93,7 @@ __global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, 
 template <bool TABU>
 __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long long best, uint32_t mask,
                             int32_t *delta_out, uint8_t *flags_out, unsigned long long *best_key, uint64_t N) {
-    MissionView M;
-    M.del = I.del; M.svc = I.svc; M.vcls = I.vcls; M.vloc = I.vloc; M.T = I.T;
-    M.n = I.n; M.V = I.V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
-    extern __shared__ int32_t sh_small[];
-    // heli flags / class flags as int in smem (tiny)
-    int32_t *heli_s = sh_small;
-    int32_t *ch_s = sh_small + I.n;
-    for (int i = threadIdx.x; i < I.n; i += blockDim.x) heli_s[i] = I.heli[i];
-    for (int i = threadIdx.x; i < I.NC; i += blockDim.x) ch_s[i] = I.cls_heli[i];
-    __syncthreads();
-    M.heli = heli_s;
-    M.clsheli = ch_s;
+    MissionView M = global_view(I);
     RunView R;
     R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
     R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = TABU ? G.E : nullptr;
@@ -130,53 +124,52 @@ __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long l
 // ----------------------------------------------------------------------------
 // Persistent search kernel: one run per CTA.
 struct SmemLayout {
-    // offsets in int32 words
+    // byte offsets, 16-byte aligned
     int T, del, heli, svc, vcls, vloc, clsheli;
     int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc;
-    int red;      // 64-bit aligned, 32 x u64
-    int ctrl;     // control words
-    int total;    // words
+    int red, ctrl, total;
 };
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
     SmemLayout L;
     int o = 0;
     const int S = n + V;
     L.T = T_smem ? o : -1;
-    o += T_smem ? NC * NL * NL : 0;
-    L.del = o; o += n;
-    L.heli = o; o += n;
-    L.svc = o; o += NC * n;
-    L.vcls = o; o += V;
-    L.vloc = o; o += V;
-    L.clsheli = o; o += NC;
-    L.succ = o; o += S;
-    L.pred = o; o += S;
-    L.veh = o; o += S;
-    L.endc = o; o += S;
-    L.depc = o; o += S;
-    L.inc = o; o += S;
-    L.svco = o; o += S;
-    L.pick_s = o; o += S;
-    L.w_s = o; o += S;
-    L.F = o; o += V;
-    L.bsucc = o; o += S;
+    o = align16(o + (T_smem ? NC * NL * NL * 4 : 0));
+    L.del = o; o = align16(o + n * 4);
+    L.heli = o; o = align16(o + n);
+    L.svc = o; o = align16(o + NC * n * 4);
+    L.vcls = o; o = align16(o + V);
+    L.vloc = o; o = align16(o + V * 4);
+    L.clsheli = o; o = align16(o + NC);
+    L.succ = o; o = align16(o + S * 4);
+    L.pred = o; o = align16(o + S * 4);
+    L.veh = o; o = align16(o + S * 4);
+    L.endc = o; o = align16(o + S * 4);
+    L.depc = o; o = align16(o + S * 4);
+    L.inc = o; o = align16(o + S * 4);
+    L.svco = o; o = align16(o + S * 4);
+    L.pick_s = o; o = align16(o + S * 4);
+    L.w_s = o; o = align16(o + S * 4);
+    L.F = o; o = align16(o + V * 4);
+    L.bsucc = o; o = align16(o + S * 4);
     L.E = E_smem ? o : -1;
-    o += E_smem ? n * V : 0;
-    o = (o + 1) & ~1;
-    L.red = o; o += 2 * 32;
-    L.ctrl = o; o += 16;
+    o = align16(o + (E_smem ? n * V * 4 : 0));
+    L.red = o; o = align16(o + 32 * 8);
+    L.ctrl = o; o = align16(o + 16 * 4);
     L.total = o;
     return L;
 }
 
 size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
-    return (size_t)make_layout(n, V, NL, NC, T_smem, E_smem).total * 4;
+    return (size_t)make_layout(n, V, NL, NC, T_smem, E_smem).total;
 }
 
 template <bool TABU>
 __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
-    extern __shared__ __align__(16) int32_t sm[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC;
     const int run = blockIdx.x;
@@ -184,36 +177,40 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     const SmemLayout L = make_layout(n, V, I.NL, NC, A.T_smem, A.E_smem);
 
     // ---- stage instance constants -----------------------------------------
+#define SM32(off) reinterpret_cast<int32_t *>(smem_raw + (off))
+#define SM8(off) reinterpret_cast<uint8_t *>(smem_raw + (off))
     if (A.T_smem) {
         const int4 *src = reinterpret_cast<const int4 *>(I.T);
-        int4 *dst = reinterpret_cast<int4 *>(sm + L.T);
+        int4 *dst = reinterpret_cast<int4 *>(smem_raw + L.T);
         int nT = NC * I.NL * I.NL;
         for (int i = tid; i < nT / 4; i += blockDim.x) dst[i] = src[i];
-        for (int i = (nT / 4) * 4 + tid; i < nT; i += blockDim.x) sm[L.T + i] = I.T[i];
+        for (int i = (nT / 4) * 4 + tid; i < nT; i += blockDim.x) SM32(L.T)[i] = I.T[i];
     }
     for (int i = tid; i < n; i += blockDim.x) {
-        sm[L.del + i] = I.del[i];
-        sm[L.heli + i] = I.heli[i];
+        SM32(L.del)[i] = I.del[i];
+        SM8(L.heli)[i] = I.heli[i];
     }
-    for (int i = tid; i < NC * n; i += blockDim.x) sm[L.svc + i] = I.svc[i];
+    for (int i = tid; i < NC * n; i += blockDim.x) SM32(L.svc)[i] = I.svc[i];
     for (int i = tid; i < V; i += blockDim.x) {
-        sm[L.vcls + i] = I.vcls[i];
-        sm[L.vloc + i] = I.vloc[i];
+        SM8(L.vcls)[i] = (uint8_t)I.vcls[i];
+        SM32(L.vloc)[i] = I.vloc[i];
     }
-    for (int i = tid; i < NC; i += blockDim.x) sm[L.clsheli + i] = I.cls_heli[i];
+    for (int i = tid; i < NC; i += blockDim.x) SM8(L.clsheli)[i] = I.cls_heli[i];
 
     MissionView M;
-    M.del = sm + L.del; M.heli = sm + L.heli; M.svc = sm + L.svc; M.vcls = sm + L.vcls; M.vloc = sm + L.vloc;
-    M.clsheli = sm + L.clsheli; M.T = A.T_smem ? sm + L.T : I.T;
-    M.n = n; M.V = V; M.NL = I.NL; M.P = I.P; M.DAY = I.DAY;
-    int32_t *Eg = A.E_smem ? sm + L.E : (A.E_global ? A.E_global + (size_t)run * n * V : nullptr);
+    M.del = SM32(L.del); M.heli = SM8(L.heli); M.svc = SM32(L.svc); M.vcls = SM8(L.vcls); M.vloc = SM32(L.vloc);
+    M.clsheli = SM8(L.clsheli); M.T = A.T_smem ? SM32(L.T) : I.T;
+    M.n = n; M.V = V; M.NL = I.NL; M.NLp = I.NL; M.P = I.P; M.DAY = I.DAY;
+    int32_t *Eg = A.E_smem ? SM32(L.E) : (A.E_global ? A.E_global + (size_t)run * n * V : nullptr);
     RunView R;
-    R.succ = sm + L.succ; R.pred = sm + L.pred; R.veh = sm + L.veh; R.endc = sm + L.endc; R.depc = sm + L.depc;
-    R.inc = sm + L.inc; R.svco = sm + L.svco; R.pick_s = sm + L.pick_s; R.w_s = sm + L.w_s; R.F = sm + L.F;
+    R.succ = SM32(L.succ); R.pred = SM32(L.pred); R.veh = SM32(L.veh); R.endc = SM32(L.endc); R.depc = SM32(L.depc);
+    R.inc = SM32(L.inc); R.svco = SM32(L.svco); R.pick_s = SM32(L.pick_s); R.w_s = SM32(L.w_s); R.F = SM32(L.F);
     R.E = TABU ? Eg : nullptr;
-    int32_t *bsucc = sm + L.bsucc;
-    unsigned long long *red = reinterpret_cast<unsigned long long *>(sm + L.red);
-    int32_t *ctrl = sm + L.ctrl;   // 0: stop, 1: copy-best, 2: infeasible flag
+    int32_t *bsucc = SM32(L.bsucc);
+    unsigned long long *red = reinterpret_cast<unsigned long long *>(smem_raw + L.red);
+    int32_t *ctrl = SM32(L.ctrl);   // 0: stop, 1: copy-best, 2: infeasible flag
+    int32_t *pick_w = SM32(L.pick_s);
+    int32_t *w_w = SM32(L.w_s);
 
     // ---- start schedule (CSR) -> linked lists ------------------------------
     const int32_t *ptr = A.start_ptr + (A.shared_start ? 0 : (size_t)run * (V + 1));
@@ -221,12 +218,12 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     for (int x = tid; x < S; x += blockDim.x) {
         if (x < n) {
             R.veh[x] = -1;
-            sm[L.pick_s + x] = I.pick[x];
-            sm[L.w_s + x] = I.w[x];
+            pick_w[x] = I.pick[x];
+            w_w[x] = I.w[x];
         } else {
             R.veh[x] = x - n;
-            sm[L.pick_s + x] = I.vloc[x - n];
-            sm[L.w_s + x] = I.DAY;
+            pick_w[x] = I.vloc[x - n];
+            w_w[x] = I.DAY;
         }
     }
     if (tid < 16) ctrl[tid] = 0;
@@ -258,17 +255,17 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
         refresh_slot(M, R, x);
         // con7/con8 of the incoming link, con9 compatibility
         if (R.depc[x] + R.inc[x] > R.w_s[x]) atomicOr(&ctrl[2], 1);
-        if (x < n && M.heli[x] && !M.clsheli[M.vcls[R.veh[x]]]) atomicOr(&ctrl[2], 1);
+        if (x < n && M.hl(x) && !M.hok(M.cls(R.veh[x]))) atomicOr(&ctrl[2], 1);
     }
     __syncthreads();
     if (!ctrl[2])
         for (int v = tid; v < V; v += blockDim.x) {
             int f = 0;
             int x = R.succ[n + v];
-            while (x < n) { f += R.inc[x]; x = R.succ[x]; }
+            for (int guard = 0; x < n && guard <= n; guard++) { f += R.inc[x]; x = R.succ[x]; }
             f += R.inc[n + v];
             R.F[v] = f;
-            if (f > I.P) atomicOr(&ctrl[2], 1);   // con6
+            if (f > I.P || x < n) atomicOr(&ctrl[2], 1);   // con6 (or a corrupt list)
         }
     __syncthreads();
 
@@ -395,19 +392,7 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
                     A.trace[(size_t)run * A.max_iters + it] = tr;
                 }
                 if (A.digest && TABU) {
-                    uint64_t h = 0xcbf29ce484222325ull;
-                    for (int mm = 0; mm < n; mm++)
-                        for (int v = 0; v < V; v++) {
-                            int ev = R.E[mm * V + v];
-                            if (ev < it + 1) continue;
-                            int trip[3] = {mm, v, ev};
-                            for (int q3 = 0; q3 < 3; q3++)
-                                for (int by = 0; by < 4; by++) {
-                                    h ^= (uint64_t)(((uint32_t)trip[q3] >> (8 * by)) & 0xFFu);
-                                    h *= 0x100000001b3ull;
-                                }
-                        }
-                    A.digest[(size_t)run * A.max_iters + it] = h;
+                    A.digest[(size_t)run * A.max_iters + it] = tabu_digest(R.E, n, V, it);
                 }
             }
         }
@@ -461,7 +446,7 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
     uint64_t blocks64 = (N + threads - 1) / threads;
     int blocks = (int)(blocks64 < (uint64_t)n_sm * 8 ? blocks64 : (uint64_t)n_sm * 8);
     if (blocks < 1) blocks = 1;
-    size_t smem = (size_t)(I.n + I.NC) * 4;
+    size_t smem = 0;
     if (mode == 1)
         k_eval_dump<true><<<blocks, threads, smem, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
     else

@@ -16,6 +16,7 @@ struct RunViewG {
 
 struct SearchArgs {
     DevInst inst;
+    int32_t n_runs;
     const int32_t *start_ptr, *start_ms;   // [R][V+1], [R][n] or shared
     int32_t shared_start;
     const uint64_t *seeds;                 // [R] or null -> seed
@@ -37,6 +38,9 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
                              uint32_t mask, int32_t *delta, uint8_t *flags, unsigned long long *best_key, uint64_t N,
                              int n_sm, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st);
+void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
+                size_t *run_bytes);
+cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st);
 cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
                        cudaStream_t st);
 

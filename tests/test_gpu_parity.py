@@ -311,3 +311,56 @@ def _compare_run_mask(A, ctx, O, h, p, m):
     g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True)
     o = O.search(p, m, mode=1, tenure=10, max_iters=300, mask=1)
     assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and g["best_obj"] == o["best_obj"]
+
+
+@pytest.mark.parametrize("cfg,runs,iters", [("tiny", 64, 200), ("ontario", 64, 300), ("large", 6, 30)])
+def test_batch_kernel_parity_configs(A, ctx, oracle_mod, cfg, runs, iters):
+    """The one-run-per-warp batch kernel on every instance shape it accepts, NS and TS,
+    with per-run seeds; sampled runs compared with the oracle trace by trace."""
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    c = instgen.CONFIGS[cfg]
+    p, m = start_of(O, inst)
+    seeds = np.arange(1, runs + 1, dtype=np.uint64)
+    for mode in (1, 0):
+        res = np.zeros(runs, A.RESULT_DTYPE)
+        tr = np.zeros((runs, iters), A.TRACE_DTYPE)
+        bp = np.zeros((runs, inst.n_vehicles + 1), np.int32)
+        bm = np.zeros((runs, inst.n_missions), np.int32)
+        prm = A.params(mode=mode, tenure=c.tenure, max_iters=iters, kick=4, trace_level=1)
+        A.as_batch_run(ctx, h, runs, p, m, prm, seeds, shared_start=True, results=res, best_ptr_out=bp,
+                       best_missions_out=bm, trace_out=tr)
+        for r in sorted({0, runs // 2, runs - 1}):
+            o = O.search(p, m, mode=mode, tenure=c.tenure, max_iters=iters, seed=int(seeds[r]), kick=4)
+            k = o["iters_done"]
+            assert res[r]["iters_done"] == k and res[r]["stop_reason"] == o["stop_reason"]
+            assert (tr[r]["idx"][:k] == o["trace"]["idx"]).all()
+            assert (tr[r]["cur"][:k] == o["trace"]["cur"]).all() and (tr[r]["cls"][:k] == o["trace"]["cls"]).all()
+            assert res[r]["best_obj"] == o["best_obj"] and routes_of(bp[r], bm[r]) == routes_of(*o["best"])
+
+
+def test_batch_per_run_starts(A, ctx, oracle_mod):
+    """Distinct start schedules per run (shared_start = 0)."""
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    starts = [O.kick(p, m, s, 10)[1] for s in range(1, 9)]
+    R = len(starts)
+    sp = np.stack([s[0] for s in starts]).astype(np.int32)
+    sm = np.stack([s[1] for s in starts]).astype(np.int32)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    prm = A.params(mode=1, tenure=10, max_iters=150)
+    A.as_batch_run(ctx, h, R, sp, sm, prm, np.zeros(R, np.uint64), shared_start=False, results=res)
+    for r in range(R):
+        o = O.search(sp[r], sm[r], mode=1, tenure=10, max_iters=150)
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["best_iter"] == o["best_iter"]
+    # an infeasible start in a batch reports stop_reason 3 and the call still succeeds
+    sm2 = sm.copy()
+    sm2[3] = sm2[3][::-1]
+    sp2 = sp.copy()
+    sp2[3] = np.array([0] + [inst.n_missions] * inst.n_vehicles, np.int32)
+    A.as_batch_run(ctx, h, R, sp2, sm2, prm, np.zeros(R, np.uint64), shared_start=False, results=res)
+    assert res[3]["stop_reason"] == A.AS_STOP_INFEASIBLE_START
+    assert res[0]["stop_reason"] == A.AS_STOP_MAX_ITERS
