@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC) 
                     ok = ok & (same ? (rem_ok & (ins <= intra_lim)) : (inter_ok & (ins <= c_slk[k])));
                     bool adm;
                     if (TABU) {
-                        const bool tabu = (int)Erow[b & 0x7FFF] >= it;
+                        const bool tabu = (int)Erow[max(b, 0)] >= it;
                         adm = !tabu | (delta < asp);
                     } else {
                         adm = delta < 0;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC) 
                     bool adm;
                     if (TABU) {
                         const int m2c = m2 < n ? m2 : 0;
-                        const bool tabu = ((int)Erow[b & 0x7FFF] >= it) | ((int)E[m2c * V + a] >= it);
+                        const bool tabu = ((int)Erow[max(b, 0)] >= it) | ((int)E[m2c * V + a] >= it);
                         adm = !tabu | (delta < asp);
                     } else {
                         adm = delta < 0;
