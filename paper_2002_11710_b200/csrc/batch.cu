@@ -124,13 +124,6 @@ __device__ __forceinline__ T bcast(T v) {
     return __shfl_sync(0xFFFFFFFFu, v, 0);
 }
 
-// Rare path: an adjacent swap whose two deadlines are equal (the only case in
-// which it can be feasible on a feasible state), via engine code.
-template <class MV, class RV>
-__device__ __noinline__ MoveEval adjacent_swap(const MV &M, const RV &R, int m1, int m2, uint32_t mask, int it) {
-    return swap_eval(M, R, m1, m2, mask, it);
-}
-
 template <bool TABU, class TT, class ET>
 __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -293,194 +286,201 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC) 
         uint64_t kmin = KEY_NONE;
         const int asp = (int)(best - cur);   // aspiration: cur + delta < best  <=>  delta < asp
 
+        // Per-lane best inside a block: 32-bit key (class << 31 | delta + 2^30) plus
+        // the index.  Each lane visits its items in increasing index order inside a
+        // block, so a strict '<' keeps the lowest index among equal keys; blocks are
+        // merged through the 64-bit key.
+        constexpr int NEG = -(1 << 29);
+        const bool en_inter_r = (mask & 1u) != 0, en_intra_r = (mask & 2u) != 0;
+        const bool en_inter_s = (mask & 4u) != 0, en_intra_s = (mask & 8u) != 0;
+
         // ============================ relocate block ============================
         for (int t0 = 0; t0 < S; t0 += 32 * KR) {
-            int c_info[KR], c_loc[KR], c_dep[KR], c_k[KR], c_wsv[KR], c_slk[KR];
+            int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_inf[KR];
 #pragma unroll
             for (int k = 0; k < KR; k++) {
                 const int t = t0 + lane + 32 * k;
-                int info = 0xFFFF, loc = 0, dp = 0, kk = 0, wsv = 0, slk = 0;
+                int t1 = 0, t2 = 0, dw = 0, kk = 0, wsv = NEG, slk = NEG, inf = 0xFFFF;
                 if (t < S) {
                     const int4 rs = RS4[t];
                     const int b = (int16_t)((uint32_t)rs.w >> 16);
                     if (b >= 0) {
                         const int4 cs = CS4[t];
                         const uint32_t vc = VC[b];
-                        info = (b & 0xFFFF) | ((vc & 0xFF) << 16) | (((vc >> 8) & 1) << 20);
-                        loc = (rs.w & 0xFFFF) | (cs.y << 16);     // endc | pick << 16
-                        dp = rs.x;
-                        kk = rs.z - rs.y;                          // svco - inc
-                        wsv = cs.x - rs.z;                         // w - svco
+                        const int cb = vc & 0xFF;
+                        t1 = (cb * NL + (rs.w & 0xFFFF)) * NLp;     // row of T_cb[endc(t)][.]
+                        t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb
+                        dw = -rs.x;                                  // -dep(pred t)
+                        kk = rs.z - rs.y;                            // svco(t) - inc(t)
+                        wsv = cs.x - rs.z;                           // w(t) - svco(t)
                         slk = P - F[b];
+                        inf = (b & 0xFFFF) | (cb << 16) | (((vc >> 8) & 1) << 20);
                     }
                 }
-                c_info[k] = info;
-                c_loc[k] = loc;
-                c_dep[k] = dp;
-                c_k[k] = kk;
-                c_wsv[k] = wsv;
-                c_slk[k] = slk;
+                c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk;
+                c_inf[k] = inf;
             }
+            uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
             for (int m = 0; m < n; m++) {
                 const int4 rm = RS4[m];
                 const int a = (int16_t)((uint32_t)rm.w >> 16);
                 if (a < 0) continue;
                 const int s = LK[m] & 0xFFFF;
-                const int4 cm = CS4[m];
                 const int4 rsx = RS4[s];
-                const int w_s = *reinterpret_cast<const int32_t *>(CS + s * 16);
-                const int pick_s = *reinterpret_cast<const uint16_t *>(CS + s * 16 + 4);
+                const int4 csx = CS4[s];
                 const int ca = VC[a] & 0xFF;
-                const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + pick_s] + rsx.z;
-                const int rem = Dps - rm.y - rsx.y;
-                const bool rem_ok = rm.x + Dps <= w_s;
+                const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+                if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
+                const int rem = Dps - rm.y - rsx.y;   // removal delta d(p,s) - d(p,m) - d(m,s)
+                const int4 cm = CS4[m];
                 const int Fa = F[a];
-                const bool inter_ok = rem_ok && (Fa + rem <= P);
+                const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
                 const int intra_lim = P - Fa - rem;
-                const int w_m = cm.x, pick_m = cm.y & 0xFFFF, del_m = (uint32_t)cm.y >> 16;
+                const int w_m = cm.x, pick_m = cm.y & 0xFFFF, rowD = ((uint32_t)cm.y >> 16) * NLp;
                 const int svm0 = cm.z, svm1 = cm.w;
                 const bool heli_m = MH[m] != 0;
                 const ET *Erow = TABU ? E + m * V : nullptr;
-                const uint32_t base = (uint32_t)m * (uint32_t)S;
+                const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
 #pragma unroll
                 for (int k = 0; k < KR; k++) {
                     const int t = t0 + lane + 32 * k;
-                    const int info = c_info[k];
-                    const int b = (int)(int16_t)(info & 0xFFFF);
-                    const int cb = (info >> 16) & 0xF;
-                    const bool hok = (info >> 20) & 1;
-                    const bool same = b == a;
-                    // branch-free: every lane evaluates, invalid lanes are masked out of the key
-                    bool ok = (b >= 0) & (t != m) & (t != s) & ((mask & (same ? 2u : 1u)) != 0);
-                    const int e = c_loc[k] & 0xFFFF, pk = (uint32_t)c_loc[k] >> 16;
-                    const int T1 = (int)Ts[(cb * NL + e) * NLp + pick_m];
-                    const int T2 = (int)Ts[(cb * NL + del_m) * NLp + pk];
-                    const int x1 = T1 + (cb ? svm1 : svm0);
+                    const int inf = c_inf[k];
+                    const int b = (int)(int16_t)(inf & 0xFFFF);
+                    const bool cb1 = (inf >> 16) & 1;
+                    const bool hok = (inf >> 20) & 1;
+                    const int T1 = (int)Ts[c_t1[k] + pick_m];
+                    const int T2 = (int)Ts[c_t2[k] + rowD];
+                    const int x1 = T1 + (cb1 ? svm1 : svm0);
                     const int ins = x1 + T2 + c_k[k];
                     const int delta = rem + ins;
-                    ok = ok & (hok | !heli_m) & (x1 <= w_m - c_dep[k]) & (T2 <= c_wsv[k] - w_m);
-                    ok = ok & (same ? (rem_ok & (ins <= intra_lim)) : (inter_ok & (ins <= c_slk[k])));
+                    const bool same = b == a;
+                    const int lim = same ? intra_lim : c_slk[k] + inter_bias;
+                    const int mg = min(min(w_m + c_dw[k] - x1, c_wsv[k] - w_m - T2), lim - ins);
+                    const bool ok = (mg >= 0) & (t != m) & (t != s) & (same ? en_intra_r : en_inter_r) &
+                                    (hok | !heli_m);
                     bool adm;
-                    if (TABU) {
-                        const bool tabu = (int)Erow[max(b, 0)] >= it;
-                        adm = !tabu | (delta < asp);
-                    } else {
-                        adm = delta < 0;
-                    }
-                    const uint64_t key = make_key(adm ? 0 : 1, delta, base + (uint32_t)t);
-                    kmin = (ok && key < kmin) ? key : kmin;
+                    if (TABU) adm = ((int)Erow[max(b, 0)] < it) | (delta < asp);
+                    else adm = delta < 0;
+                    uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+                    k32 = ok ? k32 : 0xFFFFFFFFu;
+                    const bool better = k32 < bk32;
+                    bk32 = better ? k32 : bk32;
+                    bidx = better ? base + 32 * k : bidx;
                 }
             }
+            const uint64_t kb = bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+            kmin = kb < kmin ? kb : kmin;
         }
 
         // ============================== swap block ==============================
-        for (int c0 = 0; c0 < n; c0 += 32 * KS) {
-            int q_info[KS], q_loc[KS], q_dls[KS], q_s2[KS], q_dep[KS], q_w[KS], q_kb[KS], q_ws2[KS], q_slk[KS];
-            int q_svc0[KS], q_svc1[KS];
+        // m2 chunks of 32*KS aligned to the top (hi = n, n - 64, ...) so only the
+        // lowest chunk is ragged; adjacent pairs are excluded here and scored exactly
+        // by the generic three-link formula below.
+        for (int hi = n; hi > 1; hi -= 32 * KS) {
+            const int lo = hi - 32 * KS;
+            int q_ps[KS], q_sv0[KS], q_sv1[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS],
+                q_ws2[KS], q_slk[KS], q_inf[KS];
 #pragma unroll
             for (int k = 0; k < KS; k++) {
-                const int m2 = c0 + lane + 32 * k;
-                int info = 0xFFFF, loc = 0, dls = 0, s2 = 0, dp = 0, w2 = 0, kb = 0, ws2 = 0, slk = 0, sv0 = 0, sv1 = 0;
-                if (m2 < n) {
+                const int m2 = lo + lane + 32 * k;
+                int ps = 0, sv0 = 0, sv1 = 0, d2 = 0, e2 = 0, p2 = 0, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
+                    inf = 0xFFFF;
+                if (m2 >= 0) {
                     const int4 r2 = RS4[m2];
                     const int b = (int16_t)((uint32_t)r2.w >> 16);
                     if (b >= 0) {
                         const int4 c2 = CS4[m2];
                         const uint32_t vc = VC[b];
-                        s2 = LK[m2] & 0xFFFF;
+                        const int cb = vc & 0xFF;
+                        const int s2 = LK[m2] & 0xFFFF;
                         const int4 rs2 = RS4[s2];
-                        const int w_s2 = *reinterpret_cast<const int32_t *>(CS + s2 * 16);
-                        const int pick_s2 = *reinterpret_cast<const uint16_t *>(CS + s2 * 16 + 4);
-                        info = (b & 0xFFFF) | ((vc & 0xFF) << 16) | ((int)MH[m2] << 20) | (((vc >> 8) & 1) << 21);
-                        loc = (r2.w & 0xFFFF) | ((c2.y & 0xFFFF) << 16);           // endc2 | pick2 << 16
-                        dls = ((uint32_t)c2.y >> 16) | (pick_s2 << 16);            // del2 | pick(s2) << 16
-                        dp = r2.x;
-                        w2 = c2.x;
-                        kb = rs2.z - r2.y - rs2.y;                                 // svco(s2) - inc2 - inc(s2)
-                        ws2 = w_s2 - rs2.z;                                        // w(s2) - svco(s2)
-                        slk = P - F[b];
+                        const int4 cs2 = CS4[s2];
+                        ps = (c2.y & 0xFFFF) | (s2 << 16);              // pick2 | s2 << 16
                         sv0 = c2.z;
                         sv1 = c2.w;
+                        d2 = ((uint32_t)c2.y >> 16) * NLp;               // row del2 (any class)
+                        e2 = (cb * NL + (r2.w & 0xFFFF)) * NLp;           // row T_cb[endc2]
+                        p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
+                        w2 = c2.x;
+                        dep2 = r2.x;
+                        kb = rs2.z - r2.y - rs2.y;                        // svco(s2) - inc2 - inc(s2)
+                        ws2 = cs2.x - rs2.z;                              // w(s2) - svco(s2)
+                        slk = P - F[b];
+                        inf = (b & 0xFFFF) | (cb << 16) | ((int)MH[m2] << 20) | (((vc >> 8) & 1) << 21);
                     }
                 }
-                q_info[k] = info;
-                q_loc[k] = loc;
-                q_dls[k] = dls;
-                q_s2[k] = s2;
-                q_dep[k] = dp;
-                q_w[k] = w2;
-                q_kb[k] = kb;
-                q_ws2[k] = ws2;
-                q_slk[k] = slk;
-                q_svc0[k] = sv0;
-                q_svc1[k] = sv1;
+                q_ps[k] = ps; q_sv0[k] = sv0; q_sv1[k] = sv1; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2;
+                q_w2[k] = w2; q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_inf[k] = inf;
             }
-            const int last_row = min(n - 2, c0 + 32 * KS - 2);
-            for (int m1 = 0; m1 <= last_row; m1++) {
+            uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+            for (int m1 = 0; m1 <= hi - 2; m1++) {
                 const int4 r1 = RS4[m1];
                 const int a = (int16_t)((uint32_t)r1.w >> 16);
                 if (a < 0) continue;
                 const int s1 = LK[m1] & 0xFFFF;
                 const int4 c1 = CS4[m1];
                 const int4 rs1 = RS4[s1];
-                const int w_s1 = *reinterpret_cast<const int32_t *>(CS + s1 * 16);
-                const int pick_s1 = *reinterpret_cast<const uint16_t *>(CS + s1 * 16 + 4);
+                const int4 cs1 = CS4[s1];
                 const uint32_t vca = VC[a];
                 const int ca = vca & 0xFF;
                 const bool hoka = (vca >> 8) & 1;
-                const int endc1 = r1.w & 0xFFFF, depc1 = r1.x;
-                const int pick1 = c1.y & 0xFFFF, del1 = (uint32_t)c1.y >> 16, w1 = c1.x;
+                const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
+                const int col_ta2 = ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
+                const int pick1 = c1.y & 0xFFFF, row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+                const int depc1 = r1.x, w1 = c1.x;
                 const bool heli1 = MH[m1] != 0;
-                const int wsv1 = w_s1 - rs1.z;                 // w(s1) - svco(s1)
-                const int ka = rs1.z - r1.y - rs1.y;           // svco(s1) - inc1 - inc(s1)
+                const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
+                const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
                 const int slkA = P - F[a];
                 const int sv10 = c1.z, sv11 = c1.w;
                 const ET *Erow = TABU ? E + m1 * V : nullptr;
-                const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n;
+                const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
 #pragma unroll
                 for (int k = 0; k < KS; k++) {
-                    if (c0 + 32 * k + 31 <= m1) continue;     // whole sub-chunk on or below the diagonal
-                    const int m2 = c0 + lane + 32 * k;
-                    const int info = q_info[k];
-                    const int b = (int)(int16_t)(info & 0xFFFF);
-                    const int cb = (info >> 16) & 0xF;
-                    const bool h2 = (info >> 20) & 1, hokb = (info >> 21) & 1;
+                    if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+                    const int m2 = lo + lane + 32 * k;
+                    const int inf = q_inf[k];
+                    const int b = (int)(int16_t)(inf & 0xFFFF);
+                    const bool cb1 = (inf >> 16) & 1;
+                    const bool h2 = (inf >> 20) & 1, hokb = (inf >> 21) & 1;
+                    const int pick2 = q_ps[k] & 0xFFFF, s2 = (uint32_t)q_ps[k] >> 16;
                     const bool same = a == b;
-                    bool ok = (m2 > m1) & (b >= 0) & ((mask & (same ? 8u : 4u)) != 0);
-                    const bool adj = (s1 == m2) || (q_s2[k] == m1);
-                    const int e2 = q_loc[k] & 0xFFFF, p2 = (uint32_t)q_loc[k] >> 16;
-                    const int d2 = q_dls[k] & 0xFFFF, ps2 = (uint32_t)q_dls[k] >> 16;
-                    const int ya1 = (int)Ts[(ca * NL + endc1) * NLp + p2] + (ca ? q_svc1[k] : q_svc0[k]); // p1 -> m2
-                    const int Ta2 = (int)Ts[(ca * NL + d2) * NLp + pick_s1];                           // m2 -> s1
-                    const int yb1 = (int)Ts[(cb * NL + e2) * NLp + pick1] + (cb ? sv11 : sv10);        // p2 -> m1
-                    const int Tb2 = (int)Ts[(cb * NL + del1) * NLp + ps2];                             // m1 -> s2
+                    const int ya1 = (int)Ts[row_ya1 + pick2] + (ca ? q_sv1[k] : q_sv0[k]);   // p1 -> m2
+                    const int Ta2 = (int)Ts[col_ta2 + q_d2[k]];                              // m2 -> s1
+                    const int yb1 = (int)Ts[q_e2[k] + pick1] + (cb1 ? sv11 : sv10);          // p2 -> m1
+                    const int Tb2 = (int)Ts[q_p2[k] + row_tb2];                              // m1 -> s2
                     const int da = ya1 + Ta2 + ka;
                     const int db = yb1 + Tb2 + q_kb[k];
-                    int delta = da + db;
-                    bool f = (!h2 | hoka) & (!heli1 | hokb) & (depc1 + ya1 <= q_w[k]) & (q_w[k] + Ta2 <= wsv1) &
-                             (q_dep[k] + yb1 <= w1) & (Tb2 <= q_ws2[k] - w1);
-                    f = f & (same ? (delta <= slkA) : ((da <= slkA) & (db <= q_slk[k])));
-                    if (adj) {
-                        // adjacent pair: feasible only if both deadlines are equal;
-                        // then take the exact three-link formula.
-                        f = false;
-                        if (ok && q_w[k] == w1) {
-                            MoveEval ev = adjacent_swap(M, R, m1, m2, mask, it);
-                            f = ev.feasible;
-                            delta = ev.delta;
-                        }
-                    }
-                    ok = ok & f;
+                    const int delta = da + db;
+                    const int mf = same ? slkA - delta : min(slkA - da, q_slk[k] - db);
+                    const int mg = min(min(min(q_w2[k] - depc1 - ya1, wsv1 - q_w2[k] - Ta2),
+                                           min(w1 - q_dep2[k] - yb1, q_ws2[k] - w1 - Tb2)), mf);
+                    const bool ok = (mg >= 0) & (m2 > m1) & (s1 != m2) & (s2 != m1) &
+                                    (same ? en_intra_s : en_inter_s) & (!h2 | hoka) & (!heli1 | hokb);
                     bool adm;
-                    if (TABU) {
-                        const int m2c = m2 < n ? m2 : 0;
-                        const bool tabu = ((int)Erow[max(b, 0)] >= it) | ((int)E[m2c * V + a] >= it);
-                        adm = !tabu | (delta < asp);
-                    } else {
-                        adm = delta < 0;
-                    }
-                    const uint64_t key = make_key(adm ? 0 : 1, delta, base + (uint32_t)m2);
-                    kmin = (ok && key < kmin) ? key : kmin;
+                    if (TABU) adm = (((int)Erow[max(b, 0)] < it) & ((int)E[max(m2, 0) * V + a] < it)) | (delta < asp);
+                    else adm = delta < 0;
+                    uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+                    k32 = ok ? k32 : 0xFFFFFFFFu;
+                    const bool better = k32 < bk32;
+                    bk32 = better ? k32 : bk32;
+                    bidx = better ? base + 32 * k : bidx;
+                }
+            }
+            const uint64_t kb = bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+            kmin = kb < kmin ? kb : kmin;
+        }
+        // adjacent pairs (x, succ x): the exact three-link formula (engine.cuh)
+        if (mask & 8u) {
+            for (int x = lane; x < n; x += 32) {
+                const int g = LK[x] & 0xFFFF;
+                if (R.veh[x] < 0 || g >= n) continue;
+                const int m1 = min(x, g), m2 = max(x, g);
+                const MoveEval e = swap_eval(M, R, m1, m2, mask, it);
+                const int cls = move_class<TABU>(e, cur, best);
+                if (cls >= 0) {
+                    const uint64_t key = make_key(cls, e.delta, Rb + (uint32_t)m1 * (uint32_t)n + (uint32_t)m2);
+                    kmin = key < kmin ? key : kmin;
                 }
             }
         }
