@@ -213,6 +213,8 @@ struct DevBuf {
 struct InstDev {
     uint64_t uid = 0;
     DevInst d{};
+    void *Tpad = nullptr;     // padded travel-time table (uint16 when every entry fits)
+    int tpad_bytes = 4;
     std::vector<void *> allocs;
 };
 
@@ -346,6 +348,16 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
     D.d.svc = (const int32_t *)svc;
     D.d.n = I->n; D.d.V = I->V; D.d.NL = I->NL; D.d.NC = I->NC; D.d.P = I->P; D.d.DAY = I->DAY;
     D.d.maxT = I->maxT;
+    D.tpad_bytes = I->maxT <= 65535 ? 2 : 4;
+    {
+        const int NLp = padded_stride_host(I->NL, D.tpad_bytes);
+        void *tp = nullptr;
+        CUDA_TRY(cudaMalloc(&tp, (size_t)I->NC * I->NL * NLp * D.tpad_bytes + 16));
+        D.allocs.push_back(tp);
+        CUDA_TRY(launch_pad_table(D.d.T, tp, I->NC, I->NL, NLp, D.tpad_bytes, s));
+        ctx->launches++;
+        D.Tpad = tp;
+    }
     auto &slot = ctx->insts[I];
     slot = std::move(D);
     *out = &slot.d;
@@ -549,7 +561,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int n = I->n, V = I->V;
     int T_smem, E_smem;
     size_t smem;
-    if ((st = pick_layout(ctx, I, tabu, &T_smem, &E_smem, &smem)) != AS_OK) return st;
+    const bool kfit = pick_layout(ctx, I, tabu, &T_smem, &E_smem, &smem) == AS_OK;
+    if (!kfit) { T_smem = 0; E_smem = 0; smem = 0; }
     const int force_T = env_int("AIRSCHED_T_SMEM", -1);
     if (force_T == 0 && T_smem) {
         T_smem = 0;
@@ -611,14 +624,69 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !tabu_out;
     const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
     bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single));
+    // single large instances: one persistent cooperative grid (k_grid)
+    bool use_grid = false;
+    GridArgs GA;
+    memset(&GA, 0, sizeof(GA));
+    size_t grid_smem = 0;
+    int grid_blocks = 0;
+    if (single && compact_ok) {
+        const int want_grid = env_int("AIRSCHED_GRID", -1);
+        const bool kfits = kfit;
+        const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000);
+        if (want_grid == 1 || (want_grid == -1 && (big || !kfits))) {
+            auto &D = ctx->insts[I];
+            const int tb = D.tpad_bytes;
+            struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
+            for (auto o : gopts) {
+                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, 4, o.t, o.e && tabu, tabu);
+                if (b <= ctx->max_smem) {
+                    GA.T_smem = o.t;
+                    GA.E_smem = o.e && tabu;
+                    grid_smem = b;
+                    use_grid = true;
+                    break;
+                }
+            }
+            if (use_grid) {
+                int occ = 0;
+                int coop = 0;
+                cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+                use_grid = coop != 0;
+                grid_blocks = ctx->n_sm;
+                (void)occ;
+                GA.Tglobal = D.Tpad;
+                void *p;
+                if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
+                GA.gkey = (unsigned long long *)p;
+                CUDA_TRY(cudaMemsetAsync(p, 0xFF, 3 * 8, ctx->stream));
+                if ((st = scratch(ctx, "g_bs", (size_t)S * 4, &p)) != AS_OK) return st;
+                GA.BS = (int32_t *)p;
+                if (tabu && !GA.E_smem) {
+                    if ((st = scratch(ctx, "g_E", (size_t)n * V * 4 + 4, &p)) != AS_OK) return st;
+                    GA.Eglobal = (int32_t *)p;
+                }
+                const int warps_all = grid_blocks * 32;
+                const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
+                const int64_t pairs = (int64_t)n * nTC + (int64_t)n * nSC / 2;
+                GA.G = (int)std::max<int64_t>(1, pairs / (4 * (int64_t)warps_all));
+                GA.G = std::max(1, env_int("AIRSCHED_GRID_G", GA.G));
+            }
+        }
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    if (use_batch) {
+    if (use_grid) {
+        CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, 768, grid_smem, ctx->stream));
+        ctx->launches += A.best_ptr ? 2 : 1;
+        ctx->launches--;   // counted once below
+    } else if (use_batch) {
         int rpc = (int)std::min<int64_t>(28, std::min<int64_t>(rpc_fit, (n_runs + ctx->n_sm - 1) / ctx->n_sm));
         rpc = std::max(1, env_int("AIRSCHED_RPC", rpc));
         rpc = std::min(rpc, std::min(28, rpc_fit));
         size_t smem_b = sh_b + (size_t)rpc * run_b;
         CUDA_TRY(launch_batch(A, tabu ? 1 : 0, rpc, tbytes, ebytes, smem_b, ctx->stream));
     } else {
+        if (!kfit) return fail(AS_ERR_UNSUPPORTED, "instance too large for the per-CTA kernel (n=%d, V=%d)", n, V);
         int threads;
         if (single) {
             int64_t t = 64;

@@ -1,0 +1,75 @@
+// compact.cuh -- compact array-of-structs layout shared by the batched and the
+// grid-wide kernels: views with the engine.cuh interface over the records
+//   CS[x] (16 B): {w, pick | del << 16, svc_class0, svc_class1}   (constants)
+//   RS[x] (16 B): {depc, inc, svco, endc | veh << 16}             (per replica)
+//   LK[x] (4 B):  {succ | pred << 16}                             (per replica)
+#pragma once
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace airsched {
+
+__host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline int padded_stride(int NL, int tbytes) {
+    if (tbytes == 2) {            // row stride in halfwords = 2 * odd number of words
+        int w = (NL + 1) / 2;
+        if ((w & 1) == 0) w++;
+        return 2 * w;
+    }
+    return (NL & 1) ? NL : NL + 1; // odd number of words
+}
+
+// Mission view over the AoS records (same interface as MissionViewT).
+template <class TT>
+struct CompactMV {
+    const TT *T;
+    const unsigned char *CS;
+    const uint8_t *MH;
+    const uint32_t *VC;
+    const uint8_t *CH;
+    int32_t n, V, NL, NLp, P, DAY;
+    __device__ __forceinline__ int cls(int v) const { return VC[v] & 0xFF; }
+    __device__ __forceinline__ int hok(int c) const { return CH[c]; }
+    __device__ __forceinline__ int vl(int v) const { return (int)(VC[v] >> 16); }
+    __device__ __forceinline__ int dl(int m) const { return *reinterpret_cast<const uint16_t *>(CS + m * 16 + 6); }
+    __device__ __forceinline__ int hl(int m) const { return MH[m]; }
+    __device__ __forceinline__ int sv(int c, int m) const {
+        return *reinterpret_cast<const int32_t *>(CS + m * 16 + 8 + 4 * c);
+    }
+};
+
+template <class ET>
+struct CompactRV {
+    Field<uint16_t, 4, 0> succ;
+    Field<uint16_t, 4, 2> pred;
+    Field<int16_t, 16, 14> veh;
+    Field<uint16_t, 16, 12> endc;
+    Field<int32_t, 16, 0> depc;
+    Field<int32_t, 16, 4> inc;
+    Field<int32_t, 16, 8> svco;
+    Field<uint16_t, 16, 4> pick_s;
+    Field<int32_t, 16, 0> w_s;
+    int32_t *F;
+    ET *E;
+};
+
+__device__ __forceinline__ uint64_t wmin(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t u = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+template <class T>
+__device__ __forceinline__ T bcast(T v) {
+    return __shfl_sync(0xFFFFFFFFu, v, 0);
+}
+
+// FULL: every move kind enabled (move_mask == 15): the per-move mask test is compiled out.
+// L (the shared-memory layout) and NLp are computed on the host and passed by value,
+// so the offsets are kernel-parameter constants rather than live registers.
+}  // namespace airsched

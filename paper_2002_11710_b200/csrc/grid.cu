@@ -1,0 +1,367 @@
+// grid.cu -- k_grid: ONE large instance on the whole GPU (configs C4, C5).
+//
+// Persistent cooperative kernel, one CTA per SM.  Every CTA holds a replica of
+// the run state (slot records, links, route totals; the tabu matrix too when it
+// fits) in shared memory; the travel-time table is staged in shared memory
+// when it fits, otherwise read from an L2-resident padded copy.  Per iteration:
+//   1. every warp scores its share of the tiles (score.cuh: relocate tiles,
+//      top-aligned swap tiles, adjacent-swap tiles), reduces to one packed key
+//      per CTA, and thread 0 folds it into a global key with atomicMin;
+//   2. grid.sync();
+//   3. every CTA reads the winning key and applies the same move to its own
+//      replica (identical integer arithmetic => identical replicas); CTA 0 also
+//      writes the trace and the best schedule.
+// One grid barrier per iteration; the keys are triple-buffered so a CTA that
+// races ahead into iteration it+1 never sees a slot that is still being read.
+// The tabu matrix, when it lives in global memory, is written by every CTA with
+// identical values, so each CTA's own reads after its apply are up to date.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "compact.cuh"
+#include "engine.cuh"
+#include "launch.h"
+#include "score.cuh"
+
+namespace cg = cooperative_groups;
+
+constexpr int GRID_THREADS = 768;   // 24 warps per SM: ~85 registers per thread
+
+namespace airsched {
+
+__host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, int NLp, int tbytes, int ebytes,
+                                                  bool T_smem, bool E_smem, bool tabu) {
+    GridLayout L;
+    const int S = n + V;
+    int o = 0;
+    L.T = o; o = al16(o + (T_smem ? NC * NL * NLp * tbytes : 0));
+    L.CS = o; o = al16(o + S * 16);
+    L.MH = o; o = al16(o + n);
+    L.VC = o; o = al16(o + V * 4);
+    L.CH = o; o = al16(o + NC);
+    L.RS = o; o = al16(o + S * 16);
+    L.LK = o; o = al16(o + S * 4);
+    L.F = o; o = al16(o + V * 4);
+    L.E = o; o = al16(o + (tabu && E_smem ? n * V * ebytes : 0));
+    L.red = o; o = al16(o + 32 * 8 + 64);
+    L.total = o;
+    return L;
+}
+
+size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu) {
+    return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
+}
+
+struct GridTiles {
+    int nTC, nSC, nAdj, nRG, G;   // t-chunks, swap chunks, adjacent tiles, row groups, rows per group
+    int n_reloc, n_swap, n_total; // tile counts
+};
+
+__host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
+    GridTiles T;
+    const int S = n + V;
+    T.G = G;
+    T.nTC = (S + 32 * KR - 1) / (32 * KR);
+    T.nSC = n > 1 ? (n - 1 + 32 * KS - 1) / (32 * KS) : 0;
+    T.nRG = (n + G - 1) / G;
+    T.nAdj = (n + 31) / 32;
+    T.n_reloc = T.nTC * T.nRG;
+    T.n_swap = T.nSC * T.nRG;
+    T.n_total = T.n_reloc + T.n_swap + T.nAdj;
+    return T;
+}
+
+// Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
+template <bool TABU, bool FULL, class TT, class ET, class MV, class RV>
+__device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
+                                                const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
+                                                int it, long long cur, long long best, int lane) {
+    const int n = SC.n;
+    const int asp = (int)(best - cur);
+    uint64_t kmin = KEY_NONE;
+    for (int tile = tlo + gwarp; tile < thi; tile += nwarps_all) {
+        uint64_t kb = KEY_NONE;
+        if (tile < GT.n_reloc) {
+            const int c = tile % GT.nTC, g = tile / GT.nTC;
+            const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
+            kb = score_reloc<TABU, FULL>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
+        } else if (tile < GT.n_reloc + GT.n_swap) {
+            const int r = tile - GT.n_reloc;
+            const int j = r % GT.nSC, g = r / GT.nSC;
+            const int hi = n - j * 32 * KS;
+            const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
+            if (m_lo < m_hi) kb = score_swap<TABU, FULL>(SC, hi, m_lo, m_hi, it, asp, lane);
+        } else {
+            const int x = (tile - GT.n_reloc - GT.n_swap) * 32 + lane;
+            if (x < n && (FULL || (SC.mask & 8u))) {
+                const int gg = SC.LK[x] & 0xFFFF;
+                if (R.veh[x] >= 0 && gg < n) {
+                    const int m1 = min(x, gg), m2 = max(x, gg);
+                    const MoveEval e = swap_eval(M, R, m1, m2, SC.mask, it);
+                    const int cls = move_class<TABU>(e, cur, best);
+                    if (cls >= 0) kb = make_key(cls, e.delta, SC.Rb + (uint32_t)m1 * (uint32_t)n + (uint32_t)m2);
+                }
+            }
+        }
+        kmin = kb < kmin ? kb : kmin;
+    }
+    return kmin;
+}
+
+template <bool TABU, class TT, class ET, bool FULL>
+__global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    cg::grid_group grid = cg::this_grid();
+    const DevInst &I = A.inst;
+    const int n = I.n, V = I.V, S = n + V, NC = I.NC, NL = I.NL, NLp = GA.NLp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const GridLayout L = GA.L;
+    TT *Ts = GA.T_smem ? reinterpret_cast<TT *>(smem + L.T) : reinterpret_cast<TT *>(const_cast<void *>(GA.Tglobal));
+    int4 *CS4 = reinterpret_cast<int4 *>(smem + L.CS);
+    uint8_t *MH = smem + L.MH;
+    uint32_t *VC = reinterpret_cast<uint32_t *>(smem + L.VC);
+    uint8_t *CH = smem + L.CH;
+    int4 *RS4 = reinterpret_cast<int4 *>(smem + L.RS);
+    uint32_t *LK = reinterpret_cast<uint32_t *>(smem + L.LK);
+    int32_t *F = reinterpret_cast<int32_t *>(smem + L.F);
+    ET *E = TABU ? (GA.E_smem ? reinterpret_cast<ET *>(smem + L.E) : reinterpret_cast<ET *>(GA.Eglobal)) : nullptr;
+    unsigned long long *red = reinterpret_cast<unsigned long long *>(smem + L.red);
+    int *ctrl = reinterpret_cast<int *>(smem + L.red + 32 * 8);
+
+    // ---- stage constants --------------------------------------------------
+    if (GA.T_smem)
+        for (int i = tid; i < NC * NL * NL; i += blockDim.x) {
+            int c = i / (NL * NL), r = (i / NL) % NL, col = i % NL;
+            Ts[(c * NL + r) * NLp + col] = (TT)I.T[i];
+        }
+    for (int x = tid; x < S; x += blockDim.x) {
+        int4 r;
+        if (x < n) {
+            r.x = I.w[x];
+            r.y = (I.pick[x] & 0xFFFF) | (I.del[x] << 16);
+            r.z = I.svc[x];
+            r.w = NC > 1 ? I.svc[n + x] : 0;
+        } else {
+            r.x = I.DAY;
+            r.y = (I.vloc[x - n] & 0xFFFF) | (I.vloc[x - n] << 16);
+            r.z = 0;
+            r.w = 0;
+        }
+        CS4[x] = r;
+    }
+    for (int i = tid; i < n; i += blockDim.x) MH[i] = I.heli[i];
+    for (int i = tid; i < V; i += blockDim.x) {
+        int c = I.vcls8[i];
+        VC[i] = (uint32_t)c | ((uint32_t)I.cls_heli[c] << 8) | ((uint32_t)I.vloc[i] << 16);
+    }
+    for (int i = tid; i < NC; i += blockDim.x) CH[i] = I.cls_heli[i];
+
+    CompactMV<TT> M;
+    M.T = Ts; M.CS = reinterpret_cast<unsigned char *>(CS4); M.MH = MH; M.VC = VC; M.CH = CH;
+    M.n = n; M.V = V; M.NL = NL; M.NLp = NLp; M.P = I.P; M.DAY = I.DAY;
+    CompactRV<ET> R;
+    unsigned char *RSb = reinterpret_cast<unsigned char *>(RS4);
+    R.succ.base = reinterpret_cast<unsigned char *>(LK); R.pred.base = reinterpret_cast<unsigned char *>(LK);
+    R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
+    R.pick_s.base = reinterpret_cast<unsigned char *>(CS4); R.w_s.base = reinterpret_cast<unsigned char *>(CS4);
+    R.F = F; R.E = E;
+
+    // ---- start schedule -> replica (every CTA) -----------------------------
+    for (int x = tid; x < S; x += blockDim.x) R.veh[x] = x < n ? (int16_t)-1 : (int16_t)(x - n);
+    if (TABU && (GA.E_smem || blockIdx.x == 0))
+        for (int i = tid; i < n * V; i += blockDim.x) E[i] = (ET)-1;
+    if (tid == 0) ctrl[0] = ctrl[1] = 0;
+    __syncthreads();
+    const int32_t *ptr = A.start_ptr, *ms = A.start_ms;
+    for (int v = tid; v < V; v += blockDim.x) {
+        int prev = n + v;
+        for (int i = ptr[v]; i < ptr[v + 1]; i++) {
+            int m = ms[i];
+            R.veh[m] = (int16_t)v;
+            R.succ[prev] = (uint16_t)m;
+            R.pred[m] = (uint16_t)prev;
+            prev = m;
+        }
+        R.succ[prev] = (uint16_t)(n + v);
+        R.pred[n + v] = (uint16_t)prev;
+    }
+    __syncthreads();
+    for (int x = tid; x < S; x += blockDim.x) refresh_slot(M, R, x);
+    __syncthreads();
+    for (int v = tid; v < V; v += blockDim.x) {
+        int f = 0, x = R.succ[n + v];
+        for (int g = 0; x < n && g <= n; g++) { f += R.inc[x]; x = R.succ[x]; }
+        F[v] = f + R.inc[n + v];
+    }
+    __syncthreads();
+
+    // ---- seeded kick (identical in every CTA) ------------------------------
+    __shared__ long long s_cur, s_best, s_start;
+    __shared__ int s_best_it, s_kicks;
+    if (tid == 0) {
+        int kicks = 0;
+        if (A.seed != 0 && n > 0) {
+            uint64_t s = A.seed;
+            const uint64_t Rb = (uint64_t)n * (uint64_t)S;
+            for (int k = 0; k < A.kick; k++)
+                for (int tr = 0; tr < 64; tr++) {
+                    uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
+                    MoveEval e = eval_index(M, R, idx, 0xFu, 0);
+                    if (e.valid && e.feasible) {
+                        apply_move(M, R, idx, e, 0, 0, false);
+                        kicks++;
+                        break;
+                    }
+                }
+        }
+        long long c = 0;
+        for (int v = 0; v < V; v++) c += F[v];
+        s_cur = s_best = s_start = c;
+        s_best_it = -1;
+        s_kicks = kicks;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
+    grid.sync();   // global tabu matrix initialised before anyone reads it
+
+    ScoreCtx<TT, ET> SC;
+    SC.Ts = Ts; SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
+    SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
+    SC.mask = A.mask;
+    const GridTiles GT = grid_tiles(n, V, GA.G);
+    const int gwarp = blockIdx.x * nwarps + warp, nwarps_all = gridDim.x * nwarps;
+    unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
+
+    int it = 0;
+    for (; it < A.max_iters; it++) {
+        const long long cur = s_cur, best = s_best;
+        uint64_t kmin = score_tiles<TABU, FULL>(SC, M, R, GT, 0, GT.n_total, gwarp, nwarps_all, it, cur, best, lane);
+        kmin = wmin(kmin);
+        if (lane == 0) red[warp] = kmin;
+        __syncthreads();
+        if (tid == 0) {
+            uint64_t k = red[0];
+            for (int w2 = 1; w2 < nwarps; w2++) k = red[w2] < k ? red[w2] : k;
+            if (k != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)k);
+            if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
+        }
+        grid.sync();
+        if (tid == 0) {
+            const uint64_t k = __ldcg(&gkey[it % 3]);
+            int stop = 0;
+            if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
+            else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
+            ctrl[0] = stop;
+            ctrl[1] = 0;
+            if (!stop) {
+                const uint32_t idx = key_idx(k);
+                MoveEval e = eval_index(M, R, idx, A.mask, it);
+                apply_move(M, R, idx, e, it, A.tenure, TABU);
+                const long long c = s_cur + e.delta;
+                s_cur = c;
+                if (c < s_best) {
+                    s_best = c;
+                    s_best_it = it;
+                    ctrl[1] = 1;
+                }
+                if (blockIdx.x == 0 && A.trace) {
+                    as_trace_rec tr;
+                    tr.cur = c;
+                    tr.best = s_best;
+                    tr.idx = idx;
+                    tr.delta = e.delta;
+                    tr.cls = key_cls(k);
+                    tr.it = it;
+                    A.trace[it] = tr;
+                }
+            }
+        }
+        __syncthreads();
+        if (ctrl[0]) break;
+        if (ctrl[1] && blockIdx.x == 0)
+            for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        as_run_result *res = A.results;
+        if (res) {
+            res->start_obj = s_start;
+            res->best_obj = s_best;
+            res->final_obj = s_cur;
+            res->best_iter = s_best_it;
+            res->iters_done = it;
+            res->stop_reason = ctrl[0] ? ctrl[0] : AS_STOP_MAX_ITERS;
+            res->kicks_applied = s_kicks;
+        }
+    }
+    if (blockIdx.x == 0 && A.tabu_out && TABU)
+        for (int i = tid; i < n * V; i += blockDim.x) A.tabu_out[i] = (int32_t)E[i];
+}
+
+// Best schedule (global BS successor array) -> CSR; one thread.
+__global__ void k_bs_to_csr(const int32_t *BS, int n, int V, int32_t *bp, int32_t *bm) {
+    if (threadIdx.x || blockIdx.x) return;
+    int pos = 0;
+    for (int v = 0; v < V; v++) {
+        bp[v] = pos;
+        int x = BS[n + v];
+        for (int g = 0; x < n && g < n; g++) { bm[pos++] = x; x = BS[x]; }
+    }
+    bp[V] = pos;
+}
+
+template <bool TABU, class TT, class ET, bool FULL>
+static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks, int threads, size_t smem,
+                            cudaStream_t st) {
+    auto kern = k_grid<TABU, TT, ET, FULL>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    SearchArgs a = A;
+    GridArgs g = GA;
+    void *args[] = {&a, &g};
+    return cudaLaunchCooperativeKernel((void *)kern, blocks, threads, args, smem, st);
+}
+
+cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
+                        cudaStream_t st) {
+    const DevInst &I = A.inst;
+    GA.NLp = padded_stride(I.NL, tbytes);
+    GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, 4, GA.T_smem, GA.E_smem, mode == 1);
+    const bool full = (A.mask & 15u) == 15u;
+    cudaError_t err;
+    if (mode == 1) {
+        if (tbytes == 2) err = full ? launch_g<true, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)
+                                    : launch_g<true, uint16_t, int32_t, false>(A, GA, blocks, threads, smem, st);
+        else err = launch_g<true, int32_t, int32_t, false>(A, GA, blocks, threads, smem, st);
+    } else {
+        if (tbytes == 2) err = full ? launch_g<false, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)
+                                    : launch_g<false, uint16_t, int32_t, false>(A, GA, blocks, threads, smem, st);
+        else err = launch_g<false, int32_t, int32_t, false>(A, GA, blocks, threads, smem, st);
+    }
+    if (err != cudaSuccess) return err;
+    if (A.best_ptr) {
+        k_bs_to_csr<<<1, 1, 0, st>>>(GA.BS, I.n, I.V, A.best_ptr, A.best_ms);
+        err = cudaGetLastError();
+    }
+    return err;
+}
+
+__global__ void k_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NC * NL * NL; i += gridDim.x * blockDim.x) {
+        int c = i / (NL * NL), r = (i / NL) % NL, col = i % NL;
+        size_t o = (size_t)(c * NL + r) * NLp + col;
+        if (tbytes == 2) reinterpret_cast<uint16_t *>(out)[o] = (uint16_t)T[i];
+        else reinterpret_cast<int32_t *>(out)[o] = T[i];
+    }
+}
+
+cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, cudaStream_t st) {
+    k_pad_table<<<256, 256, 0, st>>>(T, out, NC, NL, NLp, tbytes);
+    return cudaGetLastError();
+}
+
+int padded_stride_host(int NL, int tbytes) { return padded_stride(NL, tbytes); }
+
+}  // namespace airsched

@@ -32,6 +32,27 @@ struct SearchArgs {
     int32_t *tabu_out;                     // [R][n][V]
 };
 
+struct GridLayout {
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, total;   // shared-memory byte offsets per CTA
+};
+
+struct GridArgs {
+    int NLp;                       // padded row stride of the travel-time table
+    GridLayout L;
+    int T_smem, E_smem;            // table / tabu matrix staged in shared memory?
+    const void *Tglobal;           // padded table in global memory (uint16 or int32)
+    int32_t *Eglobal;              // [n][V] tabu matrix when !E_smem
+    int32_t *BS;                   // [S] best-schedule successor array
+    unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
+    int G;                         // rows per tile
+};
+
+size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
+cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
+                        cudaStream_t st);
+cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, cudaStream_t st);
+int padded_stride_host(int NL, int tbytes);
+
 size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem);
 cudaError_t launch_build_state(const DevInst &I, const int32_t *ptr, const int32_t *ms, RunViewG &G, cudaStream_t st);
 cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int it, long long cur, long long best,

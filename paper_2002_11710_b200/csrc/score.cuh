@@ -1,0 +1,233 @@
+// score.cuh -- the per-move scoring loops of the evaluation kernels (sm_100a).
+//
+// A "tile" is a set of moves one warp scores with part of the operands cached
+// in registers: a relocate tile is one chunk of 32*KR target slots (the
+// target-side records are cached per lane) times a range of rows m; a swap tile
+// is one chunk of 32*KS missions m2 aligned to the top of [0, n) (the m2-side
+// records are cached per lane) times a range of rows m1 < m2.  Inside a tile a
+// lane visits its moves in increasing canonical index, so the per-lane best is
+// kept as a 32-bit key (class << 31 | delta + 2^30) plus the index, and a strict
+// '<' keeps the lowest index among equal keys (O9, reading #26).  Each scorer
+// returns the tile's best packed 64-bit key for this lane (AS_KEY_NONE if none).
+//
+// Formulas: DESIGN.md §3 (the same arithmetic as engine.cuh, rewritten for
+// register-resident operands; adjacent swaps are excluded here and scored by
+// engine.cuh's exact three-link formula).  Operands are in the AoS records of
+// batch.cu's layout (CS: per-slot constants, RS: per-slot incoming-link record,
+// LK: links), in shared or global memory.
+#pragma once
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace airsched {
+
+constexpr int KR = 4;              // relocate tile: 4 x 32 target slots cached per lane
+constexpr int KS = 2;              // swap tile: 2 x 32 m2 missions cached per lane
+constexpr int NEG = -(1 << 29);    // "never feasible" margin
+
+template <class TT, class ET>
+struct ScoreCtx {
+    const TT *Ts;          // [NC][NL][NLp] travel times
+    const int4 *CS4;       // [S] {w, pick | del << 16, svc0, svc1}
+    const uint8_t *MH;     // [n] helicopter-only
+    const uint32_t *VC;    // [V] cls | heli_ok << 8 | base location << 16
+    const int4 *RS4;       // [S] {depc, inc, svco, endc | veh << 16}
+    const uint32_t *LK;    // [S] succ | pred << 16
+    const int32_t *F;      // [V] route flight time
+    const ET *E;           // [n][V] tabu expiry (TABU only)
+    int n, V, S, NL, NLp, P;
+    uint32_t Rb, mask;
+};
+
+template <bool TABU, bool FULL, class TT, class ET>
+__device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
+                                                int asp, int lane) {
+    const TT *Ts = C.Ts;
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint8_t *MH = C.MH;
+    const uint32_t *VC = C.VC, *LK = C.LK;
+    const int32_t *F = C.F;
+    const ET *E = C.E;
+    const int V = C.V, S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
+    const uint32_t mask = C.mask;
+    const bool en_inter_r = FULL || (mask & 1u) != 0, en_intra_r = FULL || (mask & 2u) != 0;
+    int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_inf[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) {
+        const int t = t0 + lane + 32 * k;
+        int t1 = 0, t2 = 0, dw = 0, kk = 0, wsv = NEG, slk = NEG, inf = 0xFFFF;
+        if (t < S) {
+            const int4 rs = RS4[t];
+            const int b = (int16_t)((uint32_t)rs.w >> 16);
+            if (b >= 0) {
+                const int4 cs = CS4[t];
+                const uint32_t vc = VC[b];
+                const int cb = vc & 0xFF;
+                t1 = (cb * NL + (rs.w & 0xFFFF)) * NLp;     // row of T_cb[endc(t)][.]
+                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb
+                dw = -rs.x;                                  // -dep(pred t)
+                kk = rs.z - rs.y;                            // svco(t) - inc(t)
+                wsv = cs.x - rs.z;                           // w(t) - svco(t)
+                slk = P - F[b];
+                inf = (b & 0xFFFF) | (cb << 16) | (((vc >> 8) & 1) << 20);
+            }
+        }
+        c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk;
+        c_inf[k] = inf;
+    }
+    uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+    for (int m = m_lo; m < m_hi; m++) {
+        const int4 rm = RS4[m];
+        const int a = (int16_t)((uint32_t)rm.w >> 16);
+        if (a < 0) continue;
+        const int s = LK[m] & 0xFFFF;
+        const int4 rsx = RS4[s];
+        const int4 csx = CS4[s];
+        const int ca = VC[a] & 0xFF;
+        const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+        if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
+        const int rem = Dps - rm.y - rsx.y;   // removal delta d(p,s) - d(p,m) - d(m,s)
+        const int4 cm = CS4[m];
+        const int Fa = F[a];
+        const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
+        const int intra_lim = P - Fa - rem;
+        const int w_m = cm.x, pick_m = cm.y & 0xFFFF, rowD = ((uint32_t)cm.y >> 16) * NLp;
+        const int svm0 = cm.z, svm1 = cm.w;
+        const bool heli_m = MH[m] != 0;
+        const ET *Erow = TABU ? E + m * V : nullptr;
+        const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
+#pragma unroll
+        for (int k = 0; k < KR; k++) {
+            const int t = t0 + lane + 32 * k;
+            const int inf = c_inf[k];
+            const int b = (int)(int16_t)(inf & 0xFFFF);
+            const bool cb1 = (inf >> 16) & 1;
+            const bool hok = (inf >> 20) & 1;
+            const int T1 = (int)Ts[c_t1[k] + pick_m];
+            const int T2 = (int)Ts[c_t2[k] + rowD];
+            const int x1 = T1 + (cb1 ? svm1 : svm0);
+            const int ins = x1 + T2 + c_k[k];
+            const int delta = rem + ins;
+            const bool same = b == a;
+            const int lim = same ? intra_lim : c_slk[k] + inter_bias;
+            const int mg = min(min(w_m + c_dw[k] - x1, c_wsv[k] - w_m - T2), lim - ins);
+            const bool ok = (mg >= 0) & (t != m) & (t != s) & (FULL || (same ? en_intra_r : en_inter_r)) &
+                            (hok | !heli_m);
+            bool adm;
+            if (TABU) adm = ((int)Erow[max(b, 0)] < it) | (delta < asp);
+            else adm = delta < 0;
+            uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+            k32 = ok ? k32 : 0xFFFFFFFFu;
+            const bool better = k32 < bk32;
+            bk32 = better ? k32 : bk32;
+            bidx = better ? base + 32 * k : bidx;
+        }
+    }    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+}
+
+template <bool TABU, bool FULL, class TT, class ET>
+__device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi, int m1_lo, int m1_hi, int it,
+                                               int asp, int lane) {
+    const TT *Ts = C.Ts;
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint8_t *MH = C.MH;
+    const uint32_t *VC = C.VC, *LK = C.LK;
+    const int32_t *F = C.F;
+    const ET *E = C.E;
+    const int n = C.n, V = C.V, NL = C.NL, NLp = C.NLp, P = C.P;
+    const uint32_t Rb = C.Rb, mask = C.mask;
+    const bool en_inter_s = FULL || (mask & 4u) != 0, en_intra_s = FULL || (mask & 8u) != 0;
+    const int lo = hi - 32 * KS;
+    int q_ps[KS], q_sv0[KS], q_sv1[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS],
+        q_ws2[KS], q_slk[KS], q_inf[KS];
+#pragma unroll
+    for (int k = 0; k < KS; k++) {
+        const int m2 = lo + lane + 32 * k;
+        int ps = 0, sv0 = 0, sv1 = 0, d2 = 0, e2 = 0, p2 = 0, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
+            inf = 0xFFFF;
+        if (m2 >= 0) {
+            const int4 r2 = RS4[m2];
+            const int b = (int16_t)((uint32_t)r2.w >> 16);
+            if (b >= 0) {
+                const int4 c2 = CS4[m2];
+                const uint32_t vc = VC[b];
+                const int cb = vc & 0xFF;
+                const int s2 = LK[m2] & 0xFFFF;
+                const int4 rs2 = RS4[s2];
+                const int4 cs2 = CS4[s2];
+                ps = (c2.y & 0xFFFF) | (s2 << 16);              // pick2 | s2 << 16
+                sv0 = c2.z;
+                sv1 = c2.w;
+                d2 = ((uint32_t)c2.y >> 16) * NLp;               // row del2 (any class)
+                e2 = (cb * NL + (r2.w & 0xFFFF)) * NLp;           // row T_cb[endc2]
+                p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
+                w2 = c2.x;
+                dep2 = r2.x;
+                kb = rs2.z - r2.y - rs2.y;                        // svco(s2) - inc2 - inc(s2)
+                ws2 = cs2.x - rs2.z;                              // w(s2) - svco(s2)
+                slk = P - F[b];
+                inf = (b & 0xFFFF) | (cb << 16) | ((int)MH[m2] << 20) | (((vc >> 8) & 1) << 21);
+            }
+        }
+        q_ps[k] = ps; q_sv0[k] = sv0; q_sv1[k] = sv1; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2;
+        q_w2[k] = w2; q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_inf[k] = inf;
+    }
+    uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+    for (int m1 = m1_lo; m1 < m1_hi; m1++) {
+        const int4 r1 = RS4[m1];
+        const int a = (int16_t)((uint32_t)r1.w >> 16);
+        if (a < 0) continue;
+        const int s1 = LK[m1] & 0xFFFF;
+        const int4 c1 = CS4[m1];
+        const int4 rs1 = RS4[s1];
+        const int4 cs1 = CS4[s1];
+        const uint32_t vca = VC[a];
+        const int ca = vca & 0xFF;
+        const bool hoka = (vca >> 8) & 1;
+        const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
+        const int col_ta2 = ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
+        const int pick1 = c1.y & 0xFFFF, row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+        const int depc1 = r1.x, w1 = c1.x;
+        const bool heli1 = MH[m1] != 0;
+        const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
+        const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
+        const int slkA = P - F[a];
+        const int sv10 = c1.z, sv11 = c1.w;
+        const ET *Erow = TABU ? E + m1 * V : nullptr;
+        const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
+#pragma unroll
+        for (int k = 0; k < KS; k++) {
+            if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+            const int m2 = lo + lane + 32 * k;
+            const int inf = q_inf[k];
+            const int b = (int)(int16_t)(inf & 0xFFFF);
+            const bool cb1 = (inf >> 16) & 1;
+            const bool h2 = (inf >> 20) & 1, hokb = (inf >> 21) & 1;
+            const int pick2 = q_ps[k] & 0xFFFF, s2 = (uint32_t)q_ps[k] >> 16;
+            const bool same = a == b;
+            const int ya1 = (int)Ts[row_ya1 + pick2] + (ca ? q_sv1[k] : q_sv0[k]);   // p1 -> m2
+            const int Ta2 = (int)Ts[col_ta2 + q_d2[k]];                              // m2 -> s1
+            const int yb1 = (int)Ts[q_e2[k] + pick1] + (cb1 ? sv11 : sv10);          // p2 -> m1
+            const int Tb2 = (int)Ts[q_p2[k] + row_tb2];                              // m1 -> s2
+            const int da = ya1 + Ta2 + ka;
+            const int db = yb1 + Tb2 + q_kb[k];
+            const int delta = da + db;
+            const int mf = same ? slkA - delta : min(slkA - da, q_slk[k] - db);
+            const int mg = min(min(min(q_w2[k] - depc1 - ya1, wsv1 - q_w2[k] - Ta2),
+                                   min(w1 - q_dep2[k] - yb1, q_ws2[k] - w1 - Tb2)), mf);
+            const bool ok = (mg >= 0) & (m2 > m1) & (s1 != m2) & (s2 != m1) &
+                            (FULL || (same ? en_intra_s : en_inter_s)) & (!h2 | hoka) & (!heli1 | hokb);
+            bool adm;
+            if (TABU) adm = (((int)Erow[max(b, 0)] < it) & ((int)E[max(m2, 0) * V + a] < it)) | (delta < asp);
+            else adm = delta < 0;
+            uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+            k32 = ok ? k32 : 0xFFFFFFFFu;
+            const bool better = k32 < bk32;
+            bk32 = better ? k32 : bk32;
+            bidx = better ? base + 32 * k : bidx;
+        }
+    }    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+}
+
+}  // namespace airsched

@@ -364,3 +364,30 @@ def test_batch_per_run_starts(A, ctx, oracle_mod):
     A.as_batch_run(ctx, h, R, sp2, sm2, prm, np.zeros(R, np.uint64), shared_start=False, results=res)
     assert res[3]["stop_reason"] == A.AS_STOP_INFEASIBLE_START
     assert res[0]["stop_reason"] == A.AS_STOP_MAX_ITERS
+
+
+@pytest.mark.parametrize("cfg,iters", [("tiny", 200), ("ontario", 400), ("batched", 300)])
+def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch):
+    """The cooperative whole-GPU kernel (k_grid) forced onto small instances:
+    many tiles per row group, most warps idle -- the trace must not change."""
+    monkeypatch.setenv("AIRSCHED_GRID", "1")
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=3, kick=5)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    monkeypatch.setenv("AIRSCHED_GRID_G", "3")
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+
+
+def test_surge_run_parity_prefix(A, ctx, oracle_mod):
+    """C5 (n=4000, V=100, 32.4 M indices per iteration) on the whole-GPU kernel:
+    the first TS and NS iterations against the oracle."""
+    inst = instgen.generate("surge")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    _compare_run(A, ctx, O, h, p, m, 1, 10, 3)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, 2)
