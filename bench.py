@@ -35,8 +35,8 @@ UNIT = "move evals/s"
 # Algorithmic integer operations per scored move: the
 # adds/compares/selects the formulas of §8(a) a3-a6 require per (m,t) pair or
 # per swap pair, with the per-row removal part amortised.
-OPS_RELOCATE = 18
-OPS_SWAP = 34
+OPS_RELOCATE = 23
+OPS_SWAP = 37
 
 
 def log(*a):
@@ -294,6 +294,46 @@ def run_gpu(args):
     return 0
 
 
+def run_single(args):
+    """Single-instance workloads (C1 tiny, C2 ontario, C4 large, C5 surge): one step =
+    one as_tabu_run (or as_nbhd_run with --ns) of max_iters iterations from the
+    Alg. 1 start; device time from CUDA events around the kernel launch."""
+    import torch
+    from paper_2002_11710_b200 import airsched as A
+    cfg, inst = workload(args.workload)
+    iters = args.iters or cfg.max_iters
+    h = A.Instance(inst)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    ctx = A.Ctx(0, stream.cuda_stream)
+    ctx.upload(h)
+    p, m, _ = A.as_init_greedy(ctx, h)
+    mode = A.AS_MODE_NS if args.ns else A.AS_MODE_TABU
+    prm = A.params(mode=mode, tenure=cfg.tenure, max_iters=iters)
+    fn = A.as_nbhd_run if args.ns else A.as_tabu_run
+    for _ in range(args.warmup):
+        fn(ctx, h, p, m, prm, want_best=False)
+    sampler = ClockSampler(0)
+    sampler.start()
+    ms, its = [], 0
+    for _ in range(args.steps):
+        r = fn(ctx, h, p, m, prm, want_best=False)
+        ms.append(ctx.last_kernel_ms)
+        its += r["iters_done"]
+    clocks = sampler.stop()
+    t = sum(ms) / 1e3
+    VM = valid_moves(inst)
+    line = {"metric": METRIC, "value": its * VM / t, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: n={inst.n_missions}, V={inst.n_vehicles}, "
+                                   f"{'NS' if args.ns else 'TS'} {iters} iters", "valid_moves_per_iter": VM},
+            "tabu_iters_per_s": its / t, "iters_done_per_step": its / args.steps, "best_obj": r["best_obj"],
+            "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -308,9 +348,12 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--traffic", type=float, default=None, help="dram bytes/launch from an ncu --set full capture")
+    ap.add_argument("--ns", action="store_true", help="single-instance workloads: neighbourhood search")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if instgen.CONFIGS[args.workload].n_runs == 1:
+        return run_single(args)
     return run_gpu(args)
 
 
