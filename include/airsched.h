@@ -204,6 +204,27 @@ as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, int3
                        int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out,
                        int64_t *best_run_out);
 
+/* ------------------------------------------------------------- multi-GPU --
+ * One process per GPU.  Rank 0 creates a 128-byte NCCL unique id, the caller
+ * shares it (e.g. through torch.distributed), every rank calls as_comm_init on
+ * its own context.  With a communicator, as_tabu_run / as_nbhd_run shard the
+ * move space of ONE instance across the ranks (every rank must pass the same
+ * instance, start and params): each iteration every rank scores its slice,
+ * an 8-byte ncclAllReduce(MIN) selects the global best packed key, and every
+ * rank applies it to its replica -- the trace is identical to one GPU.
+ * as_batch_run with a communicator runs each rank's own runs and then reduces
+ * the best (objective, global run) over all ranks (best_run_out). */
+as_status as_comm_unique_id(void *uid_out /* 128 bytes, host */);
+as_status as_comm_init(as_ctx *ctx, int32_t nranks, int32_t rank, const void *uid /* 128 bytes, host */,
+                       as_comm **out);
+void as_comm_destroy(as_comm *comm);
+/* The contiguous tile range [tile_lo, tile_hi) of the flat neighbourhood tile
+ * list that `rank` scores in a sharded run on GPUs with n_sm SMs (host logic;
+ * the split balances scored moves).  weight_*: moves in the rank's range and
+ * in total.  Pointers: host, nullable. */
+as_status as_shard_plan(const as_instance *inst, int32_t nranks, int32_t rank, int32_t n_sm, int32_t *tile_lo,
+                        int32_t *tile_hi, int32_t *tile_total, int64_t *weight_rank, int64_t *weight_total);
+
 /* Device time of the last search/eval call's kernels on ctx's stream (ms),
  * measured with CUDA events around the launches. */
 float as_ctx_last_kernel_ms(const as_ctx *ctx);

@@ -27,7 +27,8 @@ AS_STOP_MAX_ITERS, AS_STOP_LOCAL_OPT, AS_STOP_NO_MOVE, AS_STOP_INFEASIBLE_START 
 SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "as_valid_moves_per_iter",
            "as_schedule_check", "as_ctx_create", "as_ctx_set_stream", "as_ctx_destroy", "as_instance_upload",
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
-           "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version"]
+           "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
+           "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan"]
 
 
 class AirschedError(RuntimeError):
@@ -88,6 +89,10 @@ def _load():
         "as_ctx_last_kernel_ms": (C.c_float, [vp]),
         "as_ctx_kernel_launches": (i64, [vp]),
         "as_last_error": (C.c_char_p, []),
+        "as_comm_unique_id": (i32, [vp]),
+        "as_comm_init": (i32, [vp, i32, i32, vp, vp]),
+        "as_comm_destroy": (None, [vp]),
+        "as_shard_plan": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "as_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -195,6 +200,47 @@ class Ctx:
         return int(lib.as_ctx_kernel_launches(self.handle))
 
 
+def as_comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib.as_comm_unique_id(C.byref(buf)))
+    return bytes(buf)
+
+
+class Comm:
+    """as_comm: NCCL communicator over the ranks of a torch.distributed job.
+
+    The 128-byte NCCL unique id is created on rank 0 and broadcast with
+    torch.distributed (any backend, e.g. gloo or nccl) -- plumbing only."""
+
+    def __init__(self, ctx: Ctx, nranks: int, rank: int, uid: bytes):
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib.as_comm_init(ctx.handle, int(nranks), int(rank), C.byref(buf), C.byref(h)))
+        self.handle = h
+        self.nranks, self.rank = nranks, rank
+
+    @classmethod
+    def from_torch_distributed(cls, ctx: Ctx, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [as_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(ctx, world, rank, obj[0])
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.as_comm_destroy(self.handle)
+            self.handle = None
+
+
+def as_shard_plan(inst: Instance, nranks: int, rank: int, n_sm: int = 148):
+    lo, hi, tot = C.c_int32(), C.c_int32(), C.c_int32()
+    wr, wt = C.c_int64(), C.c_int64()
+    _check(lib.as_shard_plan(inst.handle, int(nranks), int(rank), int(n_sm), C.byref(lo), C.byref(hi), C.byref(tot),
+                             C.byref(wr), C.byref(wt)))
+    return dict(tile_lo=lo.value, tile_hi=hi.value, tile_total=tot.value, weight=wr.value, weight_total=wt.value)
+
+
 def params(mode=AS_MODE_TABU, tenure=10, max_iters=100, kick=0, move_mask=AS_MOVE_ALL, strict_tabu_stop=0,
            trace_level=0, seed=0) -> as_run_params:
     return as_run_params(int(mode), int(tenure), int(max_iters), int(kick), int(move_mask), int(strict_tabu_stop),
@@ -232,7 +278,7 @@ def as_eval_moves(ctx: Ctx, inst: Instance, route_ptr, route_missions, mode=AS_M
 
 
 def _run(fn, ctx, inst, route_ptr, route_missions, prm, want_best=True, want_trace=False, want_digest=False,
-         want_tabu=False):
+         want_tabu=False, comm=None):
     route_ptr = np.ascontiguousarray(route_ptr, np.int32)
     route_missions = np.ascontiguousarray(route_missions, np.int32)
     res = as_run_result()
@@ -242,7 +288,8 @@ def _run(fn, ctx, inst, route_ptr, route_missions, prm, want_best=True, want_tra
     tr = np.zeros(K, TRACE_DTYPE) if want_trace else None
     dg = np.zeros(K, np.uint64) if want_digest else None
     tb = np.zeros((max(inst.n, 1), inst.V), np.int32) if want_tabu else None
-    args = [ctx.handle, None, inst.handle, _ptr(route_ptr), _ptr(route_missions), C.byref(prm), C.byref(res),
+    args = [ctx.handle, comm.handle if comm is not None else None, inst.handle, _ptr(route_ptr), _ptr(route_missions),
+            C.byref(prm), C.byref(res),
             _ptr(bp), _ptr(bm), _ptr(tr)]
     if fn is lib.as_tabu_run:
         args += [_ptr(dg), _ptr(tb)]

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "airsched.h"
 #include "engine.cuh"
 #include "launch.h"
@@ -232,8 +234,16 @@ struct as_ctx {
 };
 
 struct as_comm {
-    int nranks = 1, rank = 0;
+    int nranks = 1, rank = 0, device = 0;
+    ncclComm_t nccl = nullptr;
 };
+
+#define NCCL_TRY(expr)                                                                              \
+    do {                                                                                            \
+        ncclResult_t _r = (expr);                                                                   \
+        if (_r != ncclSuccess)                                                                      \
+            return fail(AS_ERR_COMM, "%s: %s (%s:%d)", #expr, ncclGetErrorString(_r), __FILE__, __LINE__); \
+    } while (0)
 
 static as_status set_device(as_ctx *ctx) {
     CUDA_TRY(cudaSetDevice(ctx->device));
@@ -621,7 +631,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     size_t sh_b = 0, run_b = 0;
     batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
-    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !tabu_out;
+    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest;
     const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
     bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single));
     // single large instances: one persistent cooperative grid (k_grid)
@@ -704,12 +714,15 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     return finish_out(ctx, {&o_res, &o_bp, &o_bm, &o_tr, &o_dg, &o_tb});
 }
 
+static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
+                             const int32_t *start_ms, const as_run_params *P, as_run_result *result,
+                             int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out);
+
 extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
                                  const int32_t *start_ms, const as_run_params *P, as_run_result *result,
                                  int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, uint64_t *digest,
                                  int32_t *tabu_out) {
     if (!ctx || !I || !P || !result) return fail(AS_ERR_INVALID_ARG, "null argument");
-    if (comm && comm->nranks > 1) return fail(AS_ERR_UNSUPPORTED, "sharded single-instance runs are not built yet");
     HostSched S;
     as_status st = parse_csr(I, start_ptr, start_ms, false, S);
     if (st != AS_OK) return st;
@@ -717,6 +730,10 @@ extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *
     int64_t obj;
     as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
     if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
+    if (comm || env_int("AIRSCHED_SHARDED", 0) == 1) {
+        if (digest && P->trace_level >= 2) return fail(AS_ERR_UNSUPPORTED, "tabu digests are not produced by the sharded path");
+        return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
+    }
     st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, digest, tabu_out, true);
     if (st != AS_OK) return st;
     if (result->stop_reason == AS_STOP_INFEASIBLE_START)
@@ -876,6 +893,197 @@ extern "C" as_status as_init_greedy(as_ctx *ctx, const as_instance *I, int32_t i
     }
     if (n_repairs_out) *n_repairs_out = repairs;
     return AS_OK;
+}
+
+// --------------------------------------------------------------- multi-GPU ---
+extern "C" as_status as_comm_unique_id(void *uid_out) {
+    if (!uid_out) return fail(AS_ERR_INVALID_ARG, "null uid_out");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(uid_out, &id, sizeof(id));
+    return AS_OK;
+}
+
+extern "C" as_status as_comm_init(as_ctx *ctx, int32_t nranks, int32_t rank, const void *uid, as_comm **out) {
+    if (!ctx || !uid || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(AS_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    std::unique_ptr<as_comm> c(new as_comm());
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = ctx->device;
+    NCCL_TRY(ncclCommInitRank(&c->nccl, nranks, id, rank));
+    *out = c.release();
+    return AS_OK;
+}
+
+extern "C" void as_comm_destroy(as_comm *comm) {
+    if (!comm) return;
+    if (comm->nccl) {
+        cudaSetDevice(comm->device);
+        ncclCommDestroy(comm->nccl);
+    }
+    delete comm;
+}
+
+static int shard_G(const as_instance *I, int n_sm) {
+    const int n = I->n, V = I->V, S = n + V;
+    const int warps_all = n_sm * 24;
+    const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
+    const int64_t pairs = (int64_t)n * nTC + (int64_t)n * nSC / 2;
+    return (int)std::max<int64_t>(1, pairs / (4 * (int64_t)warps_all));
+}
+
+extern "C" as_status as_shard_plan(const as_instance *I, int32_t nranks, int32_t rank, int32_t n_sm, int32_t *tile_lo,
+                                   int32_t *tile_hi, int32_t *tile_total, int64_t *weight_rank, int64_t *weight_total) {
+    if (!I || nranks < 1 || rank < 0 || rank >= nranks || n_sm < 1) return fail(AS_ERR_INVALID_ARG, "bad argument");
+    const int G = shard_G(I, n_sm);
+    int lo, hi;
+    int64_t wt, wr;
+    shard_plan(I->n, I->V, G, nranks, rank, &lo, &hi, &wt, &wr);
+    int last_lo, total;
+    shard_plan(I->n, I->V, G, 1, 0, &last_lo, &total, nullptr, nullptr);
+    if (tile_lo) *tile_lo = lo;
+    if (tile_hi) *tile_hi = hi;
+    if (tile_total) *tile_total = total;
+    if (weight_rank) *weight_rank = wr;
+    if (weight_total) *weight_total = wt;
+    return AS_OK;
+}
+
+// Sharded single-instance run: replica in global memory, K iterations per CUDA
+// graph of [eval slice -> ncclAllReduce(MIN, 8 B) -> apply].
+static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
+                             const int32_t *start_ms, const as_run_params *P, as_run_result *result,
+                             int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out) {
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const DevInst *D;
+    if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+    InstDev &ID = ctx->insts[I];
+    const bool tabu = P->mode == AS_MODE_TABU;
+    const int n = I->n, V = I->V, S = n + V, NC = I->NC;
+    if (I->NL > 65535 || S > 65535 || V > 32767 || NC > 2)
+        return fail(AS_ERR_UNSUPPORTED, "sharded path needs NL, n+V < 65536 and <= 2 classes");
+    SearchArgs A;
+    memset(&A, 0, sizeof(A));
+    A.inst = *D;
+    A.n_runs = 1;
+    const void *dp, *dm;
+    if ((st = dev_in(ctx, "start_ptr", start_ptr, (size_t)(V + 1) * 4, &dp)) != AS_OK) return st;
+    if ((st = dev_in(ctx, "start_ms", start_ms, std::max<size_t>((size_t)n * 4, 4), &dm)) != AS_OK) return st;
+    A.start_ptr = (const int32_t *)dp;
+    A.start_ms = (const int32_t *)dm;
+    A.shared_start = 1;
+    A.seed = P->seed;
+    A.kick = P->kick;
+    A.tenure = P->tenure;
+    A.max_iters = P->max_iters;
+    A.strict_tabu_stop = P->strict_tabu_stop;
+    A.mask = P->move_mask;
+    // replica buffers
+    ShardBufs B;
+    void *p;
+    size_t words = 0;
+    const size_t oCS = 0, oRS = oCS + (size_t)S * 4, oLK = oRS + (size_t)S * 4, oF = oLK + S, oE = oF + V,
+                 oBS = oE + (tabu ? (size_t)n * V : 0), oVC = oBS + S, oMH = oVC + V, oCH = oMH + (n + 3) / 4,
+                 oCtl = oCH + 4;
+    words = oCtl + (sizeof(ShardCtl) + 7) / 4 + 8;
+    if ((st = scratch(ctx, "shard_state", words * 4 + 64, &p)) != AS_OK) return st;
+    int32_t *base = (int32_t *)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    B.CS4 = (int4 *)(base + oCS);
+    B.RS4 = (int4 *)(base + oRS);
+    B.LK = (uint32_t *)(base + oLK);
+    B.F = base + oF;
+    B.E = tabu ? base + oE : nullptr;
+    B.BS = base + oBS;
+    B.VC = (uint32_t *)(base + oVC);
+    B.MH = (uint8_t *)(base + oMH);
+    B.CH = (uint8_t *)(base + oCH);
+    B.ctl = (ShardCtl *)(((uintptr_t)(base + oCtl) + 15) & ~(uintptr_t)15);
+    OutBuf o_res, o_bp, o_bm, o_tr, o_tb;
+    if ((st = dev_out(ctx, "o_res", result, sizeof(as_run_result), o_res)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_bp", best_ptr, (size_t)(V + 1) * 4, o_bp)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_bm", best_ms, std::max<size_t>((size_t)n * 4, 4), o_bm)) != AS_OK) return st;
+    const bool want_trace = trace && P->trace_level >= 1 && P->max_iters > 0;
+    if ((st = dev_out(ctx, "o_tr", want_trace ? trace : nullptr, (size_t)P->max_iters * sizeof(as_trace_rec), o_tr)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "o_tb", tabu ? tabu_out : nullptr, std::max<size_t>((size_t)n * V * 4, 4), o_tb)) != AS_OK) return st;
+    A.results = (as_run_result *)o_res.dev;
+    A.best_ptr = best_ptr ? (int32_t *)o_bp.dev : nullptr;
+    A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
+    A.trace = (as_trace_rec *)o_tr.dev;
+    A.tabu_out = (int32_t *)o_tb.dev;
+    const int tb = ID.tpad_bytes;
+    CUDA_TRY(launch_shard_init(A, B, ID.Tpad, tb, ctx->stream));
+    ctx->launches++;
+    const int nranks = comm ? comm->nranks : 1, rank = comm ? comm->rank : 0;
+    const int G = shard_G(I, ctx->n_sm);
+    int tlo, thi;
+    shard_plan(n, V, G, nranks, rank, &tlo, &thi, nullptr, nullptr);
+    // Test mode (no communicator): emulate R ranks on one GPU by scoring the R
+    // slices one after another into the same key before the apply.
+    const int emulate = comm ? 1 : std::max(1, env_int("AIRSCHED_SHARD_EMULATE", 1));
+    std::vector<std::pair<int, int>> slices;
+    if (emulate > 1) {
+        for (int r = 0; r < emulate; r++) {
+            int a, b;
+            shard_plan(n, V, G, emulate, r, &a, &b, nullptr, nullptr);
+            slices.push_back({a, b});
+        }
+    } else {
+        slices.push_back({tlo, thi});
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    if (P->max_iters > 0) {
+        const int K = std::max(1, std::min(P->max_iters, env_int("AIRSCHED_SHARD_K", 64)));
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < K; k++) {
+            cudaError_t e1 = cudaSuccess;
+            for (auto &sl : slices) {
+                e1 = launch_shard_eval(A, B, ID.Tpad, tb, tabu ? 1 : 0, G, sl.first, sl.second, ctx->n_sm, ctx->stream);
+                if (e1 != cudaSuccess) break;
+            }
+            if (e1 != cudaSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_DEVICE, "shard eval: %s", cudaGetErrorString(e1)); }
+            if (comm) {
+                ncclResult_t r = ncclAllReduce(&B.ctl->key, &B.ctl->key, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream);
+                if (r != ncclSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_COMM, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+            }
+            e1 = launch_shard_apply(A, B, ID.Tpad, tb, tabu ? 1 : 0, ctx->stream);
+            if (e1 != cudaSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_DEVICE, "shard apply: %s", cudaGetErrorString(e1)); }
+        }
+        CUDA_TRY(cudaStreamEndCapture(ctx->stream, &graph));
+        CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+        int *hstop = nullptr;
+        CUDA_TRY(cudaMallocHost(&hstop, sizeof(int)));
+        const int chunks = (P->max_iters + K - 1) / K;
+        for (int c = 0; c < chunks; c++) {
+            cudaError_t e = cudaGraphLaunch(exec, ctx->stream);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(hstop, &B.ctl->stop, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+            if (e != cudaSuccess) {
+                cudaFreeHost(hstop);
+                cudaGraphExecDestroy(exec);
+                cudaGraphDestroy(graph);
+                return fail(AS_ERR_DEVICE, "sharded iteration graph: %s", cudaGetErrorString(e));
+            }
+            ctx->launches += (int64_t)(slices.size() + 1) * K;
+            if (*hstop) break;   // identical on every rank: all ranks apply the same keys
+        }
+        cudaFreeHost(hstop);
+        CUDA_TRY(cudaGraphExecDestroy(exec));
+        CUDA_TRY(cudaGraphDestroy(graph));
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timed = true;
+    CUDA_TRY(launch_shard_finish(A, B, ctx->stream));
+    ctx->launches++;
+    return finish_out(ctx, {&o_res, &o_bp, &o_bm, &o_tr, &o_tb});
 }
 
 extern "C" const char *as_last_error(void) { return g_err.c_str(); }

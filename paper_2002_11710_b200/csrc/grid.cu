@@ -54,62 +54,6 @@ size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, boo
     return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
 }
 
-struct GridTiles {
-    int nTC, nSC, nAdj, nRG, G;   // t-chunks, swap chunks, adjacent tiles, row groups, rows per group
-    int n_reloc, n_swap, n_total; // tile counts
-};
-
-__host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
-    GridTiles T;
-    const int S = n + V;
-    T.G = G;
-    T.nTC = (S + 32 * KR - 1) / (32 * KR);
-    T.nSC = n > 1 ? (n - 1 + 32 * KS - 1) / (32 * KS) : 0;
-    T.nRG = (n + G - 1) / G;
-    T.nAdj = (n + 31) / 32;
-    T.n_reloc = T.nTC * T.nRG;
-    T.n_swap = T.nSC * T.nRG;
-    T.n_total = T.n_reloc + T.n_swap + T.nAdj;
-    return T;
-}
-
-// Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
-template <bool TABU, bool FULL, class TT, class ET, class MV, class RV>
-__device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
-                                                const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
-                                                int it, long long cur, long long best, int lane) {
-    const int n = SC.n;
-    const int asp = (int)(best - cur);
-    uint64_t kmin = KEY_NONE;
-    for (int tile = tlo + gwarp; tile < thi; tile += nwarps_all) {
-        uint64_t kb = KEY_NONE;
-        if (tile < GT.n_reloc) {
-            const int c = tile % GT.nTC, g = tile / GT.nTC;
-            const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
-            kb = score_reloc<TABU, FULL>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
-        } else if (tile < GT.n_reloc + GT.n_swap) {
-            const int r = tile - GT.n_reloc;
-            const int j = r % GT.nSC, g = r / GT.nSC;
-            const int hi = n - j * 32 * KS;
-            const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
-            if (m_lo < m_hi) kb = score_swap<TABU, FULL>(SC, hi, m_lo, m_hi, it, asp, lane);
-        } else {
-            const int x = (tile - GT.n_reloc - GT.n_swap) * 32 + lane;
-            if (x < n && (FULL || (SC.mask & 8u))) {
-                const int gg = SC.LK[x] & 0xFFFF;
-                if (R.veh[x] >= 0 && gg < n) {
-                    const int m1 = min(x, gg), m2 = max(x, gg);
-                    const MoveEval e = swap_eval(M, R, m1, m2, SC.mask, it);
-                    const int cls = move_class<TABU>(e, cur, best);
-                    if (cls >= 0) kb = make_key(cls, e.delta, SC.Rb + (uint32_t)m1 * (uint32_t)n + (uint32_t)m2);
-                }
-            }
-        }
-        kmin = kb < kmin ? kb : kmin;
-    }
-    return kmin;
-}
-
 template <bool TABU, class TT, class ET, bool FULL>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
     extern __shared__ __align__(16) unsigned char smem[];

@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "airsched.h"
 #include "engine.cuh"
@@ -46,6 +48,30 @@ struct GridArgs {
     unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
     int G;                         // rows per tile
 };
+
+// Sharded single-instance run (shard.cu): replica state in global memory.
+struct ShardCtl {
+    long long cur, best, start;
+    int it, best_it, stop, kicks;
+    unsigned long long key;     // this iteration's key (all-reduced with MIN across ranks)
+};
+
+struct ShardBufs {
+    int4 *CS4, *RS4;
+    uint8_t *MH, *CH;
+    uint32_t *VC, *LK;
+    int32_t *F, *E, *BS;
+    ShardCtl *ctl;
+};
+
+cudaError_t launch_shard_init(const SearchArgs &A, const ShardBufs &B, const void *Tpad, int tbytes, cudaStream_t st);
+cudaError_t launch_shard_eval(const SearchArgs &A, const ShardBufs &B, const void *Tpad, int tbytes, int mode, int G,
+                              int tlo, int thi, int blocks, cudaStream_t st);
+cudaError_t launch_shard_apply(const SearchArgs &A, const ShardBufs &B, const void *Tpad, int tbytes, int mode,
+                               cudaStream_t st);
+cudaError_t launch_shard_finish(const SearchArgs &A, const ShardBufs &B, cudaStream_t st);
+void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
+                int64_t *weight_rank);
 
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
