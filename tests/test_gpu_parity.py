@@ -391,3 +391,41 @@ def test_surge_run_parity_prefix(A, ctx, oracle_mod):
     p, m = start_of(O, inst)
     _compare_run(A, ctx, O, h, p, m, 1, 10, 3)
     _compare_run(A, ctx, O, h, p, m, 0, 0, 2)
+
+
+# ------------------------------------------------- sharded single instance (C5) --
+@pytest.mark.parametrize("cfg,iters,emulate", [("tiny", 200, 1), ("ontario", 400, 3), ("large", 30, 8),
+                                               ("surge", 2, 8)])
+def test_sharded_path_parity(A, ctx, oracle_mod, cfg, iters, emulate, monkeypatch):
+    """The sharded path's kernels (replica in global memory, per-iteration
+    eval -> MIN -> apply in a CUDA graph).  With `emulate` > 1 the slices of
+    that many ranks are scored one after another on this GPU (no kernel waits
+    on another) -- the move sequence must equal the oracle's."""
+    monkeypatch.setenv("AIRSCHED_SHARDED", "1")
+    monkeypatch.setenv("AIRSCHED_SHARD_EMULATE", str(emulate))
+    monkeypatch.setenv("AIRSCHED_SHARD_K", "7")
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=9, kick=3)
+    if cfg != "surge":
+        _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+
+
+def test_sharded_nccl_one_rank(A, ctx, oracle_mod):
+    """The real NCCL path (ncclAllReduce MIN on ncclUint64 inside the captured
+    graph) with a one-rank communicator on this GPU."""
+    comm = A.Comm(ctx, 1, 0, A.as_comm_unique_id())
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    for mode in (1, 0):
+        prm = A.params(mode=mode, tenure=10, max_iters=500, trace_level=1)
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, comm=comm)
+        o = O.search(p, m, mode=mode, tenure=10, max_iters=500)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and g["best_obj"] == o["best_obj"]
+        assert routes_of(*g["best"]) == routes_of(*o["best"])
