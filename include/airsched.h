@@ -218,6 +218,17 @@ as_status as_comm_unique_id(void *uid_out /* 128 bytes, host */);
 as_status as_comm_init(as_ctx *ctx, int32_t nranks, int32_t rank, const void *uid /* 128 bytes, host */,
                        as_comm **out);
 void as_comm_destroy(as_comm *comm);
+/* After as_batch_run (with or without a communicator): the best run over all
+ * ranks -- the minimum of (best_obj << 32 | global run), global run = rank *
+ * n_runs + r (every rank runs n_runs runs); as_batch_run already reduced it on
+ * the device with ncclAllReduce(MIN).  If ptr_out/ms_out are given, the owner
+ * rank broadcasts that run's best schedule (CSR) to every rank (ncclBroadcast);
+ * run_best_ptr/run_best_ms are this rank's per-run best schedules as written
+ * by as_batch_run ([n_runs][V+1], [n_runs][n], host or device).  Outputs host. */
+as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_runs, const int32_t *run_best_ptr,
+                               const int32_t *run_best_ms, int64_t *best_run_out, int64_t *best_obj_out,
+                               int32_t *ptr_out, int32_t *ms_out);
+
 /* The contiguous tile range [tile_lo, tile_hi) of the flat neighbourhood tile
  * list that `rank` scores in a sharded run on GPUs with n_sm SMs (host logic;
  * the split balances scored moves).  weight_*: moves in the rank's range and

@@ -28,7 +28,7 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_schedule_check", "as_ctx_create", "as_ctx_set_stream", "as_ctx_destroy", "as_instance_upload",
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
-           "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan"]
+           "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best"]
 
 
 class AirschedError(RuntimeError):
@@ -93,6 +93,7 @@ def _load():
         "as_comm_init": (i32, [vp, i32, i32, vp, vp]),
         "as_comm_destroy": (None, [vp]),
         "as_shard_plan": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "as_batch_gather_best": (i32, [vp, vp, i32, vp, vp, vp, vp, vp, vp]),
         "as_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -314,14 +315,31 @@ def as_nbhd_run(ctx, inst, route_ptr, route_missions, prm, **kw):
     return _run(lib.as_nbhd_run, ctx, inst, route_ptr, route_missions, prm, **kw)
 
 
+def as_batch_gather_best(ctx, inst, n_runs, run_best_ptr=None, run_best_ms=None, comm=None):
+    """Global best run over all ranks of the last as_batch_run, and (if the
+    per-run best schedules are given) that run's schedule broadcast from its owner."""
+    run, obj = C.c_int64(), C.c_int64()
+    want = run_best_ptr is not None
+    ptr = np.zeros(inst.V + 1, np.int32) if want else None
+    ms = np.zeros(max(inst.n, 1), np.int32) if want else None
+    _check(lib.as_batch_gather_best(ctx.handle, comm.handle if comm is not None else None, int(n_runs),
+                                    _ptr(run_best_ptr), _ptr(run_best_ms), C.byref(run), C.byref(obj), _ptr(ptr),
+                                    _ptr(ms)))
+    out = dict(best_run=run.value, best_obj=obj.value)
+    if want:
+        out["best"] = (ptr, ms[:inst.n])
+    return out
+
+
 def as_batch_run(ctx, inst, n_runs, start_ptr, start_missions, prm, seeds, shared_start=True, results=None,
-                 best_ptr_out=None, best_missions_out=None, trace_out=None, want_best_run=False):
+                 best_ptr_out=None, best_missions_out=None, trace_out=None, want_best_run=False, comm=None):
     """Marshalling for as_batch_run.  Arrays may be numpy (host) or torch CUDA tensors
     (device-resident; then the call only enqueues work on the ctx stream)."""
     best_run = C.c_int64(-1)
     if isinstance(seeds, np.ndarray):
         seeds = np.ascontiguousarray(seeds, np.uint64)
-    _check(lib.as_batch_run(ctx.handle, None, inst.handle, int(n_runs), _ptr(start_ptr), _ptr(start_missions),
+    _check(lib.as_batch_run(ctx.handle, comm.handle if comm is not None else None, inst.handle, int(n_runs),
+                            _ptr(start_ptr), _ptr(start_missions),
                             int(bool(shared_start)), C.byref(prm), _ptr(seeds), _ptr(results), _ptr(best_ptr_out),
                             _ptr(best_missions_out), _ptr(trace_out), C.byref(best_run) if want_best_run else None))
     return int(best_run.value)

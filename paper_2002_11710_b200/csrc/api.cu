@@ -227,9 +227,11 @@ struct as_ctx {
     size_t max_smem = 0;
     std::map<const as_instance *, InstDev> insts;
     std::map<std::string, DevBuf> scratch;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evj = nullptr;
+    cudaStream_t cap = nullptr;   // private non-blocking stream for graph capture (torch's may be legacy)
     bool timed = false;
     float last_ms = 0.f;
+    int32_t batch_runs = -1, batch_n = 0, batch_V = 0;   // last as_batch_run
     int64_t launches = 0;
 };
 
@@ -266,6 +268,8 @@ extern "C" as_status as_ctx_create(int32_t device, void *stream, as_ctx **out) {
     c->max_smem = prop.sharedMemPerBlockOptin;
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
     *out = c.release();
     return AS_OK;
 }
@@ -285,6 +289,8 @@ extern "C" void as_ctx_destroy(as_ctx *ctx) {
     for (auto &kv : ctx->scratch) cudaFree(kv.second.p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evj) cudaEventDestroy(ctx->evj);
+    if (ctx->cap) cudaStreamDestroy(ctx->cap);
     delete ctx;
 }
 
@@ -756,27 +762,81 @@ extern "C" as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance 
                                   int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int64_t *best_run_out) {
     if (!ctx || !I || !P) return fail(AS_ERR_INVALID_ARG, "null argument");
     if (!start_ptr) return fail(AS_ERR_INVALID_ARG, "null start");
-    (void)comm;
-    as_status st = run_core(ctx, I, n_runs, start_ptr, start_ms, shared_start, P, seeds, results, best_ptr, best_ms,
+    // results are needed on the device for the best-run reduction
+    as_run_result *res = results;
+    if (!res || !is_device_ptr(res)) {
+        void *p;
+        as_status st = scratch(ctx, "batch_res", (size_t)n_runs * sizeof(as_run_result), &p);
+        if (st != AS_OK) return st;
+        res = (as_run_result *)p;
+    }
+    as_status st = run_core(ctx, I, n_runs, start_ptr, start_ms, shared_start, P, seeds, res, best_ptr, best_ms,
                             trace, nullptr, nullptr, false);
     if (st != AS_OK) return st;
-    if (best_run_out) {
-        // smallest (best_obj, run) among feasible runs; needs the results on the host
-        std::vector<as_run_result> h(n_runs);
-        const as_run_result *src = results;
-        if (!results) return fail(AS_ERR_INVALID_ARG, "best_run_out needs results");
-        if (is_device_ptr(results)) {
-            CUDA_TRY(cudaMemcpyAsync(h.data(), results, n_runs * sizeof(as_run_result), cudaMemcpyDeviceToHost, ctx->stream));
-            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-            src = h.data();
-        }
-        int64_t best = -1;
-        for (int r = 0; r < n_runs; r++) {
-            if (src[r].stop_reason == AS_STOP_INFEASIBLE_START) continue;
-            if (best < 0 || src[r].best_obj < src[best].best_obj) best = r;
-        }
-        *best_run_out = best;
+    // best (objective, global run) over all ranks: on the device, NCCL MIN across ranks
+    void *kp;
+    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
+    const int64_t offset = comm ? (int64_t)comm->rank * n_runs : 0;
+    CUDA_TRY(launch_batch_best(res, n_runs, offset, (unsigned long long *)kp, ctx->stream));
+    ctx->launches++;
+    if (comm && comm->nranks > 1)
+        NCCL_TRY(ncclAllReduce(kp, kp, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream));
+    ctx->batch_runs = n_runs;
+    ctx->batch_n = I->n;
+    ctx->batch_V = I->V;
+    if (results && res != results) {
+        CUDA_TRY(cudaMemcpyAsync(results, res, (size_t)n_runs * sizeof(as_run_result), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     }
+    if (best_run_out) {
+        unsigned long long k;
+        CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        *best_run_out = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
+    }
+    return AS_OK;
+}
+
+extern "C" as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_runs, const int32_t *run_best_ptr,
+                                          const int32_t *run_best_ms, int64_t *best_run_out, int64_t *best_obj_out,
+                                          int32_t *ptr_out, int32_t *ms_out) {
+    if (!ctx) return fail(AS_ERR_INVALID_ARG, "null ctx");
+    if (ctx->batch_runs != n_runs) return fail(AS_ERR_INVALID_ARG, "no as_batch_run of %d runs on this context", n_runs);
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    void *kp;
+    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
+    unsigned long long k;
+    CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const int64_t run = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
+    if (best_run_out) *best_run_out = run;
+    if (best_obj_out) *best_obj_out = k == AS_KEY_NONE ? -1 : (int64_t)(k >> 32);
+    if (!ptr_out || run < 0) return AS_OK;
+    // owner copies its run's CSR into a buffer, NCCL broadcast to every rank
+    const as_instance *I = nullptr;
+    for (auto &kv : ctx->insts) I = kv.first;   // the instance of the last batch
+    (void)I;
+    const int rank = comm ? comm->rank : 0;
+    const int owner = (int)(run / n_runs);
+    const int r = (int)(run % n_runs);
+    if (!run_best_ptr || !run_best_ms) return fail(AS_ERR_INVALID_ARG, "run_best_ptr/ms required for the schedule");
+    const int V = ctx->batch_V, n = ctx->batch_n;
+    void *buf;
+    if ((st = scratch(ctx, "gbest", (size_t)(V + 1 + n) * 4 + 4, &buf)) != AS_OK) return st;
+    if (rank == owner) {
+        CUDA_TRY(cudaMemcpyAsync(buf, run_best_ptr + (size_t)r * (V + 1), (size_t)(V + 1) * 4, cudaMemcpyDefault, ctx->stream));
+        if (n > 0)
+            CUDA_TRY(cudaMemcpyAsync((int32_t *)buf + V + 1, run_best_ms + (size_t)r * n, (size_t)n * 4, cudaMemcpyDefault,
+                                     ctx->stream));
+    }
+    if (comm && comm->nranks > 1)
+        NCCL_TRY(ncclBroadcast(buf, buf, (size_t)(V + 1 + n), ncclInt32, owner, comm->nccl, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ptr_out, buf, (size_t)(V + 1) * 4, cudaMemcpyDefault, ctx->stream));
+    if (n > 0 && ms_out)
+        CUDA_TRY(cudaMemcpyAsync(ms_out, (int32_t *)buf + V + 1, (size_t)n * 4, cudaMemcpyDefault, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return AS_OK;
 }
 
@@ -1037,35 +1097,40 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
     } else {
         slices.push_back({tlo, thi});
     }
-    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    // the iteration graphs run on the context's private capture stream, ordered
+    // after everything already queued on cs
+    cudaStream_t cs = ctx->cap;
+    CUDA_TRY(cudaEventRecord(ctx->evj, ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evj, 0));
+    CUDA_TRY(cudaEventRecord(ctx->ev0, cs));
     if (P->max_iters > 0) {
         const int K = std::max(1, std::min(P->max_iters, env_int("AIRSCHED_SHARD_K", 64)));
         cudaGraph_t graph;
         cudaGraphExec_t exec;
-        CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < K; k++) {
             cudaError_t e1 = cudaSuccess;
             for (auto &sl : slices) {
-                e1 = launch_shard_eval(A, B, ID.Tpad, tb, tabu ? 1 : 0, G, sl.first, sl.second, ctx->n_sm, ctx->stream);
+                e1 = launch_shard_eval(A, B, ID.Tpad, tb, tabu ? 1 : 0, G, sl.first, sl.second, ctx->n_sm, cs);
                 if (e1 != cudaSuccess) break;
             }
-            if (e1 != cudaSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_DEVICE, "shard eval: %s", cudaGetErrorString(e1)); }
+            if (e1 != cudaSuccess) { cudaStreamEndCapture(cs, &graph); return fail(AS_ERR_DEVICE, "shard eval: %s", cudaGetErrorString(e1)); }
             if (comm) {
-                ncclResult_t r = ncclAllReduce(&B.ctl->key, &B.ctl->key, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream);
-                if (r != ncclSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_COMM, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+                ncclResult_t r = ncclAllReduce(&B.ctl->key, &B.ctl->key, 1, ncclUint64, ncclMin, comm->nccl, cs);
+                if (r != ncclSuccess) { cudaStreamEndCapture(cs, &graph); return fail(AS_ERR_COMM, "ncclAllReduce: %s", ncclGetErrorString(r)); }
             }
-            e1 = launch_shard_apply(A, B, ID.Tpad, tb, tabu ? 1 : 0, ctx->stream);
-            if (e1 != cudaSuccess) { cudaStreamEndCapture(ctx->stream, &graph); return fail(AS_ERR_DEVICE, "shard apply: %s", cudaGetErrorString(e1)); }
+            e1 = launch_shard_apply(A, B, ID.Tpad, tb, tabu ? 1 : 0, cs);
+            if (e1 != cudaSuccess) { cudaStreamEndCapture(cs, &graph); return fail(AS_ERR_DEVICE, "shard apply: %s", cudaGetErrorString(e1)); }
         }
-        CUDA_TRY(cudaStreamEndCapture(ctx->stream, &graph));
+        CUDA_TRY(cudaStreamEndCapture(cs, &graph));
         CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
         int *hstop = nullptr;
         CUDA_TRY(cudaMallocHost(&hstop, sizeof(int)));
         const int chunks = (P->max_iters + K - 1) / K;
         for (int c = 0; c < chunks; c++) {
-            cudaError_t e = cudaGraphLaunch(exec, ctx->stream);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(hstop, &B.ctl->stop, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+            cudaError_t e = cudaGraphLaunch(exec, cs);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(hstop, &B.ctl->stop, sizeof(int), cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
             if (e != cudaSuccess) {
                 cudaFreeHost(hstop);
                 cudaGraphExecDestroy(exec);
@@ -1079,8 +1144,10 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
         CUDA_TRY(cudaGraphExecDestroy(exec));
         CUDA_TRY(cudaGraphDestroy(graph));
     }
-    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, cs));
     ctx->timed = true;
+    CUDA_TRY(cudaEventRecord(ctx->evj, cs));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evj, 0));
     CUDA_TRY(launch_shard_finish(A, B, ctx->stream));
     ctx->launches++;
     return finish_out(ctx, {&o_res, &o_bp, &o_bm, &o_tr, &o_tb});

@@ -70,6 +70,8 @@ cudaError_t launch_shard_eval(const SearchArgs &A, const ShardBufs &B, const voi
 cudaError_t launch_shard_apply(const SearchArgs &A, const ShardBufs &B, const void *Tpad, int tbytes, int mode,
                                cudaStream_t st);
 cudaError_t launch_shard_finish(const SearchArgs &A, const ShardBufs &B, cudaStream_t st);
+cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_offset, unsigned long long *key,
+                              cudaStream_t st);
 void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
                 int64_t *weight_rank);
 

@@ -253,8 +253,8 @@ static ShardViews make_views(const ShardBufs &B, const void *Tpad, int NLp) {
 cudaError_t launch_shard_init(const SearchArgs &A, const ShardBufs &B, const void *Tpad, int tbytes, cudaStream_t st) {
     const int NLp = padded_stride(A.inst.NL, tbytes);
     ShardViews SV = make_views(B, Tpad, NLp);
-    if (tbytes == 2) k_shard_init<uint16_t><<<1, 1024, 0, st>>>(A, SV);
-    else k_shard_init<int32_t><<<1, 1024, 0, st>>>(A, SV);
+    if (tbytes == 2) k_shard_init<uint16_t><<<1, 256, 0, st>>>(A, SV);
+    else k_shard_init<int32_t><<<1, 256, 0, st>>>(A, SV);
     return cudaGetLastError();
 }
 
@@ -298,6 +298,30 @@ cudaError_t launch_shard_apply(const SearchArgs &A, const ShardBufs &B, const vo
 cudaError_t launch_shard_finish(const SearchArgs &A, const ShardBufs &B, cudaStream_t st) {
     ShardViews SV = make_views(B, nullptr, 0);
     k_shard_finish<<<1, 1, 0, st>>>(A, SV);
+    return cudaGetLastError();
+}
+
+// Best run of a batch: min over runs of (best_obj << 32 | global run).
+__global__ void k_batch_best(const as_run_result *res, int n_runs, int64_t run_offset, unsigned long long *key) {
+    unsigned long long k = KEY_NONE;
+    for (int r = threadIdx.x; r < n_runs; r += blockDim.x) {
+        if (res[r].stop_reason == AS_STOP_INFEASIBLE_START) continue;
+        const unsigned long long c = ((unsigned long long)res[r].best_obj << 32) | (unsigned long long)(run_offset + r);
+        k = c < k ? c : k;
+    }
+    __shared__ unsigned long long red[32];
+    k = wmin(k);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) k = red[w] < k ? red[w] : k;
+        *key = red[0] < k ? red[0] : k;
+    }
+}
+
+cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_offset, unsigned long long *key,
+                              cudaStream_t st) {
+    k_batch_best<<<1, 256, 0, st>>>(res, n_runs, run_offset, key);
     return cudaGetLastError();
 }
 

@@ -429,3 +429,25 @@ def test_sharded_nccl_one_rank(A, ctx, oracle_mod):
         assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
         assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and g["best_obj"] == o["best_obj"]
         assert routes_of(*g["best"]) == routes_of(*o["best"])
+
+
+def test_batch_gather_best(A, ctx, oracle_mod):
+    """Best run of a batch (device MIN of (best_obj, run)) and its schedule; with and
+    without a one-rank NCCL communicator (allreduce + broadcast path)."""
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    R = 40
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
+    bm = np.zeros((R, inst.n_missions), np.int32)
+    prm = A.params(mode=1, tenure=10, max_iters=120, kick=6)
+    for comm in (None, A.Comm(ctx, 1, 0, A.as_comm_unique_id())):
+        A.as_batch_run(ctx, h, R, p, m, prm, seeds, results=res, best_ptr_out=bp, best_missions_out=bm, comm=comm)
+        g = A.as_batch_gather_best(ctx, h, R, bp, bm, comm=comm)
+        want = int(np.lexsort((np.arange(R), res["best_obj"]))[0])
+        assert g["best_run"] == want and g["best_obj"] == res[want]["best_obj"]
+        assert routes_of(*g["best"]) == routes_of(bp[want], bm[want])
+        assert O.objective(*g["best"]) == g["best_obj"] and O.feasible(*g["best"])
