@@ -59,6 +59,8 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.rows = []
+        self.times = []
+        self.t_mark = None
         self.proc = None
         self.thread = None
 
@@ -79,6 +81,11 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == len(self.FIELDS):
                 self.rows.append(parts)
+                self.times.append(time.perf_counter())
+
+    def mark(self):
+        """Start of the timed region (samples before it are dropped if enough remain)."""
+        self.t_mark = time.perf_counter()
 
     def stop(self):
         if self.proc is not None:
@@ -89,6 +96,10 @@ class ClockSampler:
                 self.proc.kill()
         if self.thread is not None:
             self.thread.join(timeout=2)
+        if self.t_mark is not None:
+            timed = [r for r, t in zip(self.rows, self.times) if t >= self.t_mark]
+            if len(timed) >= 3:
+                self.rows = timed
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -200,17 +211,18 @@ def run_gpu(args):
         A.as_batch_run(ctx, h, R, tp, tm, prm, ts, shared_start=True, results=tres, best_ptr_out=tbp,
                        best_missions_out=tbm, comm=comm)
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = ctx.kernel_launches
-    sampler = ClockSampler(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     iters_total = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     for k in range(args.steps):
         flush.zero_()                      # L2 flush between timed steps (outside the events)
         ev[k][0].record(stream)
@@ -314,10 +326,11 @@ def run_single(args):
     mode = A.AS_MODE_NS if args.ns else A.AS_MODE_TABU
     prm = A.params(mode=mode, tenure=cfg.tenure, max_iters=iters)
     fn = A.as_nbhd_run if args.ns else A.as_tabu_run
-    for _ in range(args.warmup):
-        fn(ctx, h, p, m, prm, want_best=False)
     sampler = ClockSampler(0)
     sampler.start()
+    for _ in range(args.warmup):
+        fn(ctx, h, p, m, prm, want_best=False)
+    sampler.mark()
     ms, its = [], 0
     for _ in range(args.steps):
         r = fn(ctx, h, p, m, prm, want_best=False)
@@ -340,7 +353,7 @@ def run_single(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--workload", default="batched")
