@@ -650,7 +650,9 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
         const int want_grid = env_int("AIRSCHED_GRID", -1);
         const bool kfits = kfit;
         const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000);
-        if (want_grid == 1 || (want_grid == -1 && (big || !kfits))) {
+        // small single runs: the same kernel on ONE CTA (no grid barrier)
+        const bool one_cta = !big && kfits && want_grid != 1 && env_int("AIRSCHED_ONE_CTA", 1) == 1;
+        if (want_grid == 1 || one_cta || (want_grid == -1 && (big || !kfits))) {
             auto &D = ctx->insts[I];
             const int tb = D.tpad_bytes;
             struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
@@ -669,7 +671,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;
-                grid_blocks = ctx->n_sm;
+                grid_blocks = one_cta ? 1 : ctx->n_sm;
                 (void)occ;
                 GA.Tglobal = D.Tpad;
                 void *p;
@@ -682,10 +684,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     if ((st = scratch(ctx, "g_E", (size_t)n * V * 4 + 4, &p)) != AS_OK) return st;
                     GA.Eglobal = (int32_t *)p;
                 }
-                const int warps_all = grid_blocks * 32;
+                const int warps_all = grid_blocks * 24;
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
                 const int64_t pairs = (int64_t)n * nTC + (int64_t)n * nSC / 2;
-                GA.G = (int)std::max<int64_t>(1, pairs / (4 * (int64_t)warps_all));
+                GA.G = (int)std::max<int64_t>(1, pairs / ((one_cta ? 1 : 4) * (int64_t)warps_all));
                 GA.G = std::max(1, env_int("AIRSCHED_GRID_G", GA.G));
             }
         }

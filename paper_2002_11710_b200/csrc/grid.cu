@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     __syncthreads();
     if (blockIdx.x == 0)
         for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
-    grid.sync();   // global tabu matrix initialised before anyone reads it
+    if (gridDim.x > 1) grid.sync();   // global tabu matrix initialised before anyone reads it
 
     ScoreCtx<TT, ET> SC;
     SC.Ts = Ts; SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     SC.mask = A.mask;
     const GridTiles GT = grid_tiles(n, V, GA.G);
     const int gwarp = blockIdx.x * nwarps + warp, nwarps_all = gridDim.x * nwarps;
+    const bool one = gridDim.x == 1;
     unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
 
     int it = 0;
@@ -186,15 +187,18 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         kmin = wmin(kmin);
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
+        uint64_t kcta = KEY_NONE;
         if (tid == 0) {
-            uint64_t k = red[0];
-            for (int w2 = 1; w2 < nwarps; w2++) k = red[w2] < k ? red[w2] : k;
-            if (k != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)k);
-            if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
+            kcta = red[0];
+            for (int w2 = 1; w2 < nwarps; w2++) kcta = red[w2] < kcta ? red[w2] : kcta;
+            if (!one) {
+                if (kcta != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)kcta);
+                if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
+            }
         }
-        grid.sync();
+        if (!one) grid.sync();   // a single CTA (small instances) needs no grid barrier
         if (tid == 0) {
-            const uint64_t k = __ldcg(&gkey[it % 3]);
+            const uint64_t k = one ? kcta : __ldcg(&gkey[it % 3]);
             int stop = 0;
             if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
             else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
