@@ -451,3 +451,15 @@ def test_batch_gather_best(A, ctx, oracle_mod):
         assert g["best_run"] == want and g["best_obj"] == res[want]["best_obj"]
         assert routes_of(*g["best"]) == routes_of(bp[want], bm[want])
         assert O.objective(*g["best"]) == g["best_obj"] and O.feasible(*g["best"])
+
+
+def test_per_cta_kernel_still_exact(A, ctx, oracle_mod, monkeypatch):
+    """k_search (one run per CTA, int32 layout) -- the path for tabu digests and
+    for instances outside the compact layout -- forced for a plain run."""
+    monkeypatch.setenv("AIRSCHED_ONE_CTA", "0")
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    _compare_run(A, ctx, O, h, p, m, 1, 10, 800, seed=2, kick=4)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, 800)
