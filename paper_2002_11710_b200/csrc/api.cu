@@ -692,6 +692,11 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             }
         }
     }
+    if (env_int("AIRSCHED_VERBOSE", 0))
+        fprintf(stderr, "[airsched] n=%d V=%d runs=%d single=%d -> %s (blocks %d, G %d, T_smem %d, E_smem %d, smem %zu)\n",
+                n, V, n_runs, (int)single, use_grid ? (grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
+                use_batch ? "k_batch" : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
+                use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_grid) {
         CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, 768, grid_smem, ctx->stream));
