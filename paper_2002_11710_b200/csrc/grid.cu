@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     SC.Ts = Ts; SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
+    SC.one = A.one; SC.neg = -A.one;
     const GridTiles GT = grid_tiles(n, V, GA.G);
     const int gwarp = blockIdx.x * nwarps + warp, nwarps_all = gridDim.x * nwarps;
     const bool one = gridDim.x == 1;

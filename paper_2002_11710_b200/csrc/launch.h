@@ -18,6 +18,7 @@ struct RunViewG {
 
 struct SearchArgs {
     DevInst inst;
+    int32_t one;                           // == 1 (opaque multiplier for FMA-pipe adds)
     int32_t n_runs;
     const int32_t *start_ptr, *start_ms;   // [R][V+1], [R][n] or shared
     int32_t shared_start;

@@ -26,6 +26,18 @@ constexpr int KR = 4;              // relocate tile: 4 x 32 target slots cached 
 constexpr int KS = 2;              // swap tile: 2 x 32 m2 missions cached per lane
 constexpr int NEG = -(1 << 29);    // "never feasible" margin
 
+// Integer adds and selects on the FMA pipe.  Blackwell issues IADD3 / LOP3 /
+// ISETP / SEL / VIMNMX on the ALU pipe and IMAD on the FMA pipe, each at half
+// rate (B300_MICROARCH.md, "fma vs alu split"); the scoring loops saturate the
+// ALU pipe (profiles/r01), so sums are written as mad.lo.s32 with a multiplier
+// the compiler cannot prove to be 1 (ScoreCtx::one == 1, ScoreCtx::neg == -1 at
+// run time) and land on the otherwise idle FMA pipe.  Exact integer results.
+__device__ __forceinline__ int madd(int a, int mul, int b) {   // a * mul + b
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(mul), "r"(b));
+    return r;
+}
+
 template <class TT, class ET>
 struct ScoreCtx {
     const TT *Ts;          // [NC][NL][NLp] travel times
@@ -38,6 +50,7 @@ struct ScoreCtx {
     const ET *E;           // [n][V] tabu expiry (TABU only)
     int n, V, S, NL, NLp, P;
     uint32_t Rb, mask;
+    int one, neg;          // 1 and -1, opaque to the compiler (see madd)
 };
 
 template <bool TABU, bool FULL, class TT, class ET>
@@ -97,6 +110,8 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
         const bool heli_m = MH[m] != 0;
         const ET *Erow = TABU ? E + m * V : nullptr;
         const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
+        const int one = C.one, neg = C.neg;
+        const int wm_neg = madd(w_m, neg, 0);                      // -w_m
 #pragma unroll
         for (int k = 0; k < KR; k++) {
             const int t = t0 + lane + 32 * k;
@@ -104,20 +119,21 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
             const int b = (int)(int16_t)(inf & 0xFFFF);
             const bool cb1 = (inf >> 16) & 1;
             const bool hok = (inf >> 20) & 1;
-            const int T1 = (int)Ts[c_t1[k] + pick_m];
-            const int T2 = (int)Ts[c_t2[k] + rowD];
-            const int x1 = T1 + (cb1 ? svm1 : svm0);
-            const int ins = x1 + T2 + c_k[k];
-            const int delta = rem + ins;
+            const int T1 = (int)Ts[madd(c_t1[k], one, pick_m)];
+            const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];
+            const int x1 = madd(T1, one, cb1 ? svm1 : svm0);
+            const int ins = madd(x1, one, madd(T2, one, c_k[k]));
+            const int delta = madd(rem, one, ins);
             const bool same = b == a;
-            const int lim = same ? intra_lim : c_slk[k] + inter_bias;
-            const int mg = min(min(w_m + c_dw[k] - x1, c_wsv[k] - w_m - T2), lim - ins);
+            const int lim = same ? intra_lim : madd(c_slk[k], one, inter_bias);
+            const int mg = min(min(madd(x1, neg, madd(w_m, one, c_dw[k])), madd(T2, neg, madd(c_wsv[k], one, wm_neg))),
+                               madd(ins, neg, lim));
             const bool ok = (mg >= 0) & (t != m) & (t != s) & (FULL || (same ? en_intra_r : en_inter_r)) &
                             (hok | !heli_m);
             bool adm;
             if (TABU) adm = ((int)Erow[max(b, 0)] < it) | (delta < asp);
             else adm = delta < 0;
-            uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+            uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | (adm ? 0u : 0x80000000u);
             k32 = ok ? k32 : 0xFFFFFFFFu;
             const bool better = k32 < bk32;
             bk32 = better ? k32 : bk32;
@@ -196,6 +212,8 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
         const int sv10 = c1.z, sv11 = c1.w;
         const ET *Erow = TABU ? E + m1 * V : nullptr;
         const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
+        const int one = C.one, neg = C.neg;
+        const int ndepc1 = madd(depc1, neg, 0), nw1 = madd(w1, neg, 0);
 #pragma unroll
         for (int k = 0; k < KS; k++) {
             if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
@@ -206,22 +224,26 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
             const bool h2 = (inf >> 20) & 1, hokb = (inf >> 21) & 1;
             const int pick2 = q_ps[k] & 0xFFFF, s2 = (uint32_t)q_ps[k] >> 16;
             const bool same = a == b;
-            const int ya1 = (int)Ts[row_ya1 + pick2] + (ca ? q_sv1[k] : q_sv0[k]);   // p1 -> m2
-            const int Ta2 = (int)Ts[col_ta2 + q_d2[k]];                              // m2 -> s1
-            const int yb1 = (int)Ts[q_e2[k] + pick1] + (cb1 ? sv11 : sv10);          // p2 -> m1
-            const int Tb2 = (int)Ts[q_p2[k] + row_tb2];                              // m1 -> s2
-            const int da = ya1 + Ta2 + ka;
-            const int db = yb1 + Tb2 + q_kb[k];
-            const int delta = da + db;
-            const int mf = same ? slkA - delta : min(slkA - da, q_slk[k] - db);
-            const int mg = min(min(min(q_w2[k] - depc1 - ya1, wsv1 - q_w2[k] - Ta2),
-                                   min(w1 - q_dep2[k] - yb1, q_ws2[k] - w1 - Tb2)), mf);
+            const int ya1 = madd((int)Ts[madd(row_ya1, one, pick2)], one, ca ? q_sv1[k] : q_sv0[k]); // p1 -> m2
+            const int Ta2 = (int)Ts[madd(col_ta2, one, q_d2[k])];                              // m2 -> s1
+            const int yb1 = madd((int)Ts[madd(q_e2[k], one, pick1)], one, cb1 ? sv11 : sv10);  // p2 -> m1
+            const int Tb2 = (int)Ts[madd(q_p2[k], one, row_tb2)];                             // m1 -> s2
+            const int da = madd(ya1, one, madd(Ta2, one, ka));
+            const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
+            const int delta = madd(da, one, db);
+            const int mA = madd(da, neg, slkA), mB = madd(db, neg, q_slk[k]);
+            const int mf = same ? madd(delta, neg, slkA) : min(mA, mB);
+            const int mg = min(min(min(madd(ya1, neg, madd(q_w2[k], one, ndepc1)),
+                                       madd(Ta2, neg, madd(q_w2[k], neg, wsv1))),
+                                   min(madd(yb1, neg, madd(q_dep2[k], neg, w1)),
+                                       madd(Tb2, neg, madd(q_ws2[k], one, nw1)))),
+                               mf);
             const bool ok = (mg >= 0) & (m2 > m1) & (s1 != m2) & (s2 != m1) &
                             (FULL || (same ? en_intra_s : en_inter_s)) & (!h2 | hoka) & (!heli1 | hokb);
             bool adm;
             if (TABU) adm = (((int)Erow[max(b, 0)] < it) & ((int)E[max(m2, 0) * V + a] < it)) | (delta < asp);
             else adm = delta < 0;
-            uint32_t k32 = (uint32_t)(delta + DELTA_BIAS) | (adm ? 0u : 0x80000000u);
+            uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | (adm ? 0u : 0x80000000u);
             k32 = ok ? k32 : 0xFFFFFFFFu;
             const bool better = k32 < bk32;
             bk32 = better ? k32 : bk32;

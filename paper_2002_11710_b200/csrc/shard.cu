@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(768, 1) k_shard_eval(SearchArgs A, ShardViews 
     SC.LK = SV.LK; SC.F = SV.F; SC.E = SV.E;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = I.NL; SC.NLp = SV.NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
+    SC.one = A.one; SC.neg = -A.one;
     const GridTiles GT = grid_tiles(n, V, G);
     const int it = ctl->it;
     const long long cur = ctl->cur, best = ctl->best;
