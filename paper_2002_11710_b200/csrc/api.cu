@@ -66,7 +66,7 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
         return fail(AS_ERR_INVALID_ARG, "null array");
     if (n > 0 && (!d->pickup_loc || !d->delivery_loc || !d->deadline_s || !d->heli_only))
         return fail(AS_ERR_INVALID_ARG, "null mission array");
-    if (d->flight_limit_s <= 0 || d->day_length_s < d->flight_limit_s)
+    if (d->flight_limit_s <= 0 || d->flight_limit_s >= (1 << 30) || d->day_length_s < d->flight_limit_s)
         return fail(AS_ERR_INVALID_ARG, "need flight_limit_s > 0 and day_length_s >= flight_limit_s (SPEC S:117)");
     std::unique_ptr<as_instance> I(new (std::nothrow) as_instance());
     if (!I) return fail(AS_ERR_OOM, "host allocation");
@@ -364,6 +364,10 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
     D.d.svc = (const int32_t *)svc;
     D.d.n = I->n; D.d.V = I->V; D.d.NL = I->NL; D.d.NC = I->NC; D.d.P = I->P; D.d.DAY = I->DAY;
     D.d.maxT = I->maxT;
+    D.d.svcpos = 1;
+    for (int c = 0; c < I->NC; c++)
+        for (int m = 0; m < I->n; m++)
+            if (hT(I, c, I->pick[m], I->del[m]) <= 0) D.d.svcpos = 0;
     D.tpad_bytes = I->maxT <= 65535 ? 2 : 4;
     {
         const int NLp = padded_stride_host(I->NL, D.tpad_bytes);

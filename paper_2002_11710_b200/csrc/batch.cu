@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
         // Per-lane best inside a tile (score.cuh); tiles merged through the 64-bit key.
         // ============================ relocate block ============================
         for (int t0 = 0; t0 < S; t0 += 32 * KR) {
-            const uint64_t kb = score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
+            const uint64_t kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
+                                     : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
         }
         // ============================== swap block ==============================
@@ -239,7 +240,8 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
         // lowest chunk is ragged; adjacent pairs are excluded there and scored exactly
         // by the generic three-link formula below.
         for (int hi = n; hi > 1; hi -= 32 * KS) {
-            const uint64_t kb = score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
+            const uint64_t kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
+                                     : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
         }
         // adjacent pairs (x, succ x): the exact three-link formula (engine.cuh)
@@ -336,7 +338,7 @@ static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStr
 
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,
                          cudaStream_t st) {
-    const bool full = (A.mask & 15u) == 15u;
+    const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     if (mode == 1) {
         if (tbytes == 2 && ebytes == 2)
             return full ? launch_one<true, uint16_t, int16_t, true>(A, RPC, smem, st)

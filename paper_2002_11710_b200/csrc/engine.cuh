@@ -40,6 +40,7 @@ struct DevInst {
     const int32_t *svc;      // [NC][n] = T_c[pick][del] (pickup->delivery leg)
     int32_t n, V, NL, NC, P, DAY;
     int32_t maxT;            // max travel time (selects the uint16 table)
+    int32_t svcpos;          // every pickup->delivery leg > 0 in every class (enables the FAST scorers)
 };
 
 // Selection key (O9): class bit 63, biased delta bits 62..32, index bits 31..0.

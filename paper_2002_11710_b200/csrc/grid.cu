@@ -278,7 +278,7 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
     const DevInst &I = A.inst;
     GA.NLp = padded_stride(I.NL, tbytes);
     GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, 4, GA.T_smem, GA.E_smem, mode == 1);
-    const bool full = (A.mask & 15u) == 15u;
+    const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     cudaError_t err;
     if (mode == 1) {
         if (tbytes == 2) err = full ? launch_g<true, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)

@@ -253,6 +253,227 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
 }
 
 // ---------------------------------------------------------------------------
+// FAST scorers: every move kind enabled AND every pickup->delivery leg > 0 in
+// every class (DevInst::svcpos).  Then the two no-op relocate targets (t = m,
+// t = succ m) and the adjacent swap pairs fail a link check by construction
+// (their margins are -svc < 0), so no per-move validity test is
+// needed; feasibility, compatibility and the triangle m1 < m2 are folded into
+// one integer margin whose sign bit poisons the key, and admissibility is a
+// sign-bit expression -- the scoring loops are issue-bound, so every
+// compare/select removed counts.
+template <bool TABU, bool HELI, class TT, class ET>
+__device__ __forceinline__ void reloc_row_fast(const TT *Ts, const ET *Erow, const int (&c_t1)[KR],
+                                               const int (&c_t2)[KR], const int (&c_dw)[KR], const int (&c_k)[KR],
+                                               const int (&c_wsv)[KR], const int (&c_slk)[KR],
+                                               const int (&c_b)[KR], const int (&c_cb)[KR], int a, int rem,
+                                               int inter_bias, int intra_lim, int w_m, int pick_m, int rowD,
+                                               int svm0, int dsvm, int it, int asp, uint32_t base, int one,
+                                               int neg, uint32_t &bk32, uint32_t &bidx) {
+    const int wm_neg = madd(w_m, neg, 0);
+#pragma unroll
+    for (int k = 0; k < KR; k++) {
+        const int T1 = (int)Ts[madd(c_t1[k], one, pick_m)];
+        const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];
+        const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));                 // d(c, m)
+        const int ins = madd(x1, one, madd(T2, one, c_k[k]));
+        const int delta = madd(rem, one, ins);
+        // inter-route limit P - F_b (bit 30 of c_slk = vehicle may not fly a heli-only mission)
+        const int slk = HELI ? ((int)((uint32_t)c_slk[k] << 1) >> 1) : (c_slk[k] & 0x3FFFFFFF);
+        const int lim = c_b[k] == a ? intra_lim : madd(slk, one, inter_bias);
+        const int mg = min(min(madd(x1, neg, madd(w_m, one, c_dw[k])), madd(T2, neg, madd(c_wsv[k], one, wm_neg))),
+                           madd(ins, neg, lim));
+        uint32_t nadm;
+        if (TABU) {
+            const int e1 = madd(it, neg, (int)Erow[c_b[k]]);   // E[m][b] - it  (>= 0: tabu)
+            const int e2 = madd(asp, neg, delta);              // delta - asp   (>= 0: no aspiration)
+            nadm = ~(uint32_t)(e1 | e2) & 0x80000000u;
+        } else {
+            nadm = ~(uint32_t)delta & 0x80000000u;             // NS: admissible iff delta < 0
+        }
+        const uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | nadm | (uint32_t)(mg >> 31);
+        const bool better = k32 < bk32;
+        bk32 = better ? k32 : bk32;
+        bidx = better ? base + 32 * k : bidx;
+    }
+}
+
+template <bool TABU, class TT, class ET>
+__device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
+                                                     int asp, int lane) {
+    const TT *Ts = C.Ts;
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint8_t *MH = C.MH;
+    const uint32_t *VC = C.VC, *LK = C.LK;
+    const int32_t *F = C.F;
+    const ET *E = C.E;
+    const int V = C.V, S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
+    const int one = C.one, neg = C.neg;
+    int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) {
+        const int t = t0 + lane + 32 * k;
+        int t1 = 0, t2 = 0, dw = 0, kk = 0, wsv = NEG, slk = 0, b = -1, cb = 0;
+        if (t < S) {
+            const int4 rs = RS4[t];
+            const int bb = (int16_t)((uint32_t)rs.w >> 16);
+            if (bb >= 0) {
+                const int4 cs = CS4[t];
+                const uint32_t vc = VC[bb];
+                b = bb;
+                cb = vc & 0xFF;
+                t1 = (cb * NL + (rs.w & 0xFFFF)) * NLp;     // row of T_cb[endc(t)][.]
+                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb
+                dw = -rs.x;                                  // -dep(pred t)
+                kk = rs.z - rs.y;                            // svco(t) - inc(t)
+                wsv = cs.x - rs.z;                           // w(t) - svco(t)
+                slk = (P - F[bb]) | (((vc >> 8) & 1) ? 0 : (1 << 30));
+            }
+        }
+        c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
+        c_cb[k] = cb;
+    }
+    uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+    for (int m = m_lo; m < m_hi; m++) {
+        const int4 rm = RS4[m];
+        const int a = (int16_t)((uint32_t)rm.w >> 16);
+        if (a < 0) continue;
+        const int s = LK[m] & 0xFFFF;
+        const int4 rsx = RS4[s];
+        const int4 csx = CS4[s];
+        const int ca = VC[a] & 0xFF;
+        const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+        if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
+        const int rem = Dps - rm.y - rsx.y;
+        const int4 cm = CS4[m];
+        const int Fa = F[a];
+        const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
+        const int intra_lim = P - Fa - rem;
+        const int w_m = cm.x, pick_m = cm.y & 0xFFFF, rowD = ((uint32_t)cm.y >> 16) * NLp;
+        const ET *Erow = TABU ? E + m * V : nullptr;
+        const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
+        if (MH[m])
+            reloc_row_fast<TABU, true>(Ts, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
+                                       intra_lim, w_m, pick_m, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
+                                       bidx);
+        else
+            reloc_row_fast<TABU, false>(Ts, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
+                                        intra_lim, w_m, pick_m, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
+                                        bidx);
+    }
+    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+}
+
+template <bool TABU, class TT, class ET>
+__device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, int hi, int m1_lo, int m1_hi, int it,
+                                                    int asp, int lane) {
+    const TT *Ts = C.Ts;
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint8_t *MH = C.MH;
+    const uint32_t *VC = C.VC, *LK = C.LK;
+    const int32_t *F = C.F;
+    const ET *E = C.E;
+    const int n = C.n, V = C.V, NL = C.NL, NLp = C.NLp, P = C.P;
+    const uint32_t Rb = C.Rb;
+    const int one = C.one, neg = C.neg;
+    const int lo = hi - 32 * KS;
+    // m2-side cache; q_f: bit 20 = m2 heli-only, bit 21 = vehicle of m2 cannot fly heli-only
+    int q_p2m[KS], q_sv0[KS], q_dsv[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS],
+        q_slk[KS], q_bf[KS];
+    int q_cb[KS];
+#pragma unroll
+    for (int k = 0; k < KS; k++) {
+        const int m2 = lo + lane + 32 * k;
+        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = 0, p2 = 0, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
+            bf = -1, cb = 0;
+        if (m2 >= 0) {
+            const int4 r2 = RS4[m2];
+            const int b = (int16_t)((uint32_t)r2.w >> 16);
+            if (b >= 0) {
+                const int4 c2 = CS4[m2];
+                const uint32_t vc = VC[b];
+                cb = vc & 0xFF;
+                const int s2 = LK[m2] & 0xFFFF;
+                const int4 rs2 = RS4[s2];
+                const int4 cs2 = CS4[s2];
+                p2m = c2.y & 0xFFFF;                              // pick2
+                sv0 = c2.z;
+                dsv = c2.w - c2.z;
+                d2 = ((uint32_t)c2.y >> 16) * NLp;               // row del2 (any class)
+                e2 = (cb * NL + (r2.w & 0xFFFF)) * NLp;           // row T_cb[endc2]
+                p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
+                w2 = c2.x;
+                dep2 = r2.x;
+                kb = rs2.z - r2.y - rs2.y;                        // svco(s2) - inc2 - inc(s2)
+                ws2 = cs2.x - rs2.z;                              // w(s2) - svco(s2)
+                slk = P - F[b];
+                bf = b | ((int)MH[m2] << 20) | ((((vc >> 8) & 1) ? 0 : 1) << 21);
+            }
+        }
+        q_p2m[k] = p2m; q_sv0[k] = sv0; q_dsv[k] = dsv; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2;
+        q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_cb[k] = cb;
+    }
+    uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+    for (int m1 = m1_lo; m1 < m1_hi; m1++) {
+        const int4 r1 = RS4[m1];
+        const int a = (int16_t)((uint32_t)r1.w >> 16);
+        if (a < 0) continue;
+        const int s1 = LK[m1] & 0xFFFF;
+        const int4 c1 = CS4[m1];
+        const int4 rs1 = RS4[s1];
+        const int4 cs1 = CS4[s1];
+        const uint32_t vca = VC[a];
+        const int ca = vca & 0xFF;
+        const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
+        const int col_ta2 = ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
+        const int pick1 = c1.y & 0xFFFF, row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+        const int ndepc1 = -r1.x, w1 = c1.x, nw1 = -c1.x;
+        const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
+        const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
+        const int slkA = P - F[a];
+        const int sv10 = c1.z, dsv1 = c1.w - c1.z;
+        // compatibility mask over q_bf: m1 heli-only needs bit 21 clear; m2 heli-only (bit 20) needs route a heli-ok
+        const int cmask = (MH[m1] ? (1 << 21) : 0) | (((vca >> 8) & 1) ? 0 : (1 << 20));
+        const ET *Erow = TABU ? E + m1 * V : nullptr;
+        const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
+        const int tri = -m1 - 1;
+#pragma unroll
+        for (int k = 0; k < KS; k++) {
+            if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+            const int m2 = lo + lane + 32 * k;
+            const int bf = q_bf[k];
+            const int b = (int)(int16_t)(bf & 0xFFFF);
+            const int ya1 = madd(q_dsv[k], ca, madd((int)Ts[madd(row_ya1, one, q_p2m[k])], one, q_sv0[k]));  // p1 -> m2
+            const int Ta2 = (int)Ts[madd(col_ta2, one, q_d2[k])];                                        // m2 -> s1
+            const int yb1 = madd(q_cb[k], dsv1, madd((int)Ts[madd(q_e2[k], one, pick1)], one, sv10));    // p2 -> m1
+            const int Tb2 = (int)Ts[madd(q_p2[k], one, row_tb2)];                                       // m1 -> s2
+            const int da = madd(ya1, one, madd(Ta2, one, ka));
+            const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
+            const int delta = madd(da, one, db);
+            const int mf = a == b ? madd(delta, neg, slkA) : min(madd(da, neg, slkA), madd(db, neg, q_slk[k]));
+            // link margins; the triangle m2 > m1 and compatibility are folded into the first one
+            const int l1 = madd(bf & cmask, -512, madd(ya1, neg, madd(q_w2[k], one, ndepc1)));
+            const int mg = min(min(min(l1, madd(Ta2, neg, madd(q_w2[k], neg, wsv1))),
+                                   min(madd(yb1, neg, madd(q_dep2[k], neg, w1)), madd(Tb2, neg, madd(q_ws2[k], one, nw1)))),
+                               min(mf, madd(m2, one, tri)));
+            uint32_t nadm;
+            if (TABU) {
+                const int t1 = madd(it, neg, (int)Erow[b]);                      // E[m1][b] - it
+                const int t2 = madd(it, neg, (int)E[max(m2, 0) * V + a]);        // E[m2][a] - it
+                const int e2 = madd(asp, neg, delta);
+                nadm = ~(uint32_t)((t1 & t2) | e2) & 0x80000000u;
+            } else {
+                nadm = ~(uint32_t)delta & 0x80000000u;
+            }
+            const uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | nadm | (uint32_t)(mg >> 31);
+            const bool better = k32 < bk32;
+            bk32 = better ? k32 : bk32;
+            bidx = better ? base + 32 * k : bidx;
+        }
+    }
+    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+}
+
+// ---------------------------------------------------------------------------
 // Flat tile list of one neighbourhood (used by the whole-GPU and the sharded
 // kernels): relocate tiles (t-chunk, row group), swap tiles (top-aligned m2
 // chunk, row group), adjacent-swap tiles (32 missions each).
@@ -288,13 +509,16 @@ __device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, cons
         if (tile < GT.n_reloc) {
             const int c = tile % GT.nTC, g = tile / GT.nTC;
             const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
-            kb = score_reloc<TABU, FULL>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
+            kb = FULL ? score_reloc_fast<TABU>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane)
+                      : score_reloc<TABU, FULL>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
         } else if (tile < GT.n_reloc + GT.n_swap) {
             const int r = tile - GT.n_reloc;
             const int j = r % GT.nSC, g = r / GT.nSC;
             const int hi = n - j * 32 * KS;
             const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
-            if (m_lo < m_hi) kb = score_swap<TABU, FULL>(SC, hi, m_lo, m_hi, it, asp, lane);
+            if (m_lo < m_hi)
+                kb = FULL ? score_swap_fast<TABU>(SC, hi, m_lo, m_hi, it, asp, lane)
+                          : score_swap<TABU, FULL>(SC, hi, m_lo, m_hi, it, asp, lane);
         } else {
             const int x = (tile - GT.n_reloc - GT.n_swap) * 32 + lane;
             if (x < n && (FULL || (SC.mask & 8u))) {

@@ -263,7 +263,7 @@ cudaError_t launch_shard_eval(const SearchArgs &A, const ShardBufs &B, const voi
                               int tlo, int thi, int blocks, cudaStream_t st) {
     const int NLp = padded_stride(A.inst.NL, tbytes);
     ShardViews SV = make_views(B, Tpad, NLp);
-    const bool full = (A.mask & 15u) == 15u;
+    const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     if (mode == 1) {
         if (tbytes == 2) {
             if (full) k_shard_eval<true, uint16_t, true><<<blocks, 768, 0, st>>>(A, SV, G, tlo, thi);
