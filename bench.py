@@ -312,41 +312,66 @@ def run_gpu(args):
 def run_single(args):
     """Single-instance workloads (C1 tiny, C2 ontario, C4 large, C5 surge): one step =
     one as_tabu_run (or as_nbhd_run with --ns) of max_iters iterations from the
-    Alg. 1 start; device time from CUDA events around the kernel launch."""
+    Alg. 1 start; device time from CUDA events around the kernel launches.  Under
+    torchrun (N > 1) the ONE instance's move space is sharded over the ranks with an
+    8-byte NCCL MIN per iteration (strong scaling; time = max over ranks)."""
     import torch
+    import torch.distributed as dist
     from paper_2002_11710_b200 import airsched as A
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
     cfg, inst = workload(args.workload)
     iters = args.iters or cfg.max_iters
     h = A.Instance(inst)
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    ctx = A.Ctx(0, stream.cuda_stream)
+    ctx = A.Ctx(local, stream.cuda_stream)
     ctx.upload(h)
     p, m, _ = A.as_init_greedy(ctx, h)
+    comm = A.Comm.from_torch_distributed(ctx) if world > 1 else None
     mode = A.AS_MODE_NS if args.ns else A.AS_MODE_TABU
     prm = A.params(mode=mode, tenure=cfg.tenure, max_iters=iters)
-    fn = A.as_nbhd_run if args.ns else A.as_tabu_run
-    sampler = ClockSampler(0)
+
+    def fn():
+        f = A.as_nbhd_run if args.ns else A.as_tabu_run
+        return f(ctx, h, p, m, prm, want_best=False, comm=comm)
+
+    sampler = ClockSampler(local)
     sampler.start()
     for _ in range(args.warmup):
-        fn(ctx, h, p, m, prm, want_best=False)
+        fn()
+    if world > 1:
+        dist.barrier()
     sampler.mark()
     ms, its = [], 0
     for _ in range(args.steps):
-        r = fn(ctx, h, p, m, prm, want_best=False)
+        r = fn()
         ms.append(ctx.last_kernel_ms)
         its += r["iters_done"]
     clocks = sampler.stop()
     t = sum(ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
     VM = valid_moves(inst)
-    line = {"metric": METRIC, "value": its * VM / t, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+    line = {"metric": METRIC, "value": its * VM / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
             "config": {"workload": f"{args.workload}: n={inst.n_missions}, V={inst.n_vehicles}, "
-                                   f"{'NS' if args.ns else 'TS'} {iters} iters", "valid_moves_per_iter": VM},
+                                   f"{'NS' if args.ns else 'TS'} {iters} iters", "valid_moves_per_iter": VM,
+                       "parallelism": f"move space sharded over {world} GPUs" if world > 1 else "1 GPU"},
             "tabu_iters_per_s": its / t, "iters_done_per_step": its / args.steps, "best_obj": r["best_obj"],
             "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches}
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
