@@ -463,3 +463,34 @@ def test_per_cta_kernel_still_exact(A, ctx, oracle_mod, monkeypatch):
     p, m = start_of(O, inst)
     _compare_run(A, ctx, O, h, p, m, 1, 10, 800, seed=2, kick=4)
     _compare_run(A, ctx, O, h, p, m, 0, 0, 800)
+
+
+def test_bench_configuration_sampled_runs(A, ctx, oracle_mod):
+    """BASELINE configs[2] at full size in bench.py's launch configuration: 4096 runs
+    x 1000 iterations, shared start from Alg. 1, seeds 1..4096, kick 8, device-resident
+    inputs and outputs; sampled runs must equal the oracle run for run."""
+    import torch
+    inst = instgen.generate("batched")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    c = instgen.CONFIGS["batched"]
+    p, m, _ = A.as_init_greedy(ctx, h)
+    R, iters = c.n_runs, c.max_iters
+    dev = torch.device("cuda:0")
+    tp, tm = torch.from_numpy(p).to(dev), torch.from_numpy(m).to(dev)
+    ts = torch.from_numpy(np.arange(1, R + 1, dtype=np.uint64).view(np.int64)).to(dev)
+    tres = torch.zeros((R, 40), dtype=torch.uint8, device=dev)
+    tbp = torch.zeros((R, inst.n_vehicles + 1), dtype=torch.int32, device=dev)
+    tbm = torch.zeros((R, inst.n_missions), dtype=torch.int32, device=dev)
+    prm = A.params(mode=1, tenure=c.tenure, max_iters=iters, kick=c.kick)
+    A.as_batch_run(ctx, h, R, tp, tm, prm, ts, shared_start=True, results=tres, best_ptr_out=tbp,
+                   best_missions_out=tbm)
+    torch.cuda.synchronize()
+    res = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(R)
+    bp, bm = tbp.cpu().numpy(), tbm.cpu().numpy()
+    assert (res["iters_done"] == iters).all()
+    for r in (0, 1234, 4095):
+        o = O.search(p, m, mode=1, tenure=c.tenure, max_iters=iters, seed=r + 1, kick=c.kick, trace=False)
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["final_obj"] == o["final_obj"]
+        assert res[r]["best_iter"] == o["best_iter"] and res[r]["kicks_applied"] == o["kicks_applied"]
+        assert routes_of(bp[r], bm[r]) == routes_of(*o["best"])
