@@ -88,7 +88,7 @@ def main():
              "GPU ms NS / TS |", "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         opt = r["opt_h"]
-        g = (lambda a: f"{100 * (a - opt) / opt:.2f} %") if opt else (lambda a: "—")
+        g = (lambda a: f"{abs(100 * (a - opt) / opt) if abs(a - opt) < 1e-9 else 100 * (a - opt) / opt:.2f} %") if opt else (lambda a: "—")
         lines.append(f"| {r['n']} | {r['start_h']:.3f} | {opt:.3f} | {r['t_ilp']:.1f} | " if opt else
                      f"| {r['n']} | {r['start_h']:.3f} | — | {r['t_ilp']:.1f} | ")
         lines[-1] += (f"{r['NS']['U']:.3f} / {r['NS']['L']:.3f} / {r['NS']['A']:.3f} | "
