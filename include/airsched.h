@@ -157,6 +157,14 @@ typedef struct {
     int32_t strict_tabu_stop; /* TS: stop (reason 2) instead of the by-default move */
     int32_t trace_level;      /* 0 none, 1 per-iteration records, 2 + tabu-list digest */
     uint64_t seed;            /* run seed; 0 = start unchanged */
+    int32_t sweep;            /* 0: north_star's global-best iteration (every move, one best per
+                                 iteration).  1: the paper-literal sweep of Alg. 2 / Alg. 3 (P:294-336,
+                                 P:362-415): for each vehicle i, for each mission j of route i,
+                                 apply the best admissible inter-route relocate of j; one iteration =
+                                 one (i, j) step, max_iters = steps; seed != 0 permutes the vehicle and
+                                 mission order each sweep; kick and move_mask are ignored.
+                                 Runs on the batched kernel (as_batch_run, as_tabu_run, as_nbhd_run). */
+    int32_t reserved;
 } as_run_params;
 
 enum { AS_STOP_MAX_ITERS = 0, AS_STOP_LOCAL_OPT = 1, AS_STOP_NO_MOVE = 2, AS_STOP_INFEASIBLE_START = 3 };

@@ -197,6 +197,22 @@ class Oracle:
             out["trace"] = {key: val[:k].copy() for key, val in tr.items()}
         return out
 
+    def sweep(self, ptr, ms, mode=MODE_TABU, tenure=10, max_steps=100, seed=0):
+        """f1: Alg. 2 / Alg. 3 as written -- one (vehicle, mission) step at a time."""
+        length, r = self.to_lists(ptr, ms)
+        bl, br = np.zeros_like(length), np.zeros_like(r)
+        K = max(int(max_steps), 1)
+        tr = dict(idx=np.zeros(K, np.int64), delta=np.zeros(K, np.int32), cur=np.zeros(K, np.int64),
+                  best=np.zeros(K, np.int64))
+        prm = _Params(int(mode), int(tenure), int(max_steps), 0, 0, 0, 1, int(seed))
+        res = _Result()
+        lib().or_sweep(self.ref, _p(length), _p(r), C.byref(prm), _p(bl), _p(br), C.byref(res), _p(tr["idx"]),
+                       _p(tr["delta"]), _p(tr["cur"]), _p(tr["best"]))
+        k = res.iters_done
+        return dict(best_obj=res.best_obj, final_obj=res.final_obj, start_obj=res.start_obj, best_iter=res.best_iter,
+                    iters_done=k, stop_reason=res.stop_reason, best=self.to_csr(bl, br),
+                    trace={key: val[:k].copy() for key, val in tr.items()})
+
     def kick(self, ptr, ms, seed, kick):
         length, r = self.to_lists(ptr, ms)
         applied = lib().or_kick(self.ref, _p(length), _p(r), int(seed), int(kick))

@@ -622,3 +622,104 @@ int32_t or_greedy(const or_inst *I, int32_t insert_mode, int32_t max_repairs, in
     free(order); free(tmp); free(len2); free(r2);
     return status;
 }
+
+/* ------------------------------------------------------- f1: Alg. 2 / 3 sweep */
+/* The paper-literal sweep (reading #39): for each
+ * vehicle i ("for i <- 1 to number of bases"; seeded permutation vectors,
+ * P:269), for each mission j of route i as it stood when i's turn began,
+ * CurrentMin = the best (delta, idx) inter-route relocate of j (k != i, P:299-301;
+ * every position) that is feasible and admissible (NS: delta
+ * < 0; TS: (j, k) not tabu or cur + delta < best); if CurrentMin is not
+ * empty it is applied (P:331-333 / P:408-411) and, in TS, (j, i) becomes tabu for
+ * `tenure` steps (expiry = step + tenure, one step per (i, j)).  NS stops
+ * after a sweep without a move ("while improvement"); TS after max_steps or
+ * a sweep without a move.  Permutations: SplitMix64(seed), Fisher-Yates from the
+ * top, vehicles first then each route snapshot; seed 0 = identity order. */
+int32_t or_sweep(const or_inst *I, const int32_t *len0, const int32_t *r0, const or_params *prm,
+                 int32_t *best_len, int32_t *best_r, or_result *res, int64_t *tr_idx, int32_t *tr_delta,
+                 int64_t *tr_cur, int64_t *tr_best) {
+    int32_t n = I->n, V = I->V;
+    size_t rs = sizeof(int32_t) * (size_t)V * (size_t)(n > 0 ? n : 1);
+    int32_t *len = (int32_t *)malloc(sizeof(int32_t) * (size_t)V);
+    int32_t *r = (int32_t *)malloc(rs);
+    int32_t *E = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1) * (size_t)V);
+    int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)V);
+    int32_t *snap = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    memcpy(len, len0, sizeof(int32_t) * (size_t)V);
+    memcpy(r, r0, rs);
+    for (int64_t k = 0; k < (int64_t)n * V; k++) E[k] = -1;
+    memset(res, 0, sizeof(*res));
+    int64_t cur = or_objective(I, len, r), best = cur;
+    res->start_obj = cur;
+    res->best_iter = -1;
+    memcpy(best_len, len, sizeof(int32_t) * (size_t)V);
+    memcpy(best_r, r, rs);
+    uint64_t s = prm->seed;
+    int32_t step = 0, stop = 0;
+    const int64_t S = (int64_t)n + V;
+    while (!stop && step < prm->max_iters) {
+        int32_t moved = 0;
+        for (int32_t v = 0; v < V; v++) perm[v] = v;
+        if (prm->seed)
+            for (int32_t x = V - 1; x >= 1; x--) {
+                int32_t y = (int32_t)(or_splitmix64_next(&s) % (uint64_t)(x + 1));
+                int32_t tmp = perm[x]; perm[x] = perm[y]; perm[y] = tmp;
+            }
+        for (int32_t pi = 0; pi < V && !stop; pi++) {
+            int32_t i = perm[pi];
+            int32_t L = len[i];
+            memcpy(snap, r + (int64_t)i * n, sizeof(int32_t) * (size_t)L);
+            if (prm->seed)
+                for (int32_t x = L - 1; x >= 1; x--) {
+                    int32_t y = (int32_t)(or_splitmix64_next(&s) % (uint64_t)(x + 1));
+                    int32_t tmp = snap[x]; snap[x] = snap[y]; snap[y] = tmp;
+                }
+            for (int32_t jj = 0; jj < L; jj++) {
+                int32_t j = snap[jj];
+                evalctx X;
+                evalctx_init(&X, I, len, r);
+                int64_t bidx = -1, bdelta = 0;
+                for (int64_t t = 0; t < S; t++) {
+                    move_t mv;
+                    int64_t delta;
+                    int32_t feas;
+                    int64_t idx = (int64_t)j * S + t;
+                    if (!eval_one(&X, len, r, idx, 1u /* inter-route relocate */, 0, &mv, &delta, &feas)) continue;
+                    if (!feas) continue;
+                    int32_t adm = prm->mode == OR_MODE_TABU ? (!is_tabu(I, &mv, E, step) || cur + delta < best)
+                                                            : delta < 0;
+                    if (adm && (bidx < 0 || delta < bdelta)) { bidx = idx; bdelta = delta; }
+                }
+                if (bidx >= 0) {
+                    move_t mv;
+                    int64_t d2;
+                    int32_t f2;
+                    eval_one(&X, len, r, bidx, 1u, 0, &mv, &d2, &f2);
+                    write_back(I, len, r, &mv, X.ra, X.rb);
+                    cur += bdelta;
+                    moved = 1;
+                    if (prm->mode == OR_MODE_TABU) E[(int64_t)mv.from_m[0] * V + mv.from_v[0]] = step + prm->tenure;
+                    if (cur < best) {
+                        best = cur;
+                        res->best_iter = step;
+                        memcpy(best_len, len, sizeof(int32_t) * (size_t)V);
+                        memcpy(best_r, r, rs);
+                    }
+                }
+                evalctx_free(&X);
+                if (tr_idx) tr_idx[step] = bidx;
+                if (tr_delta) tr_delta[step] = (int32_t)(bidx >= 0 ? bdelta : 0);
+                if (tr_cur) tr_cur[step] = cur;
+                if (tr_best) tr_best[step] = best;
+                step++;
+                if (step >= prm->max_iters) { stop = 1; break; }
+            }
+        }
+        if (!moved && !stop) { res->stop_reason = prm->mode == OR_MODE_NS ? 1 : 2; break; }
+    }
+    res->iters_done = step;
+    res->best_obj = best;
+    res->final_obj = cur;
+    free(len); free(r); free(E); free(perm); free(snap);
+    return 0;
+}

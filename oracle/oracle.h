@@ -90,6 +90,12 @@ int32_t or_search(const or_inst *I, const int32_t *len0, const int32_t *r0, cons
                   or_result *res, int64_t *tr_idx, int32_t *tr_delta, int64_t *tr_cur,
                   int64_t *tr_best, int32_t *tr_cls, uint64_t *tr_digest, int32_t *E_out);
 
+/* f1: the paper-literal (i, j) sweep of Alg. 2 / Alg. 3 (see oracle.c).  One
+ * trace entry per (i, j) step, idx -1 when CurrentMin stayed empty. */
+int32_t or_sweep(const or_inst *I, const int32_t *len0, const int32_t *r0, const or_params *prm,
+                 int32_t *best_len, int32_t *best_r, or_result *res, int64_t *tr_idx, int32_t *tr_delta,
+                 int64_t *tr_cur, int64_t *tr_best);
+
 /* The kick alone (O12): returns the number of relocates applied. */
 int32_t or_kick(const or_inst *I, int32_t *len, int32_t *r, uint64_t seed, int32_t kick);
 

@@ -49,7 +49,7 @@ class as_instance_desc(C.Structure):
 class as_run_params(C.Structure):
     _fields_ = [("mode", C.c_int32), ("tenure", C.c_int32), ("max_iters", C.c_int32), ("kick", C.c_int32),
                 ("move_mask", C.c_uint32), ("strict_tabu_stop", C.c_int32), ("trace_level", C.c_int32),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("sweep", C.c_int32), ("reserved", C.c_int32)]
 
 
 class as_run_result(C.Structure):
@@ -243,9 +243,9 @@ def as_shard_plan(inst: Instance, nranks: int, rank: int, n_sm: int = 148):
 
 
 def params(mode=AS_MODE_TABU, tenure=10, max_iters=100, kick=0, move_mask=AS_MOVE_ALL, strict_tabu_stop=0,
-           trace_level=0, seed=0) -> as_run_params:
+           trace_level=0, seed=0, sweep=0) -> as_run_params:
     return as_run_params(int(mode), int(tenure), int(max_iters), int(kick), int(move_mask), int(strict_tabu_stop),
-                         int(trace_level), int(seed))
+                         int(trace_level), int(seed), int(sweep), 0)
 
 
 # ---------------------------------------------------------------- entry points --

@@ -606,7 +606,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     A.tenure = P->tenure;
     A.max_iters = P->max_iters;
     A.strict_tabu_stop = P->strict_tabu_stop;
-    A.mask = P->move_mask;
+    A.mask = P->sweep ? 1u : P->move_mask;   // the sweep relocates between bases only
+    A.sweep = P->sweep ? 1 : 0;
     A.T_smem = T_smem;
     A.E_smem = E_smem;
     if (tabu && !E_smem) {
@@ -644,14 +645,16 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
     const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest;
     const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
-    bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single));
+    bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single) || P->sweep);
+    if (P->sweep && !use_batch)
+        return fail(AS_ERR_UNSUPPORTED, "the sweep mode runs on the batched kernel (compact layout required)");
     // single large instances: one persistent cooperative grid (k_grid)
     bool use_grid = false;
     GridArgs GA;
     memset(&GA, 0, sizeof(GA));
     size_t grid_smem = 0;
     int grid_blocks = 0;
-    if (single && compact_ok) {
+    if (single && compact_ok && !P->sweep) {
         const int want_grid = env_int("AIRSCHED_GRID", -1);
         const bool kfits = kfit;
         const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000);
@@ -748,7 +751,7 @@ extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *
     int64_t obj;
     as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
     if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
-    if (comm || env_int("AIRSCHED_SHARDED", 0) == 1) {
+    if ((comm || env_int("AIRSCHED_SHARDED", 0) == 1) && !P->sweep) {
         if (digest && P->trace_level >= 2) return fail(AS_ERR_UNSUPPORTED, "tabu digests are not produced by the sharded path");
         return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
     }

@@ -33,7 +33,7 @@ constexpr int MAXTHREADS = 896;    // <= 28 runs per CTA (one wave of 4096 runs 
 struct BatchLayout {
     int T, CS, MH, VC, CH;   // CTA-wide part
     int shared_bytes;
-    int RS, LK, BS, F, E;    // per-run part (offsets inside a run block)
+    int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
     int run_bytes;
 };
 
@@ -54,6 +54,8 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.BS = r; r = al16(r + S * 2);
     L.F = r; r = al16(r + V * 4);
     L.E = r; r = al16(r + (tabu ? n * V * ebytes : 0));
+    L.PM = r; r = al16(r + V * 2);
+    L.SN = r; r = al16(r + n * 2);
     L.run_bytes = r;
     return L;
 }
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
 
     // ---- seeded kick (O12), lane 0 -------------------------------------------
     int kicks = 0;
-    if (lane == 0) {
+    if (lane == 0 && !A.sweep) {
         uint64_t seed = A.seeds ? A.seeds[run] : A.seed;
         if (seed != 0 && n > 0) {
             uint64_t s = seed;
@@ -223,7 +225,89 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = Rb; SC.mask = mask;
     SC.one = A.one; SC.neg = -A.one;
     int it = 0, stop = 0;
-    for (; it < A.max_iters; it++) {
+    if (A.sweep) {
+        // ---- f1: the paper-literal (i, j) sweep of Alg. 2 / Alg. 3 (oracle or_sweep) ----
+        uint16_t *PM = reinterpret_cast<uint16_t *>(rb + L.PM);
+        uint16_t *SN = reinterpret_cast<uint16_t *>(rb + L.SN);
+        uint64_t ps = A.seeds ? A.seeds[run] : A.seed;
+        const bool shuffled = ps != 0;
+        while (!stop && it < A.max_iters) {
+            int moved = 0;
+            if (lane == 0) {
+                for (int v = 0; v < V; v++) PM[v] = (uint16_t)v;
+                if (shuffled)
+                    for (int x = V - 1; x >= 1; x--) {
+                        const int y = (int)(splitmix64_next(ps) % (uint64_t)(x + 1));
+                        const uint16_t tmp = PM[x]; PM[x] = PM[y]; PM[y] = tmp;
+                    }
+            }
+            __syncwarp();
+            for (int pi = 0; pi < V && !stop; pi++) {
+                int Lr = 0;
+                if (lane == 0) {
+                    const int i = PM[pi];
+                    for (int x = R.succ[n + i]; x < n && Lr < n; x = R.succ[x]) SN[Lr++] = (uint16_t)x;
+                    if (shuffled)
+                        for (int x = Lr - 1; x >= 1; x--) {
+                            const int y = (int)(splitmix64_next(ps) % (uint64_t)(x + 1));
+                            const uint16_t tmp = SN[x]; SN[x] = SN[y]; SN[y] = tmp;
+                        }
+                }
+                Lr = bcast(Lr);
+                __syncwarp();
+                for (int jj = 0; jj < Lr; jj++) {
+                    const int j = SN[jj];
+                    const int asp = (int)(best - cur);
+                    uint64_t kmin = KEY_NONE;
+                    for (int t0 = 0; t0 < S; t0 += 32 * KR) {
+                        const uint64_t kb = score_reloc<TABU, false>(SC, t0, j, j + 1, it, asp, lane);
+                        kmin = kb < kmin ? kb : kmin;
+                    }
+                    kmin = wmin(kmin);
+                    int improved = 0;
+                    if (lane == 0) {
+                        uint32_t idx = 0xFFFFFFFFu;
+                        int32_t dl = 0;
+                        if (kmin != KEY_NONE && key_cls(kmin) == 0) {     // CurrentMin not empty
+                            idx = key_idx(kmin);
+                            MoveEval e = eval_index(M, R, idx, mask, it);
+                            apply_move(M, R, idx, e, it, A.tenure, TABU);
+                            dl = e.delta;
+                            cur += e.delta;
+                            moved = 1;
+                            if (cur < best) {
+                                best = cur;
+                                best_it = it;
+                                improved = 1;
+                            }
+                        }
+                        if (A.trace) {
+                            as_trace_rec tr;
+                            tr.cur = cur;
+                            tr.best = best;
+                            tr.idx = idx;
+                            tr.delta = dl;
+                            tr.cls = idx == 0xFFFFFFFFu ? -1 : 0;
+                            tr.it = it;
+                            A.trace[(size_t)run * A.max_iters + it] = tr;
+                        }
+                    }
+                    cur = bcast(cur);
+                    best = bcast(best);
+                    improved = bcast(improved);
+                    __syncwarp();
+                    if (improved)
+                        for (int x = lane; x < S; x += 32) BS[x] = (uint16_t)(LK[x] & 0xFFFF);
+                    if (++it >= A.max_iters) { stop = 0; break; }
+                }
+                if (it >= A.max_iters) break;
+            }
+            moved = bcast(moved);
+            if (it >= A.max_iters) break;
+            if (!moved) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;   // a sweep without a move
+        }
+    }
+    for (; !A.sweep && it < A.max_iters; it++) {
         __syncwarp();
         uint64_t kmin = KEY_NONE;
         const int asp = (int)(best - cur);   // aspiration: cur + delta < best  <=>  delta < asp

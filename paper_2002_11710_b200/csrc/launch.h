@@ -25,6 +25,7 @@ struct SearchArgs {
     const uint64_t *seeds;                 // [R] or null -> seed
     uint64_t seed;
     int32_t kick, tenure, max_iters, strict_tabu_stop;
+    int32_t sweep;                         // f1: paper-literal (i, j) sweep (Alg. 2 / 3)
     uint32_t mask;
     int32_t T_smem, E_smem;
     int32_t *E_global;                     // [R][n][V] when !E_smem

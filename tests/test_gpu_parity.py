@@ -494,3 +494,33 @@ def test_bench_configuration_sampled_runs(A, ctx, oracle_mod):
         assert res[r]["best_obj"] == o["best_obj"] and res[r]["final_obj"] == o["final_obj"]
         assert res[r]["best_iter"] == o["best_iter"] and res[r]["kicks_applied"] == o["kicks_applied"]
         assert routes_of(bp[r], bm[r]) == routes_of(*o["best"])
+
+
+@pytest.mark.parametrize("cfg,steps", [("tiny", 200), ("ontario", 1500), ("batched", 1500), ("large", 600)])
+def test_sweep_mode_parity(A, ctx, oracle_mod, cfg, steps):
+    """f1 (paper-literal Alg. 2 / 3 sweep) on the batched kernel: single runs and a batch
+    with per-run permutation seeds, against the oracle step by step."""
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    for mode in (0, 1):
+        prm = A.params(mode=mode, tenure=c.tenure, max_iters=steps, trace_level=1, sweep=1)
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True)
+        o = O.sweep(p, m, mode=mode, tenure=c.tenure, max_steps=steps)
+        k = o["iters_done"]
+        assert g["iters_done"] == k and g["stop_reason"] == o["stop_reason"] and g["best_obj"] == o["best_obj"]
+        gi = g["trace"]["idx"].astype(np.int64)
+        gi[gi == 0xFFFFFFFF] = -1
+        assert (gi == o["trace"]["idx"]).all() and (g["trace"]["cur"] == o["trace"]["cur"]).all()
+        assert routes_of(*g["best"]) == routes_of(*o["best"])
+    R = 8
+    seeds = np.arange(11, 11 + R, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    prm = A.params(mode=1, tenure=c.tenure, max_iters=steps, sweep=1)
+    A.as_batch_run(ctx, h, R, p, m, prm, seeds, results=res)
+    for r in (0, R - 1):
+        o = O.sweep(p, m, mode=1, tenure=c.tenure, max_steps=steps, seed=int(seeds[r]))
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == o["iters_done"]
+        assert res[r]["best_iter"] == o["best_iter"]

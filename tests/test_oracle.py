@@ -354,3 +354,41 @@ def test_generated_instances_planted_feasible(oracle_mod):
         assert O.feasible(inst.planted_ptr, inst.planted_missions), name
         a = instgen.generate(name)
         assert (a.travel_s == inst.travel_s).all() and (a.deadline_s == inst.deadline_s).all()
+
+
+def test_e1_sweep_golden(oracle_mod):
+    """f1: the paper-literal (i, j) sweep of Alg. 2 / Alg. 3 on E1, derived by hand."""
+    I = e1_instance()
+    O = oracle_mod.Oracle(I)
+    ptr, ms = csr(GOLD["start"])
+    r = O.sweep(ptr, ms, mode=0, max_steps=50)
+    assert list(r["trace"]["idx"]) == GOLD["sweep_ns"]["idx"]
+    assert r["best_obj"] == GOLD["sweep_ns"]["objective"] and r["stop_reason"] == 1
+    r = O.sweep(ptr, ms, mode=1, tenure=2, max_steps=50)
+    assert list(r["trace"]["idx"]) == GOLD["sweep_ts_tenure2"]["idx"]
+    assert list(r["trace"]["delta"]) == GOLD["sweep_ts_tenure2"]["delta"]
+
+
+def test_sweep_invariants(oracle_mod):
+    """Sweep moves are inter-route relocates only; NS never worsens; results are feasible
+    and bounded below by the exact optimum; seeded permutations change the order."""
+    for seed in (0, 5):
+        inst = tiny_instance(5, 3, 300 + seed, F=10)
+        O = oracle_mod.Oracle(inst)
+        st, (p, m), _, _ = O.greedy()
+        opt, _ = pins.brute_optimum(inst)
+        n, V = inst.n_missions, inst.n_vehicles
+        for mode in (0, 1):
+            r = O.sweep(p, m, mode=mode, tenure=3, max_steps=60, seed=seed)
+            idx = r["trace"]["idx"]
+            applied = idx[idx >= 0]
+            assert (applied < n * (n + V)).all()
+            if mode == 0:
+                assert (r["trace"]["delta"][idx >= 0] < 0).all()
+            assert O.feasible(*r["best"]) and r["best_obj"] >= opt
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    st, (p, m), _, _ = O.greedy()
+    a = O.sweep(p, m, mode=1, max_steps=200, seed=0)
+    b = O.sweep(p, m, mode=1, max_steps=200, seed=7)
+    assert not (a["trace"]["idx"] == b["trace"]["idx"]).all()
