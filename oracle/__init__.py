@@ -39,7 +39,7 @@ class _Inst(C.Structure):
     _fields_ = [("NL", C.c_int32), ("NC", C.c_int32), ("T", C.c_void_p), ("class_is_heli", C.c_void_p),
                 ("V", C.c_int32), ("veh_loc", C.c_void_p), ("veh_cls", C.c_void_p), ("n", C.c_int32),
                 ("pick", C.c_void_p), ("dele", C.c_void_p), ("w", C.c_void_p), ("heli", C.c_void_p),
-                ("P", C.c_int32), ("DAY", C.c_int32)]
+                ("P", C.c_int32), ("DAY", C.c_int32), ("no_wait", C.c_int32)]
 
 
 class _Params(C.Structure):
@@ -99,7 +99,8 @@ class Oracle:
         self.V = int(k["vloc"].shape[0])
         self.c = _Inst(int(k["T"].shape[1]), int(k["T"].shape[0]), _p(k["T"]), _p(k["ch"]), self.V,
                        _p(k["vloc"]), _p(k["vcls"]), self.n, _p(k["pick"]), _p(k["dele"]), _p(k["w"]),
-                       _p(k["heli"]), int(inst.flight_limit_s), int(inst.day_length_s))
+                       _p(k["heli"]), int(inst.flight_limit_s), int(inst.day_length_s),
+                       int(getattr(inst, "no_wait", 0)))
         self.ref = C.byref(self.c)
 
     # ---- schedule conversion (CSR <-> per-vehicle lists) -------------------

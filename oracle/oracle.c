@@ -55,7 +55,10 @@ int64_t or_route_cost(const or_inst *I, int32_t v, const int32_t *route, int32_t
 }
 
 /* ------------------------------------------------------------------- O4 -- */
-/* Route feasibility:
+/* (f3, reading #40: with no_wait the vehicle departs a mission on arrival, so
+ * the clock carries the arrival time instead of the deadline; deadlines stay
+ * upper bounds on arrival.)
+ * Route feasibility:
  *  (i)  con7/con8 (text P:148; readings #2-#6): the clock starts
  *       at 0 at the base, the vehicle departs mission x at exactly w_x, and
  *       every arrival is <= the next deadline; the return arrives by DAY
@@ -71,7 +74,7 @@ int32_t or_route_feasible(const or_inst *I, int32_t v, const int32_t *route, int
         if (I->heli[m] && !I->class_is_heli[I->veh_cls[v]]) return 0;
         int64_t arrival = dep + D_to_mission(I, v, prev, m);
         if (arrival > I->w[m]) return 0;
-        dep = I->w[m];
+        dep = I->no_wait ? arrival : I->w[m];
         prev = m;
     }
     if (dep + D_to_base(I, v, prev) > I->DAY) return 0;

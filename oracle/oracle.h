@@ -37,6 +37,7 @@ typedef struct {
     const uint8_t *heli;           /* [n] rho = 1: helicopter required */
     int32_t P;                     /* flight limit p, seconds */
     int32_t DAY;                   /* return limit, seconds */
+    int32_t no_wait;               /* f3 variant: depart on arrival instead of at w (reading #40) */
 } or_inst;
 
 /* A schedule: len[v] missions in route v, stored in r[v*n + 0 .. len[v]-1]. */

@@ -679,7 +679,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;
-                grid_blocks = one_cta ? 1 : ctx->n_sm;
+                grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS", ctx->n_sm)));
                 (void)occ;
                 GA.Tglobal = D.Tpad;
                 void *p;

@@ -101,6 +101,7 @@ class Instance:
     planted_missions: np.ndarray | None = None
     seed: int = 0
     name: str = ""
+    no_wait: int = 0            # f3 model variant: depart on arrival (reading #40)
 
     @property
     def n_missions(self) -> int:

@@ -217,3 +217,26 @@ def ilp_optimum(inst, time_limit=60.0):
     if res.status != 0 or res.x is None:
         return None
     return int(round(res.fun))
+
+
+def route_eval_nowait(inst, k, order):
+    """Independent no-wait route check (f3): the clock carries the arrival time;
+    every arrival <= its deadline, return <= day, flight <= p, compatibility."""
+    n, V, NN, d, b, f = _node_model(inst)
+    l = int(inst.vehicle_class[k])
+    if len(order) and inst.heli_only[list(order)].any() and not inst.class_is_heli[l]:
+        return None
+    if not len(order):
+        return 0
+    seq = [n + k] + list(order) + [n + k]
+    clock, cost = 0, 0
+    for i, j in zip(seq[:-1], seq[1:]):
+        dij = int(d[i, j, l])
+        clock += dij
+        cost += dij
+        wj = int(inst.day_length_s) if j >= n else int(inst.deadline_s[j])
+        if clock > wj:
+            return None
+    if cost > inst.flight_limit_s:
+        return None
+    return cost

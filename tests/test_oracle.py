@@ -392,3 +392,63 @@ def test_sweep_invariants(oracle_mod):
     a = O.sweep(p, m, mode=1, max_steps=200, seed=0)
     b = O.sweep(p, m, mode=1, max_steps=200, seed=7)
     assert not (a["trace"]["idx"] == b["trace"]["idx"]).all()
+
+
+# ------------------------------------------------------------- f3: no-wait ---
+def _nowait_copy(inst, deadlines=None):
+    import dataclasses
+    out = dataclasses.replace(inst, no_wait=1)
+    if deadlines is not None:
+        out.deadline_s = np.array(deadlines, np.int32)
+    return out
+
+
+def test_e1_nowait_golden(oracle_mod):
+    """E1 with deadlines (3000, 2000, 3000), by hand: v0 = [m1, m0, m2] (idx 2 from the start
+    [m0, m1, m2]) arrives at m1 at 900, m0 at 900 + 900 = 1800, m2 at 1800 + 100 = 1900 and
+    back at 2000 -- feasible without waiting; with waiting m1 departs at 2000, m0 at 3000 and
+    m2 is reached at 3100 > 3000."""
+    wait = _nowait_copy(e1_instance(), [3000, 2000, 3000])
+    wait.no_wait = 0
+    nowait = _nowait_copy(e1_instance(), [3000, 2000, 3000])
+    ptr, ms = csr(GOLD["start"])
+    dw, fw, _ = oracle_mod.Oracle(wait).eval_moves(ptr, ms, mode=0)
+    dn, fn, _ = oracle_mod.Oracle(nowait).eval_moves(ptr, ms, mode=0)
+    assert dw[2] == dn[2] == 200
+    assert not fw[2] & 2 and fn[2] & 2
+    assert oracle_mod.Oracle(nowait).route_feasible(0, [1, 0, 2])
+    assert not oracle_mod.Oracle(wait).route_feasible(0, [1, 0, 2])
+
+
+def test_nowait_vs_independent_check(oracle_mod):
+    rng = np.random.default_rng(12)
+    n_feas = 0
+    for seed in range(4):
+        base = tiny_instance(5, 3, 700 + seed, F=10)
+        inst = _nowait_copy(base)
+        O = oracle_mod.Oracle(inst)
+        Ow = oracle_mod.Oracle(base)
+        states = trajectory_states(Ow, base)
+        n, V = inst.n_missions, inst.n_vehicles
+        for _ in range(30):
+            perm = rng.permutation(n).astype(np.int32)
+            cuts = np.sort(rng.integers(0, n + 1, V - 1))
+            states.append((np.concatenate([[0], cuts, [n]]).astype(np.int32), perm))
+        for ptr, ms in states:
+            routes = routes_of(ptr, ms)
+            ok = all(pins.route_eval_nowait(inst, k, r) is not None for k, r in enumerate(routes))
+            assert O.feasible(ptr, ms) == ok
+            if Ow.feasible(ptr, ms):          # waiting-feasible => no-wait-feasible
+                assert ok
+        for ptr, ms in trajectory_states(Ow, base):
+            d, f, _ = O.eval_moves(ptr, ms, mode=0)
+            base_obj = O.objective(ptr, ms)
+            for idx in range(O.move_space_size()):
+                okm, (p2, m2) = O.apply_move(ptr, ms, idx)
+                if not okm:
+                    continue
+                routes = routes_of(p2, m2)
+                feas = all(pins.route_eval_nowait(inst, k, r) is not None for k, r in enumerate(routes))
+                assert bool(f[idx] & 2) == feas and d[idx] == O.objective(p2, m2) - base_obj
+                n_feas += feas
+    assert n_feas > 50
