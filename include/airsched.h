@@ -74,7 +74,13 @@ typedef struct {
     const int32_t *deadline_s;      /* [n] w_n in [1, day_length_s] */
     const uint8_t *heli_only;       /* [n] rho: 1 = helicopter required */
     int32_t flight_limit_s;         /* p > 0 (36000 = 10 h) */
-    int32_t day_length_s;           /* >= flight_limit_s (86400) */
+    int32_t day_length_s;           /* in [flight_limit_s, 2^30) (86400) */
+    int32_t no_wait;                /* 0: the paper's model -- a vehicle departs mission n at
+                                     *    exactly w_n (readings #2-#6);
+                                     * 1: no-wait variant (reading #40) -- it
+                                     *    departs on arrival, deadlines bound arrivals.  The
+                                     *    variant runs on the per-CTA kernel only: the sweep mode
+                                     *    and the sharded path return AS_ERR_UNSUPPORTED. */
 } as_instance_desc;
 
 /* Validates and copies desc (AS_ERR_INVALID_ARG names the violated rule).

@@ -43,7 +43,7 @@ class as_instance_desc(C.Structure):
                 ("n_vehicles", C.c_int32), ("vehicle_base", C.c_void_p), ("vehicle_class", C.c_void_p),
                 ("n_missions", C.c_int32), ("pickup_loc", C.c_void_p), ("delivery_loc", C.c_void_p),
                 ("deadline_s", C.c_void_p), ("heli_only", C.c_void_p), ("flight_limit_s", C.c_int32),
-                ("day_length_s", C.c_int32)]
+                ("day_length_s", C.c_int32), ("no_wait", C.c_int32)]
 
 
 class as_run_params(C.Structure):
@@ -138,7 +138,7 @@ class Instance:
         d = as_instance_desc(k["T"].shape[1], k["T"].shape[0], _ptr(k["T"]), _ptr(k["ch"]), len(k["bl"]),
                              _ptr(k["bl"]), len(k["vb"]), _ptr(k["vb"]), _ptr(k["vc"]), len(k["pk"]), _ptr(k["pk"]),
                              _ptr(k["dl"]), _ptr(k["w"]), _ptr(k["h"]), int(src.flight_limit_s),
-                             int(src.day_length_s))
+                             int(src.day_length_s), int(getattr(src, "no_wait", 0)))
         h = C.c_void_p()
         _check(lib.as_instance_create(C.byref(d), C.byref(h)))
         self.handle = h

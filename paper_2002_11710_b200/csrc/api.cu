@@ -47,6 +47,7 @@ static as_status fail(as_status st, const char *fmt, ...) {
 struct as_instance {
     uint64_t uid;
     int32_t NL, NC, V, n, n_bases, P, DAY;
+    int32_t no_wait = 0;   // f3 variant (reading #40)
     std::vector<int32_t> T, base_loc, vbase, vcls, vloc, pick, del, w;
     std::vector<uint8_t> cls_heli, heli, vcls8;
     int32_t maxT = 0;
@@ -66,12 +67,13 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
         return fail(AS_ERR_INVALID_ARG, "null array");
     if (n > 0 && (!d->pickup_loc || !d->delivery_loc || !d->deadline_s || !d->heli_only))
         return fail(AS_ERR_INVALID_ARG, "null mission array");
-    if (d->flight_limit_s <= 0 || d->flight_limit_s >= (1 << 30) || d->day_length_s < d->flight_limit_s)
-        return fail(AS_ERR_INVALID_ARG, "need flight_limit_s > 0 and day_length_s >= flight_limit_s (SPEC S:117)");
+    if (d->flight_limit_s <= 0 || d->day_length_s >= (1 << 30) || d->day_length_s < d->flight_limit_s)
+        return fail(AS_ERR_INVALID_ARG, "need 0 < flight_limit_s <= day_length_s < 2^30 (SPEC S:117)");
+    if (d->no_wait != 0 && d->no_wait != 1) return fail(AS_ERR_INVALID_ARG, "no_wait must be 0 or 1");
     std::unique_ptr<as_instance> I(new (std::nothrow) as_instance());
     if (!I) return fail(AS_ERR_OOM, "host allocation");
     I->NL = (int32_t)NL; I->NC = (int32_t)NC; I->V = (int32_t)V; I->n = (int32_t)n; I->n_bases = (int32_t)B;
-    I->P = d->flight_limit_s; I->DAY = d->day_length_s;
+    I->P = d->flight_limit_s; I->DAY = d->day_length_s; I->no_wait = d->no_wait;
     I->T.assign(d->travel_s, d->travel_s + NC * NL * NL);
     for (int64_t c = 0; c < NC; c++)
         for (int64_t a = 0; a < NL; a++)
@@ -175,7 +177,7 @@ static void route_eval(const as_instance *I, int v, const std::vector<int32_t> &
         if (dep + d > I->w[m]) ok = false;
         if (I->heli[m] && !I->cls_heli[I->vcls[v]]) ok = false;
         c += d;
-        dep = I->w[m];
+        dep = I->no_wait ? dep + d : I->w[m];   // depart at w_m, or on arrival (f3)
         prev = m;
     }
     int64_t d = h_db(I, v, prev);
@@ -364,6 +366,7 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
     D.d.svc = (const int32_t *)svc;
     D.d.n = I->n; D.d.V = I->V; D.d.NL = I->NL; D.d.NC = I->NC; D.d.P = I->P; D.d.DAY = I->DAY;
     D.d.maxT = I->maxT;
+    D.d.no_wait = I->no_wait;
     D.d.svcpos = 1;
     for (int c = 0; c < I->NC; c++)
         for (int m = 0; m < I->n; m++)
@@ -455,7 +458,7 @@ struct GState {
 static as_status alloc_gstate(as_ctx *ctx, const as_instance *I, bool with_E, RunViewG &G) {
     const size_t S = (size_t)I->n + I->V;
     void *p;
-    size_t words = 10 * S + (size_t)I->V + (with_E ? (size_t)I->n * I->V : 0) + 16;
+    size_t words = 13 * S + (size_t)I->V + (with_E ? (size_t)I->n * I->V : 0) + 16;
     as_status st = scratch(ctx, "gstate", words * 4, &p);
     if (st != AS_OK) return st;
     int32_t *b = (int32_t *)p;
@@ -469,6 +472,9 @@ static as_status alloc_gstate(as_ctx *ctx, const as_instance *I, bool with_E, Ru
     G.pick_s = b; b += S;
     G.w_s = b; b += S;
     G.F = b; b += I->V;
+    G.arr = b; b += S;
+    G.sl = b; b += S;
+    G.pos = b; b += S;
     G.E = with_E ? b : nullptr;
     return AS_OK;
 }
@@ -549,7 +555,7 @@ static as_status pick_layout(as_ctx *ctx, const as_instance *I, bool tabu, int *
     struct Opt { bool t, e; } opts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
     for (auto o : opts) {
         bool e = o.e && tabu;
-        size_t b = search_smem_bytes(n, V, NL, NC, o.t, e);
+        size_t b = search_smem_bytes(n, V, NL, NC, o.t, e, I->no_wait != 0);
         if (b <= lim) {
             *T_smem = o.t;
             *E_smem = e;
@@ -586,7 +592,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int force_T = env_int("AIRSCHED_T_SMEM", -1);
     if (force_T == 0 && T_smem) {
         T_smem = 0;
-        smem = search_smem_bytes(n, V, I->NL, I->NC, false, E_smem);
+        smem = search_smem_bytes(n, V, I->NL, I->NC, false, E_smem, I->no_wait != 0);
     }
     SearchArgs A;
     memset(&A, 0, sizeof(A));
@@ -643,7 +649,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     size_t sh_b = 0, run_b = 0;
     batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
-    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest;
+    // the compact-layout kernels (k_batch, k_grid) score the waiting model only;
+    // the no-wait variant (f3) runs on k_search
+    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !I->no_wait;
+    if (P->sweep && I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sweep mode (f1) is not built for the no-wait variant");
     const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
     bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single) || P->sweep);
     if (P->sweep && !use_batch)
@@ -675,12 +684,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 }
             }
             if (use_grid) {
-                int occ = 0;
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;
                 grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS", ctx->n_sm)));
-                (void)occ;
                 GA.Tglobal = D.Tpad;
                 void *p;
                 if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
@@ -752,6 +759,7 @@ extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *
     as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
     if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
     if ((comm || env_int("AIRSCHED_SHARDED", 0) == 1) && !P->sweep) {
+        if (I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sharded path is not built for the no-wait variant");
         if (digest && P->trace_level >= 2) return fail(AS_ERR_UNSUPPORTED, "tabu digests are not produced by the sharded path");
         return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
     }
@@ -830,9 +838,6 @@ extern "C" as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_
     if (best_obj_out) *best_obj_out = k == AS_KEY_NONE ? -1 : (int64_t)(k >> 32);
     if (!ptr_out || run < 0) return AS_OK;
     // owner copies its run's CSR into a buffer, NCCL broadcast to every rank
-    const as_instance *I = nullptr;
-    for (auto &kv : ctx->insts) I = kv.first;   // the instance of the last batch
-    (void)I;
     const int rank = comm ? comm->rank : 0;
     const int owner = (int)(run / n_runs);
     const int r = (int)(run % n_runs);
@@ -884,6 +889,17 @@ extern "C" as_status as_init_greedy(as_ctx *ctx, const as_instance *I, int32_t i
             if (insert_mode == 1) {
                 at = 0;
                 while (at < (int)r.size() && I->w[r[at]] <= I->w[m]) at++;
+            }
+            if (I->no_wait) {   // arrivals depend on the prefix: check the whole new route (f3)
+                std::vector<int32_t> r2(r);
+                r2.insert(r2.begin() + at, m);
+                int64_t c2;
+                bool f2;
+                route_eval(I, v, r2, &c2, &f2);
+                if (!f2) continue;
+                int64_t inc = c2 - F[v];
+                if (*bv < 0 || inc < *binc) { *bv = v; *bat = at; *binc = inc; }
+                continue;
             }
             int prev = at > 0 ? r[at - 1] : -1;
             int next = at < (int)r.size() ? r[at] : -1;

@@ -39,6 +39,7 @@ struct DevInst {
     const uint8_t *heli;     // [n]
     const int32_t *svc;      // [NC][n] = T_c[pick][del] (pickup->delivery leg)
     int32_t n, V, NL, NC, P, DAY;
+    int32_t no_wait;         // f3 variant: depart on arrival (reading #40)
     int32_t maxT;            // max travel time (selects the uint16 table)
     int32_t svcpos;          // every pickup->delivery leg > 0 in every class (enables the FAST scorers)
 };
@@ -96,6 +97,11 @@ struct RunViewT {
     const int32_t *w_s;             // [S] deadline (day length for END)
     int32_t *F;                     // [V] route flight time (con6)
     ET *E;                          // [n][V] tabu expiry (nullable)
+    // no-wait variant only (f3; null otherwise).  depc then holds the
+    // predecessor's ARRIVAL (its departure when it does not wait).
+    int32_t *arr;                   // [S] arrival at the slot (END: return to base)
+    int32_t *sl;                    // [S] min over the route suffix from the slot of (w - arr)
+    int32_t *pos;                   // [S] position in the route (missions 1..L, END L+1)
 };
 
 using MissionView = MissionViewT<int32_t, int32_t>;
@@ -127,6 +133,7 @@ __device__ __forceinline__ void refresh_slot(const MV &M, const RV &R, int x) {
 struct RelocRow {
     int a, s, ca;             // route of m, successor slot, class of a
     int rem;                  // d(p,s) - d(p,m) - d(m,s)
+    int Dps;                  // d(p,s)
     bool rem_ok;              // dep(p) + d(p,s) <= w(s)
     int pick_m, del_m, w_m, heli_m;
     int Fa;
@@ -141,6 +148,7 @@ __device__ __forceinline__ RelocRow reloc_row(const MV &M, const RV &R, int m) {
     r.ca = M.cls(r.a);
     int Dps = Tget(M, r.ca, R.endc[m], R.pick_s[r.s]) + R.svco[r.s];
     r.rem = Dps - R.inc[m] - R.inc[r.s];
+    r.Dps = Dps;
     r.rem_ok = R.depc[m] + Dps <= R.w_s[r.s];
     r.pick_m = R.pick_s[m];
     r.del_m = M.dl(m);
@@ -163,8 +171,82 @@ __device__ __forceinline__ MoveEval move_none() {
     return e;
 }
 
-// Insert part for target slot t (t != m, t != succ(m), both assigned).
+// ---- no-wait variant (f3, reading #40) ---------------------------
+// Without waiting a route's clock carries arrivals, so a move shifts every
+// later arrival of the route by the same amount: the route stays feasible iff
+// each shifted stretch keeps its slack.  min(w - arr) over the stretch x..y
+// (inclusive, along succ):
+template <class RV>
+__device__ __forceinline__ int nw_range_slack(const RV &R, int x, int y) {
+    int s = 0x7FFFFFFF;
+    for (;;) {
+        int v = R.w_s[x] - R.arr[x];
+        s = v < s ? v : s;
+        if (x == y) break;
+        x = R.succ[x];
+    }
+    return s;
+}
+
+// Recompute the whole route of vehicle v (incoming-link records, arrivals,
+// positions, suffix slacks) from its linked list.  Single thread, O(L).
 template <class MV, class RV>
+__device__ inline void nw_refresh_route(const MV &M, const RV &R, int v) {
+    const int n = M.n, term = n + v, c = M.cls(v);
+    int e = M.vl(v), dep = 0, k = 0;
+    int x = R.succ[term];
+    for (;;) {
+        int sv = x < n ? M.sv(c, x) : 0;
+        int inc = Tget(M, c, e, R.pick_s[x]) + sv;
+        R.endc[x] = e;
+        R.depc[x] = dep;
+        R.svco[x] = sv;
+        R.inc[x] = inc;
+        R.arr[x] = dep + inc;
+        R.pos[x] = ++k;
+        if (x >= n) break;
+        e = M.dl(x);
+        dep += inc;
+        x = R.succ[x];
+    }
+    int s = 0x7FFFFFFF;
+    x = term;
+    do {
+        int v2 = R.w_s[x] - R.arr[x];
+        s = v2 < s ? v2 : s;
+        R.sl[x] = s;
+        x = R.pred[x];
+    } while (x != term);
+}
+
+// Time feasibility of relocating m (route a: p -> m -> s) before t (route b,
+// c = pred t); x1 = d(c, m), x2 = d(m, t) in b's class.
+template <class MV, class RV>
+__device__ __forceinline__ bool nw_reloc_time(const MV &M, const RV &R, const RelocRow &r, int m, int t, int b,
+                                              int x1, int x2) {
+    const int s = r.s;
+    if (b != r.a) {
+        if (R.depc[m] + r.Dps - R.arr[s] > R.sl[s]) return false;        // a: s.. shifted
+        int Am = R.depc[t] + x1;                                           // b: c -> m -> t..
+        return Am <= r.w_m && Am + x2 - R.arr[t] <= R.sl[t];
+    }
+    if (R.pos[t] > R.pos[m]) {               // p s .. c m t ..
+        int c = R.pred[t];
+        int d1 = R.depc[m] + r.Dps - R.arr[s];
+        if (d1 > nw_range_slack(R, s, c)) return false;
+        int Am = R.arr[c] + d1 + x1;
+        return Am <= r.w_m && Am + x2 - R.arr[t] <= R.sl[t];
+    }
+    const int p = R.pred[m];                 // c m t .. p s ..
+    int Am = R.depc[t] + x1;
+    if (Am > r.w_m) return false;
+    int d1 = Am + x2 - R.arr[t];
+    if (d1 > nw_range_slack(R, t, p)) return false;
+    return R.arr[p] + d1 + r.Dps - R.arr[s] <= R.sl[s];
+}
+
+// Insert part for target slot t (t != m, t != succ(m), both assigned).
+template <bool NW = false, class MV, class RV>
 __device__ __forceinline__ MoveEval reloc_eval(const MV &M, const RV &R, const RelocRow &r, int m, int t,
                                                 uint32_t mask, int it) {
     MoveEval e = move_none();
@@ -178,7 +260,9 @@ __device__ __forceinline__ MoveEval reloc_eval(const MV &M, const RV &R, const R
     int x2 = Tget(M, cb, r.del_m, R.pick_s[t]) + R.svco[t];             // d(m, t)
     int ins = x1 + x2 - R.inc[t];
     e.delta = r.rem + ins;
-    bool ok = r.rem_ok && (!r.heli_m || M.hok(cb)) && (R.depc[t] + x1 <= r.w_m) && (r.w_m + x2 <= R.w_s[t]);
+    bool ok = !r.heli_m || M.hok(cb);
+    if constexpr (NW) ok = ok && nw_reloc_time(M, R, r, m, t, b, x1, x2);
+    else ok = ok && r.rem_ok && (R.depc[t] + x1 <= r.w_m) && (r.w_m + x2 <= R.w_s[t]);
     if (b == r.a) {
         ok = ok && (r.Fa + e.delta <= M.P);
         e.da = e.delta;
@@ -193,7 +277,7 @@ __device__ __forceinline__ MoveEval reloc_eval(const MV &M, const RV &R, const R
 }
 
 // ---- swap (O5 swap block): exchange the positions of m1 < m2 --------------
-template <class MV, class RV>
+template <bool NW = false, class MV, class RV>
 __device__ __forceinline__ MoveEval swap_eval(const MV &M, const RV &R, int m1, int m2, uint32_t mask, int it) {
     MoveEval e = move_none();
     int a = R.veh[m1], b = R.veh[m2];
@@ -220,7 +304,12 @@ __device__ __forceinline__ MoveEval swap_eval(const MV &M, const RV &R, int m1, 
         int y3 = Tget(M, ca, delf, R.pick_s[sg]) + R.svco[sg];           // f -> s
         e.delta = y1 + y2 + y3 - R.inc[f] - R.inc[g] - R.inc[sg];
         e.da = e.delta;
-        e.feasible = (R.depc[f] + y1 <= wg) && (wg + y2 <= wf) && (wf + y3 <= R.w_s[sg]) && (Fa + e.delta <= M.P);
+        if constexpr (NW) {
+            int Ag = R.depc[f] + y1, Af = Ag + y2;   // no waiting: arrivals chain
+            e.feasible = (Ag <= wg) && (Af <= wf) && (Af + y3 - R.arr[sg] <= R.sl[sg]) && (Fa + e.delta <= M.P);
+        } else {
+            e.feasible = (R.depc[f] + y1 <= wg) && (wg + y2 <= wf) && (wf + y3 <= R.w_s[sg]) && (Fa + e.delta <= M.P);
+        }
     } else {
         int cb = M.cls(b);
         int ya1 = Tget(M, ca, R.endc[m1], pick2) + M.sv(ca, m2);   // p1 -> m2
@@ -230,9 +319,30 @@ __device__ __forceinline__ MoveEval swap_eval(const MV &M, const RV &R, int m1, 
         e.da = ya1 + ya2 - R.inc[m1] - R.inc[s1];
         e.db = yb1 + yb2 - R.inc[m2] - R.inc[s2];
         e.delta = e.da + e.db;
-        bool ok = (!M.hl(m2) || M.hok(ca)) && (!M.hl(m1) || M.hok(cb)) &&
-                  (R.depc[m1] + ya1 <= w2) && (w2 + ya2 <= R.w_s[s1]) && (R.depc[m2] + yb1 <= w1) &&
-                  (w1 + yb2 <= R.w_s[s2]);
+        bool ok = (!M.hl(m2) || M.hok(ca)) && (!M.hl(m1) || M.hok(cb));
+        if constexpr (NW) {
+            if (a != b) {
+                int A2 = R.depc[m1] + ya1, A1 = R.depc[m2] + yb1;
+                ok = ok && (A2 <= w2) && (A2 + ya2 - R.arr[s1] <= R.sl[s1]) && (A1 <= w1) &&
+                     (A1 + yb2 - R.arr[s2] <= R.sl[s2]);
+            } else {
+                // one route, not adjacent: pf f sf .. pg g sg -> pf g sf .. pg f sg
+                const bool first1 = R.pos[m1] < R.pos[m2];
+                const int f = first1 ? m1 : m2, g = first1 ? m2 : m1;
+                const int sf = first1 ? s1 : s2, sg = first1 ? s2 : s1, pg = R.pred[g];
+                const int d_pf_g = first1 ? ya1 : yb1, d_g_sf = first1 ? ya2 : yb2;
+                const int d_pg_f = first1 ? yb1 : ya1, d_f_sg = first1 ? yb2 : ya2;
+                const int wf = first1 ? w1 : w2, wg = first1 ? w2 : w1;
+                int Ag = R.depc[f] + d_pf_g;
+                int d1 = Ag + d_g_sf - R.arr[sf];
+                ok = ok && (Ag <= wg) && (d1 <= nw_range_slack(R, sf, pg));
+                int Af = R.arr[pg] + d1 + d_pg_f;
+                ok = ok && (Af <= wf) && (Af + d_f_sg - R.arr[sg] <= R.sl[sg]);
+            }
+        } else {
+            ok = ok && (R.depc[m1] + ya1 <= w2) && (w2 + ya2 <= R.w_s[s1]) && (R.depc[m2] + yb1 <= w1) &&
+                 (w1 + yb2 <= R.w_s[s2]);
+        }
         if (a == b) ok = ok && (Fa + e.delta <= M.P);
         else ok = ok && (Fa + e.da <= M.P) && (R.F[b] + e.db <= M.P);
         e.feasible = ok;
@@ -250,7 +360,7 @@ __device__ __forceinline__ int move_class(const MoveEval &e, long long cur, long
 }
 
 // Evaluate canonical index idx (decode + score); used by the dump kernel and apply.
-template <class MV, class RV>
+template <bool NW = false, class MV, class RV>
 __device__ __forceinline__ MoveEval eval_index(const MV &M, const RV &R, uint32_t idx, uint32_t mask, int it) {
     const int n = M.n, S = M.n + M.V;
     uint32_t Rb = (uint32_t)n * (uint32_t)S;
@@ -258,18 +368,18 @@ __device__ __forceinline__ MoveEval eval_index(const MV &M, const RV &R, uint32_
         int m = idx / S, t = idx % S;
         RelocRow r = reloc_row(M, R, m);
         if (r.a < 0) return move_none();
-        return reloc_eval(M, R, r, m, t, mask, it);
+        return reloc_eval<NW>(M, R, r, m, t, mask, it);
     }
     uint32_t k = idx - Rb;
     int m1 = k / n, m2 = k % n;
     if (m1 >= m2) return move_none();
-    return swap_eval(M, R, m1, m2, mask, it);
+    return swap_eval<NW>(M, R, m1, m2, mask, it);
 }
 
 // Apply a VALID move whose per-route deltas are in e (single thread).
 // Relinks the lists, refreshes the incoming-link records of the touched slots,
 // updates route flight totals and the tabu expiry of the 'from' pairs (O8).
-template <class MV, class RV>
+template <bool NW = false, class MV, class RV>
 __device__ inline void apply_move(const MV &M, const RV &R, uint32_t idx, const MoveEval &e, int it, int tenure,
                                   bool write_tabu) {
     const int n = M.n, S = M.n + M.V;
@@ -287,9 +397,14 @@ __device__ inline void apply_move(const MV &M, const RV &R, uint32_t idx, const 
         R.succ[m] = t;
         R.pred[t] = m;
         R.veh[m] = b;
-        refresh_slot(M, R, s);
-        refresh_slot(M, R, m);
-        refresh_slot(M, R, t);
+        if constexpr (NW) {
+            nw_refresh_route(M, R, a);
+            if (b != a) nw_refresh_route(M, R, b);
+        } else {
+            refresh_slot(M, R, s);
+            refresh_slot(M, R, m);
+            refresh_slot(M, R, t);
+        }
         if (a == b) R.F[a] += e.delta;
         else { R.F[a] += e.da; R.F[b] += e.db; }
         if (write_tabu && R.E) R.E[m * M.V + a] = it + tenure;
@@ -300,18 +415,25 @@ __device__ inline void apply_move(const MV &M, const RV &R, uint32_t idx, const 
         int p1 = R.pred[m1], s1 = R.succ[m1], p2 = R.pred[m2], s2 = R.succ[m2];
         if (s1 == m2) {          // p1 m1 m2 s2 -> p1 m2 m1 s2
             R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = m1; R.pred[m1] = m2; R.succ[m1] = s2; R.pred[s2] = m1;
-            refresh_slot(M, R, m2); refresh_slot(M, R, m1); refresh_slot(M, R, s2);
+            if constexpr (NW) nw_refresh_route(M, R, a);
+            else { refresh_slot(M, R, m2); refresh_slot(M, R, m1); refresh_slot(M, R, s2); }
             R.F[a] += e.delta;
         } else if (s2 == m1) {   // p2 m2 m1 s1 -> p2 m1 m2 s1
             R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = m2; R.pred[m2] = m1; R.succ[m2] = s1; R.pred[s1] = m2;
-            refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1);
+            if constexpr (NW) nw_refresh_route(M, R, a);
+            else { refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1); }
             R.F[a] += e.delta;
         } else {
             R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = s1; R.pred[s1] = m2;
             R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = s2; R.pred[s2] = m1;
             R.veh[m1] = b;
             R.veh[m2] = a;
-            refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1); refresh_slot(M, R, s2);
+            if constexpr (NW) {
+                nw_refresh_route(M, R, a);
+                if (b != a) nw_refresh_route(M, R, b);
+            } else {
+                refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1); refresh_slot(M, R, s2);
+            }
             if (a == b) R.F[a] += e.delta;
             else { R.F[a] += e.da; R.F[b] += e.db; }
         }

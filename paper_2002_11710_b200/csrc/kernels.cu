@@ -39,22 +39,20 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 // ----------------------------------------------------------------------------
 // State construction from CSR (shared by the dump path; the persistent kernel
 // does the same in its prologue).  One CTA.
-__global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, int32_t *succ, int32_t *pred,
-                              int32_t *veh, int32_t *endc, int32_t *depc, int32_t *inc, int32_t *svco,
-                              int32_t *pick_s, int32_t *w_s, int32_t *F) {
+__global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, RunViewG G) {
     const int n = I.n, V = I.V, S = n + V;
     for (int x = threadIdx.x; x < S; x += blockDim.x) {
         if (x < n) {
-            veh[x] = -1;
-            succ[x] = x;
-            pred[x] = x;
-            pick_s[x] = I.pick[x];
-            w_s[x] = I.w[x];
+            G.veh[x] = -1;
+            G.succ[x] = x;
+            G.pred[x] = x;
+            G.pick_s[x] = I.pick[x];
+            G.w_s[x] = I.w[x];
         } else {
             int v = x - n;
-            veh[x] = v;
-            pick_s[x] = I.vloc[v];
-            w_s[x] = I.DAY;
+            G.veh[x] = v;
+            G.pick_s[x] = I.vloc[v];
+            G.w_s[x] = I.DAY;
         }
     }
     __syncthreads();
@@ -62,45 +60,53 @@ __global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, 
         int prev = n + v;
         for (int i = ptr[v]; i < ptr[v + 1]; i++) {
             int m = ms[i];
-            veh[m] = v;
-            succ[prev] = m;
-            pred[m] = prev;
+            G.veh[m] = v;
+            G.succ[prev] = m;
+            G.pred[m] = prev;
             prev = m;
         }
-        succ[prev] = n + v;
-        pred[n + v] = prev;
+        G.succ[prev] = n + v;
+        G.pred[n + v] = prev;
     }
     __syncthreads();
     MissionView M = global_view(I);
     RunView R;
-    R.succ = succ; R.pred = pred; R.veh = veh; R.endc = endc; R.depc = depc; R.inc = inc; R.svco = svco;
-    R.pick_s = pick_s; R.w_s = w_s; R.F = F; R.E = nullptr;
+    R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
+    R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = nullptr;
+    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos;
     for (int x = threadIdx.x; x < S; x += blockDim.x) {
-        if (x < n && veh[x] < 0) { endc[x] = depc[x] = inc[x] = svco[x] = 0; continue; }
-        refresh_slot(M, R, x);
+        if (x < n && G.veh[x] < 0) {
+            G.endc[x] = G.depc[x] = G.inc[x] = G.svco[x] = 0;
+            if (I.no_wait) G.arr[x] = G.sl[x] = G.pos[x] = 0;
+            continue;
+        }
+        if (!I.no_wait) refresh_slot(M, R, x);
     }
+    if (I.no_wait)
+        for (int v = threadIdx.x; v < V; v += blockDim.x) nw_refresh_route(M, R, v);
     __syncthreads();
     for (int v = threadIdx.x; v < V; v += blockDim.x) {
         int f = 0;
-        int x = succ[n + v];
-        while (x < n) { f += inc[x]; x = succ[x]; }
-        f += inc[n + v];
-        F[v] = f;
+        int x = G.succ[n + v];
+        while (x < n) { f += G.inc[x]; x = G.succ[x]; }
+        f += G.inc[n + v];
+        G.F[v] = f;
     }
 }
 
 // One thread per canonical index.  delta/flags nullable; best key via atomicMin.
-template <bool TABU>
+template <bool TABU, bool NW>
 __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long long best, uint32_t mask,
                             int32_t *delta_out, uint8_t *flags_out, unsigned long long *best_key, uint64_t N) {
     MissionView M = global_view(I);
     RunView R;
     R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
     R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = TABU ? G.E : nullptr;
+    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos;
     uint64_t kmin = KEY_NONE;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < N;
          idx += (uint64_t)gridDim.x * blockDim.x) {
-        MoveEval e = eval_index(M, R, (uint32_t)idx, mask, it);
+        MoveEval e = eval_index<NW>(M, R, (uint32_t)idx, mask, it);
         uint8_t fl = 0;
         int cls = move_class<TABU>(e, cur, best);
         if (e.valid) {
@@ -126,13 +132,13 @@ __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long l
 struct SmemLayout {
     // byte offsets, 16-byte aligned
     int T, del, heli, svc, vcls, vloc, clsheli;
-    int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc;
+    int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc, arr, sl, pos;
     int red, ctrl, total;
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
+__host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, bool T_smem, bool E_smem, bool nw) {
     SmemLayout L;
     int o = 0;
     const int S = n + V;
@@ -155,6 +161,9 @@ __host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, 
     L.w_s = o; o = align16(o + S * 4);
     L.F = o; o = align16(o + V * 4);
     L.bsucc = o; o = align16(o + S * 4);
+    L.arr = o; o = align16(o + (nw ? S * 4 : 0));
+    L.sl = o; o = align16(o + (nw ? S * 4 : 0));
+    L.pos = o; o = align16(o + (nw ? S * 4 : 0));
     L.E = E_smem ? o : -1;
     o = align16(o + (E_smem ? n * V * 4 : 0));
     L.red = o; o = align16(o + 32 * 8);
@@ -163,18 +172,18 @@ __host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, 
     return L;
 }
 
-size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem) {
-    return (size_t)make_layout(n, V, NL, NC, T_smem, E_smem).total;
+size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem, bool nw) {
+    return (size_t)make_layout(n, V, NL, NC, T_smem, E_smem, nw).total;
 }
 
-template <bool TABU>
+template <bool TABU, bool NW>
 __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC;
     const int run = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const SmemLayout L = make_layout(n, V, I.NL, NC, A.T_smem, A.E_smem);
+    const SmemLayout L = make_layout(n, V, I.NL, NC, A.T_smem, A.E_smem, NW);
 
     // ---- stage instance constants -----------------------------------------
 #define SM32(off) reinterpret_cast<int32_t *>(smem_raw + (off))
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     R.succ = SM32(L.succ); R.pred = SM32(L.pred); R.veh = SM32(L.veh); R.endc = SM32(L.endc); R.depc = SM32(L.depc);
     R.inc = SM32(L.inc); R.svco = SM32(L.svco); R.pick_s = SM32(L.pick_s); R.w_s = SM32(L.w_s); R.F = SM32(L.F);
     R.E = TABU ? Eg : nullptr;
+    R.arr = SM32(L.arr); R.sl = SM32(L.sl); R.pos = SM32(L.pos);
     int32_t *bsucc = SM32(L.bsucc);
     unsigned long long *red = reinterpret_cast<unsigned long long *>(smem_raw + L.red);
     int32_t *ctrl = SM32(L.ctrl);   // 0: stop, 1: copy-best, 2: infeasible flag
@@ -251,13 +261,27 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     __syncthreads();
     for (int x = tid; x < S; x += blockDim.x) {
         if (x < n && R.veh[x] < 0) { atomicOr(&ctrl[2], 1); continue; }
-        if (ctrl[2]) continue;
+        if (ctrl[2] || NW) continue;
         refresh_slot(M, R, x);
         // con7/con8 of the incoming link, con9 compatibility
         if (R.depc[x] + R.inc[x] > R.w_s[x]) atomicOr(&ctrl[2], 1);
         if (x < n && M.hl(x) && !M.hok(M.cls(R.veh[x]))) atomicOr(&ctrl[2], 1);
     }
     __syncthreads();
+    if (NW && !ctrl[2]) {
+        // no-wait: arrivals depend on the whole prefix -> one thread per route
+        for (int v = tid; v < V; v += blockDim.x) {
+            nw_refresh_route(M, R, v);
+            int x = R.succ[n + v];
+            for (;;) {
+                if (R.arr[x] > R.w_s[x]) atomicOr(&ctrl[2], 1);
+                if (x < n && M.hl(x) && !M.hok(M.cls(v))) atomicOr(&ctrl[2], 1);
+                if (x >= n) break;
+                x = R.succ[x];
+            }
+        }
+        __syncthreads();
+    }
     if (!ctrl[2])
         for (int v = tid; v < V; v += blockDim.x) {
             int f = 0;
@@ -296,9 +320,9 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
             for (int k = 0; k < A.kick; k++) {
                 for (int tr = 0; tr < 64; tr++) {
                     uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
-                    MoveEval e = eval_index(M, R, idx, 0xFu, 0);
+                    MoveEval e = eval_index<NW>(M, R, idx, 0xFu, 0);
                     if (e.valid && e.feasible) {
-                        apply_move(M, R, idx, e, 0, 0, false);
+                        apply_move<NW>(M, R, idx, e, 0, 0, false);
                         kicks++;
                         break;
                     }
@@ -332,7 +356,7 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
             if (r.a < 0) continue;
             const uint32_t base = (uint32_t)m * (uint32_t)S;
             for (int t = lane; t < S; t += 32) {
-                MoveEval e = reloc_eval(M, R, r, m, t, mask, it);
+                MoveEval e = reloc_eval<NW>(M, R, r, m, t, mask, it);
                 int cls = move_class<TABU>(e, cur, best);
                 if (cls >= 0) {
                     uint64_t k = make_key(cls, e.delta, base + t);
@@ -350,7 +374,7 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
                 int m1, m2;
                 if (j < lenA) { m1 = q; m2 = q + 1 + j; }
                 else { m1 = qb; m2 = j; }
-                MoveEval e = swap_eval(M, R, m1, m2, mask, it);
+                MoveEval e = swap_eval<NW>(M, R, m1, m2, mask, it);
                 int cls = move_class<TABU>(e, cur, best);
                 if (cls >= 0) {
                     uint64_t k = make_key(cls, e.delta, Rb + (uint32_t)m1 * n + m2);
@@ -372,8 +396,8 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
                 ctrl[0] = stop;
             } else {
                 uint32_t idx = key_idx(k);
-                MoveEval e = eval_index(M, R, idx, mask, it);
-                apply_move(M, R, idx, e, it, A.tenure, TABU);
+                MoveEval e = eval_index<NW>(M, R, idx, mask, it);
+                apply_move<NW>(M, R, idx, e, it, A.tenure, TABU);
                 long long c = s_cur + e.delta;
                 s_cur = c;
                 if (c < s_best) {
@@ -434,9 +458,18 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
 // Host-side launchers (declared in launch.h).
 cudaError_t launch_build_state(const DevInst &I, const int32_t *ptr, const int32_t *ms, RunViewG &G,
                                cudaStream_t st) {
-    k_build_state<<<1, 256, 0, st>>>(I, ptr, ms, G.succ, G.pred, G.veh, G.endc, G.depc, G.inc, G.svco, G.pick_s,
-                                     G.w_s, G.F);
+    k_build_state<<<1, 256, 0, st>>>(I, ptr, ms, G);
     return cudaGetLastError();
+}
+
+template <bool TABU>
+static void eval_dump_nw(const DevInst &I, const RunViewG &G, int blocks, int threads, int it, long long cur,
+                         long long best, uint32_t mask, int32_t *delta, uint8_t *flags, unsigned long long *best_key,
+                         uint64_t N, cudaStream_t st) {
+    if (I.no_wait)
+        k_eval_dump<TABU, true><<<blocks, threads, 0, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
+    else
+        k_eval_dump<TABU, false><<<blocks, threads, 0, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
 }
 
 cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int it, long long cur, long long best,
@@ -446,26 +479,26 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
     uint64_t blocks64 = (N + threads - 1) / threads;
     int blocks = (int)(blocks64 < (uint64_t)n_sm * 8 ? blocks64 : (uint64_t)n_sm * 8);
     if (blocks < 1) blocks = 1;
-    size_t smem = 0;
-    if (mode == 1)
-        k_eval_dump<true><<<blocks, threads, smem, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
-    else
-        k_eval_dump<false><<<blocks, threads, smem, st>>>(I, G, it, cur, best, mask, delta, flags, best_key, N);
+    if (mode == 1) eval_dump_nw<true>(I, G, blocks, threads, it, cur, best, mask, delta, flags, best_key, N, st);
+    else eval_dump_nw<false>(I, G, blocks, threads, it, cur, best, mask, delta, flags, best_key, N, st);
+    return cudaGetLastError();
+}
+
+template <bool TABU, bool NW>
+static cudaError_t launch_search_t(const SearchArgs &A, int n_runs, int threads, size_t smem, cudaStream_t st) {
+    cudaError_t err = cudaFuncSetAttribute(k_search<TABU, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    k_search<TABU, NW><<<n_runs, threads, smem, st>>>(A);
     return cudaGetLastError();
 }
 
 cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st) {
-    cudaError_t err;
-    if (mode == 1) {
-        err = cudaFuncSetAttribute(k_search<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        k_search<true><<<n_runs, threads, smem, st>>>(A);
-    } else {
-        err = cudaFuncSetAttribute(k_search<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        k_search<false><<<n_runs, threads, smem, st>>>(A);
-    }
-    return cudaGetLastError();
+    const bool nw = A.inst.no_wait != 0;
+    if (mode == 1)
+        return nw ? launch_search_t<true, true>(A, n_runs, threads, smem, st)
+                  : launch_search_t<true, false>(A, n_runs, threads, smem, st);
+    return nw ? launch_search_t<false, true>(A, n_runs, threads, smem, st)
+              : launch_search_t<false, false>(A, n_runs, threads, smem, st);
 }
 
 __global__ void k_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC) {

@@ -14,6 +14,7 @@ namespace airsched {
 // One run's state in global memory (dump path).
 struct RunViewG {
     int32_t *succ, *pred, *veh, *endc, *depc, *inc, *svco, *pick_s, *w_s, *F, *E;
+    int32_t *arr, *sl, *pos;   // no-wait variant only (f3)
 };
 
 struct SearchArgs {
@@ -83,7 +84,7 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
 cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, cudaStream_t st);
 int padded_stride_host(int NL, int tbytes);
 
-size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem);
+size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem, bool nw);
 cudaError_t launch_build_state(const DevInst &I, const int32_t *ptr, const int32_t *ms, RunViewG &G, cudaStream_t st);
 cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int it, long long cur, long long best,
                              uint32_t mask, int32_t *delta, uint8_t *flags, unsigned long long *best_key, uint64_t N,

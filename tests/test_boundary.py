@@ -83,6 +83,35 @@ def test_schedule_check_matches_oracle(A, oracle_mod):
         h.check(np.array([0, 1] + [1] * (V - 1), np.int32), np.array([n + 5], np.int32))
 
 
+def test_nowait_schedule_check_matches_oracle(A, oracle_mod):
+    """f3 (no-wait variant): the host check against the oracle on random states and
+    on the oracle's own no-wait trajectory (states infeasible under waiting)."""
+    import dataclasses
+    rng = np.random.default_rng(3)
+    n_diff = 0
+    for cfg in ("tiny", "ontario"):
+        inst = dataclasses.replace(instgen.generate(cfg), no_wait=1)
+        wait = instgen.generate(cfg)
+        h, hw = A.Instance(inst), A.Instance(wait)
+        O = oracle_mod.Oracle(inst)
+        st, (p, m), _, _ = O.greedy()
+        states = [(p, m)] + [O.search(p, m, mode=1, tenure=5, max_iters=k, trace=False)["final"] for k in (5, 30)]
+        n, V = inst.n_missions, inst.n_vehicles
+        for _ in range(30):
+            perm = rng.permutation(n).astype(np.int32)
+            cuts = np.sort(rng.integers(0, n + 1, V - 1))
+            states.append((np.concatenate([[0], cuts, [n]]).astype(np.int32), perm))
+        for p, m in states:
+            f, obj = h.check(p, m)
+            assert obj == O.objective(p, m) and f == O.feasible(p, m)
+            n_diff += f != hw.check(p, m)[0]
+    assert n_diff >= 1
+    bad = dataclasses.replace(instgen.generate("tiny"), no_wait=2)
+    with pytest.raises(A.AirschedError) as e:
+        A.Instance(bad)
+    assert e.value.status == A.AS_ERR_INVALID_ARG
+
+
 def test_ctx_without_gpu_fails_loudly(A):
     import torch
     if torch.cuda.is_available():
