@@ -224,14 +224,14 @@ class Oracle:
         return int(lib().or_tabu_digest(self.ref, _p(Ec), int(it)))
 
     # ---- O13 -------------------------------------------------------------------
-    def greedy(self, insert_mode=0, max_repairs=50):
+    def greedy(self, insert_mode=0, max_repairs=50, seed=0):
         V, n = self.V, self.n
         length = np.zeros(V, np.int32)
         r = np.zeros((V, max(n, 1)), np.int32)
         nrep = C.c_int32()
         order = np.zeros(max(n, 1), np.int32)
-        st = lib().or_greedy(self.ref, int(insert_mode), int(max_repairs), _p(length), _p(r), C.byref(nrep),
-                             _p(order))
+        st = lib().or_greedy_seeded(self.ref, int(insert_mode), int(max_repairs), C.c_uint64(int(seed)), _p(length),
+                                    _p(r), C.byref(nrep), _p(order))
         return int(st), self.to_csr(length, r), int(nrep.value), order[:n]
 
 

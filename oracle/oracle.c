@@ -575,6 +575,15 @@ static int32_t greedy_try(const or_inst *I, int32_t insert_mode, int32_t m, cons
 
 int32_t or_greedy(const or_inst *I, int32_t insert_mode, int32_t max_repairs, int32_t *len_out, int32_t *r_out,
                   int32_t *n_repairs, int32_t *order_out) {
+    return or_greedy_seeded(I, insert_mode, max_repairs, 0, len_out, r_out, n_repairs, order_out);
+}
+
+/* f2 randomized starts (reading #41): seed != 0 replaces each phase's
+ * deadline order by a permutation of it -- SplitMix64(seed) Fisher-Yates from the
+ * top, phase 0 (helicopter-only) first, one generator stream, as the sweep's
+ * permutation vectors.  seed 0 is Algorithm 1 as written. */
+int32_t or_greedy_seeded(const or_inst *I, int32_t insert_mode, int32_t max_repairs, uint64_t seed,
+                         int32_t *len_out, int32_t *r_out, int32_t *n_repairs, int32_t *order_out) {
     int32_t n = I->n, V = I->V;
     int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
     int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
@@ -594,6 +603,17 @@ int32_t or_greedy(const or_inst *I, int32_t insert_mode, int32_t max_repairs, in
             }
             order[j + 1] = x;
         }
+    }
+    if (seed) {
+        uint64_t st = seed;
+        int32_t n0 = 0;
+        for (int32_t m = 0; m < n; m++) n0 += I->heli[m] != 0;
+        int32_t lo[2] = {0, n0}, hi[2] = {n0, n};
+        for (int32_t ph = 0; ph < 2; ph++)
+            for (int32_t x = hi[ph] - 1; x >= lo[ph] + 1; x--) {
+                int32_t y = lo[ph] + (int32_t)(or_splitmix64_next(&st) % (uint64_t)(x - lo[ph] + 1));
+                int32_t tmp = order[x]; order[x] = order[y]; order[y] = tmp;
+            }
     }
     for (int32_t v = 0; v < V; v++) len_out[v] = 0;
     *n_repairs = 0;

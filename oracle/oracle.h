@@ -104,6 +104,10 @@ int32_t or_kick(const or_inst *I, int32_t *len, int32_t *r, uint64_t seed, int32
 int32_t or_greedy(const or_inst *I, int32_t insert_mode, int32_t max_repairs,
                   int32_t *len_out, int32_t *r_out, int32_t *n_repairs, int32_t *order_out);
 
+/* f2: Algorithm 1 with a seeded placement order (reading #41); seed 0 == or_greedy. */
+int32_t or_greedy_seeded(const or_inst *I, int32_t insert_mode, int32_t max_repairs, uint64_t seed,
+                         int32_t *len_out, int32_t *r_out, int32_t *n_repairs, int32_t *order_out);
+
 uint64_t or_splitmix64_next(uint64_t *state);
 uint64_t or_tabu_digest(const or_inst *I, const int32_t *E, int32_t it);
 

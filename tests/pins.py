@@ -219,10 +219,13 @@ def ilp_optimum(inst, time_limit=60.0):
     return int(round(res.fun))
 
 
-def route_eval_nowait(inst, k, order):
+def route_eval_nowait(inst, k, order, d=None):
     """Independent no-wait route check (f3): the clock carries the arrival time;
-    every arrival <= its deadline, return <= day, flight <= p, compatibility."""
-    n, V, NN, d, b, f = _node_model(inst)
+    every arrival <= its deadline, return <= day, flight <= p, compatibility.
+    d: the node model's d (from _node_model), recomputed when None."""
+    n = inst.n_missions
+    if d is None:
+        d = _node_model(inst)[3]
     l = int(inst.vehicle_class[k])
     if len(order) and inst.heli_only[list(order)].any() and not inst.class_is_heli[l]:
         return None

@@ -452,3 +452,92 @@ def test_nowait_vs_independent_check(oracle_mod):
                 assert bool(f[idx] & 2) == feas and d[idx] == O.objective(p2, m2) - base_obj
                 n_feas += feas
     assert n_feas > 50
+
+
+# --------------------------------------------------- f2: randomized starts ---
+def _replay_greedy(inst, order, insert_mode, nowait=False):
+    """Independent replay of Alg. 1's placement decisions for a given
+    order, with the route checks of tests/pins.py: candidate slot per vehicle
+    (tail, or the deadline-sorted slot), feasible candidates only, the
+    smallest cost increase, ties to the lower vehicle (reading #24).  None when a
+    mission cannot be placed (the oracle would repair)."""
+    n, V, NN, d, b, f = pins._node_model(inst)
+    routes = [[] for _ in range(V)]
+
+    def cost(k, r):
+        if nowait:
+            return pins.route_eval_nowait(inst, k, r, d)
+        return pins._route_eval(inst, k, tuple(r), d, n) if r else 0
+
+    for m in order:
+        best = None
+        for k in range(V):
+            r = routes[k]
+            at = len(r)
+            if insert_mode == 1:
+                at = 0
+                while at < len(r) and inst.deadline_s[r[at]] <= inst.deadline_s[m]:
+                    at += 1
+            r2 = r[:at] + [int(m)] + r[at:]
+            c2, c1 = cost(k, r2), cost(k, r)
+            if c2 is None:
+                continue
+            if best is None or c2 - c1 < best[0]:
+                best = (c2 - c1, k, r2)
+        if best is None:
+            return None
+        routes[best[1]] = best[2]
+    return routes
+
+
+def test_seeded_greedy_order_and_replay(oracle_mod):
+    """Seed 0 is Alg. 1 as written; seed != 0 permutes each phase (reading #41).
+    Every seeded start that needed no repair equals an independent replay of the
+    placement rule in the oracle's reported order."""
+    n_checked = 0
+    for cfg, nowait in (("tiny", False), ("ontario", False), ("batched", False), ("ontario", True)):
+        inst = instgen.generate(cfg)
+        if nowait:
+            import dataclasses
+            inst = dataclasses.replace(inst, no_wait=1)
+        O = oracle_mod.Oracle(inst)
+        heli = set(np.flatnonzero(inst.heli_only).tolist())
+        base = O.greedy(insert_mode=1)
+        assert routes_of(*O.greedy(insert_mode=1, seed=0)[1]) == routes_of(*base[1])
+        orders = set()
+        for seed in range(1, 9):
+            for mode in (0, 1):
+                st, (p, m), nrep, order = O.greedy(insert_mode=mode, seed=seed)
+                assert sorted(order.tolist()) == list(range(inst.n_missions))
+                k = len(heli)
+                assert set(order[:k].tolist()) == heli
+                orders.add(tuple(order.tolist()))
+                if st == 0:
+                    assert O.feasible(p, m)
+                if nrep == 0:
+                    rep = _replay_greedy(inst, order, mode, nowait)
+                    if st == 0:
+                        assert rep == routes_of(p, m)
+                        n_checked += 1
+                    else:
+                        assert rep is None
+        assert len(orders) == 8
+    assert n_checked >= 10
+
+
+def test_seeded_greedy_permutation_uniform(oracle_mod):
+    """The phase permutations are uniform (a Fisher-Yates range slip would not be):
+    3 non-heli missions with distinct deadlines, 6000 seeds, chi-square over the 6 orders."""
+    inst = tiny_instance(3, 3, 901)
+    inst.heli_only = np.zeros(3, np.uint8)
+    inst.deadline_s = np.array([80000, 70000, 60000], np.int32)
+    O = oracle_mod.Oracle(inst)
+    counts = {}
+    for seed in range(1, 6001):
+        order = tuple(O.greedy(insert_mode=1, seed=seed)[3].tolist())
+        counts[order] = counts.get(order, 0) + 1
+    assert len(counts) == 6
+    exp = 1000.0
+    chi2 = sum((c - exp) ** 2 / exp for c in counts.values())
+    assert chi2 < 20.5   # p ~ 0.001 at 5 degrees of freedom
+    assert O.greedy(insert_mode=1)[3].tolist() == [2, 1, 0]
