@@ -119,10 +119,29 @@ as_status as_instance_upload(as_ctx *ctx, const as_instance *inst);
  * increase wins (ties: lower id); insert_mode 0 = TAIL (route end, reading
  * #23), 1 = SORTED (deadline-sorted slot).  When no vehicle fits, one
  * neighbourhood-search iteration runs on the device over the assigned missions
- * and the mission is retried once (reading #22).
- * Outputs (host or device): route_ptr_out[V+1], route_missions_out[n]. */
+ * and the mission is retried once (reading #22).  Runs on the
+ * device (one warp scans the vehicles per mission, a packed (increase, vehicle)
+ * minimum replaces the paper's mutex-protected CurrentMin).
+ * Outputs (host or device): route_ptr_out[V+1], route_missions_out[n].
+ * AS_ERR_INIT_FAILED: a mission fits no vehicle with nothing assigned yet
+ * (P:166), the repair found no improving move, the retry failed, or more than
+ * max_repairs repairs were needed. */
 as_status as_init_greedy(as_ctx *ctx, const as_instance *inst, int32_t insert_mode, int32_t max_repairs,
                          int32_t *route_ptr_out, int32_t *route_missions_out, int32_t *n_repairs_out);
+
+/* Batched randomized starts (reading #41): Algorithm 1
+ * for n_starts starts in one launch, one warp per start.  seeds[r] == 0 keeps
+ * the paper's placement order; seeds[r] != 0 permutes each phase's order
+ * (SplitMix64 Fisher-Yates from the top, helicopter-only phase first).  seeds:
+ * [n_starts] host or device, or NULL (all 0).  Outputs, host or device:
+ * route_ptr_out[n_starts][V+1], route_missions_out[n_starts][n],
+ * status_out[n_starts] (AS_OK or AS_ERR_INIT_FAILED; a failed start has empty
+ * routes) and n_repairs_out[n_starts], both nullable.  The outputs feed
+ * as_batch_run with shared_start = 0 directly (device pointers stay on the
+ * device). */
+as_status as_init_greedy_batch(as_ctx *ctx, const as_instance *inst, int32_t n_starts, int32_t insert_mode,
+                               int32_t max_repairs, const uint64_t *seeds, int32_t *route_ptr_out,
+                               int32_t *route_missions_out, int32_t *status_out, int32_t *n_repairs_out);
 
 /* ----------------------------------------------------------- evaluation --- */
 enum { AS_MODE_NS = 0, AS_MODE_TABU = 1 };

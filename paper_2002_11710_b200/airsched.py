@@ -28,7 +28,8 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_schedule_check", "as_ctx_create", "as_ctx_set_stream", "as_ctx_destroy", "as_instance_upload",
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
-           "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best"]
+           "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
+           "as_init_greedy_batch"]
 
 
 class AirschedError(RuntimeError):
@@ -82,6 +83,7 @@ def _load():
         "as_ctx_destroy": (None, [vp]),
         "as_instance_upload": (i32, [vp, vp]),
         "as_init_greedy": (i32, [vp, vp, i32, i32, vp, vp, vp]),
+        "as_init_greedy_batch": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "as_eval_moves": (i32, [vp, vp, vp, vp, i32, vp, i32, i64, u32, vp, vp, vp]),
         "as_tabu_run": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "as_nbhd_run": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -256,6 +258,23 @@ def as_init_greedy(ctx: Ctx, inst: Instance, insert_mode=0, max_repairs=50):
     _check(lib.as_init_greedy(ctx.handle, inst.handle, int(insert_mode), int(max_repairs), _ptr(ptr), _ptr(ms),
                               C.byref(nrep)))
     return ptr, ms[:inst.n], int(nrep.value)
+
+
+def as_init_greedy_batch(ctx: Ctx, inst: Instance, n_starts, seeds=None, insert_mode=1, max_repairs=50,
+                         ptr_out=None, ms_out=None, status_out=None, nrep_out=None):
+    """Marshalling for as_init_greedy_batch.  Without output arrays, host numpy
+    arrays are allocated and returned; torch CUDA tensors stay on the device."""
+    R = int(n_starts)
+    if ptr_out is None:
+        ptr_out = np.zeros((R, inst.V + 1), np.int32)
+        ms_out = np.zeros((R, max(inst.n, 1)), np.int32)
+        status_out = np.zeros(R, np.int32)
+        nrep_out = np.zeros(R, np.int32)
+    if isinstance(seeds, np.ndarray):
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+    _check(lib.as_init_greedy_batch(ctx.handle, inst.handle, R, int(insert_mode), int(max_repairs), _ptr(seeds),
+                                    _ptr(ptr_out), _ptr(ms_out), _ptr(status_out), _ptr(nrep_out)))
+    return ptr_out, ms_out, status_out, nrep_out
 
 
 def as_eval_moves(ctx: Ctx, inst: Instance, route_ptr, route_missions, mode=AS_MODE_TABU, tabu_expiry=None,

@@ -861,128 +861,68 @@ extern "C" as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_
 }
 
 // ------------------------------------------------------------ Algorithm 1 ---
+// Device Algorithm 1 for n_starts starts (greedy.cu, one warp per start).
+extern "C" as_status as_init_greedy_batch(as_ctx *ctx, const as_instance *I, int32_t n_starts, int32_t insert_mode,
+                                          int32_t max_repairs, const uint64_t *seeds, int32_t *route_ptr_out,
+                                          int32_t *route_missions_out, int32_t *status_out, int32_t *n_repairs_out) {
+    if (!ctx || !I || !route_ptr_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (n_starts < 1) return fail(AS_ERR_INVALID_ARG, "n_starts must be >= 1");
+    if (insert_mode != 0 && insert_mode != 1) return fail(AS_ERR_INVALID_ARG, "insert_mode must be 0 (TAIL) or 1 (SORTED)");
+    if (max_repairs < 0) return fail(AS_ERR_INVALID_ARG, "max_repairs must be >= 0");
+    if (I->n > 0 && !route_missions_out) return fail(AS_ERR_INVALID_ARG, "null route_missions_out");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const DevInst *D;
+    if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+    const int n = I->n, V = I->V;
+    const size_t R = (size_t)n_starts;
+    const void *ds = nullptr;
+    if (seeds && (st = dev_in(ctx, "g_seeds", seeds, R * 8, &ds)) != AS_OK) return st;
+    OutBuf op, om, os, onr;
+    if ((st = dev_out(ctx, "g_ptr", route_ptr_out, R * (V + 1) * 4, op)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "g_ms", route_missions_out, std::max<size_t>(R * n * 4, 4), om)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "g_status", status_out, R * 4, os)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "g_nrep", n_repairs_out, R * 4, onr)) != AS_OK) return st;
+    void *ord;
+    if ((st = scratch(ctx, "g_order", (size_t)n * 4 + 4, &ord)) != AS_OK) return st;
+    // layout: T + up to 8 warps of state in shared memory, else state only, else global state
+    const size_t sb = greedy_state_bytes(*D);
+    const size_t lim = ctx->max_smem;
+    int warps = 0;
+    bool T_smem = false, state_smem = false;
+    if (env_int("AIRSCHED_GREEDY_GLOBAL", 0) == 1) warps = -1;   // test knob: state in global memory
+    for (int w = 8; w >= 1 && !warps; w /= 2)
+        if (greedy_smem_bytes(*D, w, true, true) <= lim) { warps = w; T_smem = state_smem = true; }
+    for (int w = 8; w >= 1 && !warps; w /= 2)
+        if (greedy_smem_bytes(*D, w, false, true) <= lim) { warps = w; state_smem = true; }
+    void *sg = nullptr;
+    if (warps <= 0) {
+        warps = 4;
+        T_smem = greedy_smem_bytes(*D, warps, true, false) <= lim;
+        if ((st = scratch(ctx, "g_state", R * sb, &sg)) != AS_OK) return st;
+    }
+    warps = std::max(1, std::min<int>(warps, (int)std::min<size_t>(8, R)));
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(launch_greedy(*D, n_starts, insert_mode, max_repairs, (const uint64_t *)ds, (int32_t *)ord,
+                           (int32_t *)sg, warps, T_smem, state_smem, (int32_t *)op.dev, (int32_t *)om.dev,
+                           (int32_t *)os.dev, (int32_t *)onr.dev, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timed = true;
+    ctx->launches += n > 0 ? 2 : 1;
+    return finish_out(ctx, {&op, &om, &os, &onr});
+}
+
+// Algorithm 1 for one start in the paper's order: the batched device kernel with n_starts = 1, seed 0.
 extern "C" as_status as_init_greedy(as_ctx *ctx, const as_instance *I, int32_t insert_mode, int32_t max_repairs,
                                     int32_t *route_ptr_out, int32_t *route_missions_out, int32_t *n_repairs_out) {
     if (!ctx || !I || !route_ptr_out) return fail(AS_ERR_INVALID_ARG, "null argument");
-    if (insert_mode != 0 && insert_mode != 1) return fail(AS_ERR_INVALID_ARG, "insert_mode must be 0 (TAIL) or 1 (SORTED)");
-    as_status st = set_device(ctx);
+    int32_t status = AS_OK, nrep = 0;
+    as_status st = as_init_greedy_batch(ctx, I, 1, insert_mode, max_repairs, nullptr, route_ptr_out,
+                                        route_missions_out, &status, &nrep);
     if (st != AS_OK) return st;
-    const int n = I->n, V = I->V;
-    std::vector<int32_t> order;
-    for (int phase = 0; phase < 2; phase++) {
-        std::vector<int32_t> ph;
-        for (int m = 0; m < n; m++)
-            if ((phase == 0) == (I->heli[m] != 0)) ph.push_back(m);
-        std::stable_sort(ph.begin(), ph.end(), [&](int a, int b) { return I->w[a] < I->w[b] || (I->w[a] == I->w[b] && a < b); });
-        order.insert(order.end(), ph.begin(), ph.end());
-    }
-    HostSched S;
-    S.routes.assign(V, {});
-    std::vector<int64_t> F(V, 0);
-    int repairs = 0, assigned = 0;
-    auto try_place = [&](int m, int *bv, int *bat, int64_t *binc) {
-        *bv = -1;
-        for (int v = 0; v < V; v++) {
-            if (I->heli[m] && !I->cls_heli[I->vcls[v]]) continue;              // con9 (lines 10-12)
-            const auto &r = S.routes[v];
-            int at = (int)r.size();
-            if (insert_mode == 1) {
-                at = 0;
-                while (at < (int)r.size() && I->w[r[at]] <= I->w[m]) at++;
-            }
-            if (I->no_wait) {   // arrivals depend on the prefix: check the whole new route (f3)
-                std::vector<int32_t> r2(r);
-                r2.insert(r2.begin() + at, m);
-                int64_t c2;
-                bool f2;
-                route_eval(I, v, r2, &c2, &f2);
-                if (!f2) continue;
-                int64_t inc = c2 - F[v];
-                if (*bv < 0 || inc < *binc) { *bv = v; *bat = at; *binc = inc; }
-                continue;
-            }
-            int prev = at > 0 ? r[at - 1] : -1;
-            int next = at < (int)r.size() ? r[at] : -1;
-            int64_t dep_prev = prev >= 0 ? I->w[prev] : 0;
-            int64_t d_in = h_dm(I, v, prev, m);
-            int64_t d_out = next >= 0 ? h_dm(I, v, m, next) : h_db(I, v, m);
-            int64_t d_old = next >= 0 ? h_dm(I, v, prev, next) : h_db(I, v, prev);
-            int64_t w_next = next >= 0 ? I->w[next] : I->DAY;
-            if (dep_prev + d_in > I->w[m]) continue;                           // lines 13-20
-            if (I->w[m] + d_out > w_next) continue;                            // lines 21-28
-            int64_t inc = r.empty() ? d_in + d_out : d_in + d_out - d_old;
-            if (F[v] + inc > I->P) continue;                                   // lines 29-31
-            if (*bv < 0 || inc < *binc) { *bv = v; *bat = at; *binc = inc; }   // lines 32-34
-        }
-        return *bv >= 0;
-    };
-    for (int i = 0; i < n; i++) {
-        int m = order[i], bv, bat;
-        int64_t binc;
-        if (!try_place(m, &bv, &bat, &binc)) {
-            if (assigned == 0 || repairs >= max_repairs)
-                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: no vehicle can take mission %d (P:166)", m);
-            // repair: one NS iteration on the device over the assigned missions
-            const DevInst *D;
-            if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
-            int64_t cur = 0;
-            for (int v = 0; v < V; v++) cur += F[v];
-            uint64_t key = AS_KEY_NONE;
-            if ((st = eval_core(ctx, I, D, S, AS_MODE_NS, nullptr, 0, cur, cur, AS_MOVE_ALL, nullptr, nullptr, &key)) != AS_OK)
-                return st;
-            if (key == AS_KEY_NONE || key_cls(key) != 0)
-                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: repair found no improving move for mission %d", m);
-            uint32_t idx = key_idx(key);
-            const uint32_t Sn = (uint32_t)(n + V), Rb = (uint32_t)n * Sn;
-            auto locate = [&](int x, int *vv, int *pp) {
-                for (int v = 0; v < V; v++)
-                    for (int p = 0; p < (int)S.routes[v].size(); p++)
-                        if (S.routes[v][p] == x) { *vv = v; *pp = p; return; }
-                *vv = -1; *pp = -1;
-            };
-            if (idx < Rb) {
-                int mm = idx / Sn, t = idx % Sn, a, pa;
-                locate(mm, &a, &pa);
-                S.routes[a].erase(S.routes[a].begin() + pa);
-                if (t < n) {
-                    int b, pb;
-                    locate(t, &b, &pb);
-                    S.routes[b].insert(S.routes[b].begin() + pb, mm);
-                } else {
-                    S.routes[t - n].push_back(mm);
-                }
-            } else {
-                int m1 = (idx - Rb) / n, m2 = (idx - Rb) % n, a, pa, b, pb;
-                locate(m1, &a, &pa);
-                locate(m2, &b, &pb);
-                S.routes[a][pa] = m2;
-                S.routes[b][pb] = m1;
-            }
-            for (int v = 0; v < V; v++) {
-                bool f;
-                route_eval(I, v, S.routes[v], &F[v], &f);
-            }
-            repairs++;
-            if (!try_place(m, &bv, &bat, &binc))
-                return fail(AS_ERR_INIT_FAILED, "Algorithm 1: mission %d still unplaceable after repair", m);
-        }
-        S.routes[bv].insert(S.routes[bv].begin() + bat, m);
-        F[bv] += binc;
-        assigned++;
-    }
-    std::vector<int32_t> ptr(V + 1, 0), ms;
-    for (int v = 0; v < V; v++) {
-        ms.insert(ms.end(), S.routes[v].begin(), S.routes[v].end());
-        ptr[v + 1] = (int32_t)ms.size();
-    }
-    if (is_device_ptr(route_ptr_out)) CUDA_TRY(cudaMemcpy(route_ptr_out, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice));
-    else memcpy(route_ptr_out, ptr.data(), ptr.size() * 4);
-    if (n > 0) {
-        if (!route_missions_out) return fail(AS_ERR_INVALID_ARG, "null route_missions_out");
-        if (is_device_ptr(route_missions_out)) CUDA_TRY(cudaMemcpy(route_missions_out, ms.data(), ms.size() * 4, cudaMemcpyHostToDevice));
-        else memcpy(route_missions_out, ms.data(), ms.size() * 4);
-    }
-    if (n_repairs_out) *n_repairs_out = repairs;
+    if (status != AS_OK)
+        return fail(AS_ERR_INIT_FAILED, "Algorithm 1: a mission could not be placed, even after %d repair(s) (P:166, P:213)", nrep);
+    if (n_repairs_out) *n_repairs_out = nrep;
     return AS_OK;
 }
 

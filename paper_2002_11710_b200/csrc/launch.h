@@ -93,6 +93,11 @@ cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
                 size_t *run_bytes);
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st);
+size_t greedy_smem_bytes(const DevInst &I, int warps, bool T_smem, bool state_smem);
+size_t greedy_state_bytes(const DevInst &I);
+cudaError_t launch_greedy(const DevInst &I, int n_starts, int insert_mode, int max_repairs, const uint64_t *seeds,
+                          int32_t *order_scratch, int32_t *state_global, int warps, bool T_smem, bool state_smem,
+                          int32_t *ptr_out, int32_t *ms_out, int32_t *status_out, int32_t *nrep_out, cudaStream_t st);
 cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
                        cudaStream_t st);
 
