@@ -51,6 +51,7 @@ struct as_instance {
     std::vector<int32_t> T, base_loc, vbase, vcls, vloc, pick, del, w;
     std::vector<uint8_t> cls_heli, heli, vcls8;
     int32_t maxT = 0;
+    int32_t tsym = 1;      // T[c][a][b] == T[c][b][a] for every layer
 };
 
 static uint64_t g_uid = 1;
@@ -83,6 +84,10 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
                 if (a == b && t != 0) return fail(AS_ERR_INVALID_ARG, "travel_s diagonal must be 0 (S:35)");
                 if (t > I->maxT) I->maxT = t;
             }
+    for (int64_t c = 0; c < NC && I->tsym; c++)
+        for (int64_t a = 0; a < NL && I->tsym; a++)
+            for (int64_t b = a + 1; b < NL; b++)
+                if (I->T[(c * NL + a) * NL + b] != I->T[(c * NL + b) * NL + a]) { I->tsym = 0; break; }
     I->cls_heli.assign(d->class_is_heli, d->class_is_heli + NC);
     I->base_loc.assign(d->base_location, d->base_location + B);
     for (auto x : I->base_loc)
@@ -377,9 +382,19 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
         void *tp = nullptr;
         CUDA_TRY(cudaMalloc(&tp, (size_t)I->NC * I->NL * NLp * D.tpad_bytes + 16));
         D.allocs.push_back(tp);
-        CUDA_TRY(launch_pad_table(D.d.T, tp, I->NC, I->NL, NLp, D.tpad_bytes, s));
+        CUDA_TRY(launch_pad_table(D.d.T, tp, I->NC, I->NL, NLp, D.tpad_bytes, false, s));
         ctx->launches++;
         D.Tpad = tp;
+        D.d.tsym = I->tsym;
+        D.d.TpadT = tp;
+        if (!I->tsym) {   // the scorers read T[c][x][y] for x varying as the transposed row (score.cuh)
+            void *tt = nullptr;
+            CUDA_TRY(cudaMalloc(&tt, (size_t)I->NC * I->NL * NLp * D.tpad_bytes + 16));
+            D.allocs.push_back(tt);
+            CUDA_TRY(launch_pad_table(D.d.T, tt, I->NC, I->NL, NLp, D.tpad_bytes, true, s));
+            ctx->launches++;
+            D.d.TpadT = tt;
+        }
     }
     auto &slot = ctx->insts[I];
     slot = std::move(D);
@@ -673,7 +688,9 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             auto &D = ctx->insts[I];
             const int tb = D.tpad_bytes;
             struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
+            const bool t_global = env_int("AIRSCHED_GRID_T_GLOBAL", 0) == 1;   // test knob
             for (auto o : gopts) {
+                if (t_global && o.t) continue;
                 size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, 4, o.t, o.e && tabu, tabu);
                 if (b <= ctx->max_smem) {
                     GA.T_smem = o.t;

@@ -42,6 +42,8 @@ struct DevInst {
     int32_t no_wait;         // f3 variant: depart on arrival (reading #40)
     int32_t maxT;            // max travel time (selects the uint16 table)
     int32_t svcpos;          // every pickup->delivery leg > 0 in every class (enables the FAST scorers)
+    int32_t tsym;            // every layer of T is symmetric (the transposed table is T itself)
+    const void *TpadT;       // padded table transposed per layer (== the padded table when tsym)
 };
 
 // Selection key (O9): class bit 63, biased delta bits 62..32, index bits 31..0.

@@ -54,7 +54,8 @@ size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, boo
     return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
 }
 
-template <bool TABU, class TT, class ET, bool FULL>
+// TR: the table is read from global memory (row-local reads, score.cuh).
+template <bool TABU, class TT, class ET, bool FULL, bool TR>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     if (gridDim.x > 1) grid.sync();   // global tabu matrix initialised before anyone reads it
 
     ScoreCtx<TT, ET> SC;
-    SC.Ts = Ts; SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
+    SC.Ts = Ts; SC.Tt = I.tsym ? Ts : reinterpret_cast<const TT *>(I.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     int it = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
-        uint64_t kmin = score_tiles<TABU, FULL>(SC, M, R, GT, 0, GT.n_total, gwarp, nwarps_all, it, cur, best, lane);
+        uint64_t kmin = score_tiles<TABU, FULL, TR>(SC, M, R, GT, 0, GT.n_total, gwarp, nwarps_all, it, cur, best, lane);
         kmin = wmin(kmin);
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
@@ -264,7 +265,7 @@ __global__ void k_bs_to_csr(const int32_t *BS, int n, int V, int32_t *bp, int32_
 template <bool TABU, class TT, class ET, bool FULL>
 static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks, int threads, size_t smem,
                             cudaStream_t st) {
-    auto kern = k_grid<TABU, TT, ET, FULL>;
+    auto kern = GA.T_smem ? k_grid<TABU, TT, ET, FULL, false> : k_grid<TABU, TT, ET, FULL, true>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     SearchArgs a = A;
@@ -297,17 +298,18 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
     return err;
 }
 
-__global__ void k_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes) {
+__global__ void k_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, int transpose) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NC * NL * NL; i += gridDim.x * blockDim.x) {
         int c = i / (NL * NL), r = (i / NL) % NL, col = i % NL;
-        size_t o = (size_t)(c * NL + r) * NLp + col;
+        size_t o = transpose ? (size_t)(c * NL + col) * NLp + r : (size_t)(c * NL + r) * NLp + col;
         if (tbytes == 2) reinterpret_cast<uint16_t *>(out)[o] = (uint16_t)T[i];
         else reinterpret_cast<int32_t *>(out)[o] = T[i];
     }
 }
 
-cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, cudaStream_t st) {
-    k_pad_table<<<256, 256, 0, st>>>(T, out, NC, NL, NLp, tbytes);
+cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, bool transpose,
+                             cudaStream_t st) {
+    k_pad_table<<<256, 256, 0, st>>>(T, out, NC, NL, NLp, tbytes, transpose ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -81,7 +81,8 @@ void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, i
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
                         cudaStream_t st);
-cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, cudaStream_t st);
+cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, bool transpose,
+                             cudaStream_t st);
 int padded_stride_host(int NL, int tbytes);
 
 size_t search_smem_bytes(int n, int V, int NL, int NC, bool T_smem, bool E_smem, bool nw);

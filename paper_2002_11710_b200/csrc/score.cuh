@@ -10,6 +10,14 @@
 // '<' keeps the lowest index among equal keys (O9, reading #26).  Each scorer
 // returns the tile's best packed 64-bit key for this lane (AS_KEY_NONE if none).
 //
+// Table reads: every scored move reads T at (row x, column y) with one of x, y
+// fixed for the whole row m (m1) and the other varying over the lanes.  With the
+// table in shared memory (TR = false) the lanes read down a column (rows spread
+// over the banks by the odd padded stride).  With the table in global memory
+// (TR = true) the lanes read along ONE row -- of T, or of its per-layer
+// transpose Tt -- so each row m touches a few L1-resident rows shared by the
+// CTA's warps instead of a different row per lane.
+//
 // Formulas: DESIGN.md §3 (the same arithmetic as engine.cuh, rewritten for
 // register-resident operands; adjacent swaps are excluded here and scored by
 // engine.cuh's exact three-link formula).  Operands are in the AoS records of
@@ -41,6 +49,7 @@ __device__ __forceinline__ int madd(int a, int mul, int b) {   // a * mul + b
 template <class TT, class ET>
 struct ScoreCtx {
     const TT *Ts;          // [NC][NL][NLp] travel times
+    const TT *Tt;          // the same, transposed per layer (== Ts for symmetric tables)
     const int4 *CS4;       // [S] {w, pick | del << 16, svc0, svc1}
     const uint8_t *MH;     // [n] helicopter-only
     const uint32_t *VC;    // [V] cls | heli_ok << 8 | base location << 16
@@ -53,10 +62,10 @@ struct ScoreCtx {
     int one, neg;          // 1 and -1, opaque to the compiler (see madd)
 };
 
-template <bool TABU, bool FULL, class TT, class ET>
+template <bool TABU, bool FULL, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
                                                 int asp, int lane) {
-    const TT *Ts = C.Ts;
+    const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
     const uint32_t *VC = C.VC, *LK = C.LK;
@@ -77,8 +86,9 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
                 const int4 cs = CS4[t];
                 const uint32_t vc = VC[b];
                 const int cb = vc & 0xFF;
-                t1 = (cb * NL + (rs.w & 0xFFFF)) * NLp;     // row of T_cb[endc(t)][.]
-                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb
+                t1 = TR ? cb * NL * NLp + (rs.w & 0xFFFF)    // column endc(t) of Tt_cb (row pick_m per m)
+                        : (cb * NL + (rs.w & 0xFFFF)) * NLp; // row endc(t) of T_cb (column pick_m per m)
+                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb (row del_m per m)
                 dw = -rs.x;                                  // -dep(pred t)
                 kk = rs.z - rs.y;                            // svco(t) - inc(t)
                 wsv = cs.x - rs.z;                           // w(t) - svco(t)
@@ -105,7 +115,7 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
         const int Fa = F[a];
         const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
         const int intra_lim = P - Fa - rem;
-        const int w_m = cm.x, pick_m = cm.y & 0xFFFF, rowD = ((uint32_t)cm.y >> 16) * NLp;
+        const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : (cm.y & 0xFFFF), rowD = ((uint32_t)cm.y >> 16) * NLp;
         const int svm0 = cm.z, svm1 = cm.w;
         const bool heli_m = MH[m] != 0;
         const ET *Erow = TABU ? E + m * V : nullptr;
@@ -119,8 +129,8 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
             const int b = (int)(int16_t)(inf & 0xFFFF);
             const bool cb1 = (inf >> 16) & 1;
             const bool hok = (inf >> 20) & 1;
-            const int T1 = (int)Ts[madd(c_t1[k], one, pick_m)];
-            const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];
+            const int T1 = (int)(TR ? Tt : Ts)[madd(c_t1[k], one, rowP)];     // T_cb[endc t][pick m]
+            const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];     // T_cb[del m][pick t]
             const int x1 = madd(T1, one, cb1 ? svm1 : svm0);
             const int ins = madd(x1, one, madd(T2, one, c_k[k]));
             const int delta = madd(rem, one, ins);
@@ -142,10 +152,10 @@ __device__ __forceinline__ uint64_t score_reloc(const ScoreCtx<TT, ET> &C, int t
     }    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
 }
 
-template <bool TABU, bool FULL, class TT, class ET>
+template <bool TABU, bool FULL, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi, int m1_lo, int m1_hi, int it,
                                                int asp, int lane) {
-    const TT *Ts = C.Ts;
+    const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
     const uint32_t *VC = C.VC, *LK = C.LK;
@@ -175,8 +185,10 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
                 ps = (c2.y & 0xFFFF) | (s2 << 16);              // pick2 | s2 << 16
                 sv0 = c2.z;
                 sv1 = c2.w;
-                d2 = ((uint32_t)c2.y >> 16) * NLp;               // row del2 (any class)
-                e2 = (cb * NL + (r2.w & 0xFFFF)) * NLp;           // row T_cb[endc2]
+                d2 = TR ? (int)((uint32_t)c2.y >> 16)              // column del2 of Tt (row pick(s1) per m1)
+                        : (int)((uint32_t)c2.y >> 16) * NLp;       // row del2 of T (column pick(s1) per m1)
+                e2 = TR ? cb * NL * NLp + (r2.w & 0xFFFF)          // column endc2 of Tt_cb (row pick1 per m1)
+                        : (cb * NL + (r2.w & 0xFFFF)) * NLp;       // row endc2 of T_cb (column pick1 per m1)
                 p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
                 w2 = c2.x;
                 dep2 = r2.x;
@@ -202,8 +214,9 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
         const int ca = vca & 0xFF;
         const bool hoka = (vca >> 8) & 1;
         const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
-        const int col_ta2 = ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
-        const int pick1 = c1.y & 0xFFFF, row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+        const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp   // Tt_ca[pick(s1)][.]
+                               : ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
+        const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : (c1.y & 0xFFFF), row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
         const int depc1 = r1.x, w1 = c1.x;
         const bool heli1 = MH[m1] != 0;
         const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
@@ -225,8 +238,8 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
             const int pick2 = q_ps[k] & 0xFFFF, s2 = (uint32_t)q_ps[k] >> 16;
             const bool same = a == b;
             const int ya1 = madd((int)Ts[madd(row_ya1, one, pick2)], one, ca ? q_sv1[k] : q_sv0[k]); // p1 -> m2
-            const int Ta2 = (int)Ts[madd(col_ta2, one, q_d2[k])];                              // m2 -> s1
-            const int yb1 = madd((int)Ts[madd(q_e2[k], one, pick1)], one, cb1 ? sv11 : sv10);  // p2 -> m1
+            const int Ta2 = (int)(TR ? Tt : Ts)[madd(row_ta2, one, q_d2[k])];                              // m2 -> s1
+            const int yb1 = madd((int)(TR ? Tt : Ts)[madd(q_e2[k], one, rowp1)], one, cb1 ? sv11 : sv10);  // p2 -> m1
             const int Tb2 = (int)Ts[madd(q_p2[k], one, row_tb2)];                             // m1 -> s2
             const int da = madd(ya1, one, madd(Ta2, one, ka));
             const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
@@ -261,19 +274,19 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
 // one integer margin whose sign bit poisons the key, and admissibility is a
 // sign-bit expression -- the scoring loops are issue-bound, so every
 // compare/select removed counts.
-template <bool TABU, bool HELI, class TT, class ET>
-__device__ __forceinline__ void reloc_row_fast(const TT *Ts, const ET *Erow, const int (&c_t1)[KR],
+template <bool TABU, bool HELI, bool TR, class TT, class ET>
+__device__ __forceinline__ void reloc_row_fast(const TT *Ts, const TT *Tt, const ET *Erow, const int (&c_t1)[KR],
                                                const int (&c_t2)[KR], const int (&c_dw)[KR], const int (&c_k)[KR],
                                                const int (&c_wsv)[KR], const int (&c_slk)[KR],
                                                const int (&c_b)[KR], const int (&c_cb)[KR], int a, int rem,
-                                               int inter_bias, int intra_lim, int w_m, int pick_m, int rowD,
+                                               int inter_bias, int intra_lim, int w_m, int rowP, int rowD,
                                                int svm0, int dsvm, int it, int asp, uint32_t base, int one,
                                                int neg, uint32_t &bk32, uint32_t &bidx) {
     const int wm_neg = madd(w_m, neg, 0);
 #pragma unroll
     for (int k = 0; k < KR; k++) {
-        const int T1 = (int)Ts[madd(c_t1[k], one, pick_m)];
-        const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];
+        const int T1 = (int)(TR ? Tt : Ts)[madd(c_t1[k], one, rowP)];     // T_cb[endc t][pick m]
+        const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];     // T_cb[del m][pick t]
         const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));                 // d(c, m)
         const int ins = madd(x1, one, madd(T2, one, c_k[k]));
         const int delta = madd(rem, one, ins);
@@ -297,10 +310,10 @@ __device__ __forceinline__ void reloc_row_fast(const TT *Ts, const ET *Erow, con
     }
 }
 
-template <bool TABU, class TT, class ET>
+template <bool TABU, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
                                                      int asp, int lane) {
-    const TT *Ts = C.Ts;
+    const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
     const uint32_t *VC = C.VC, *LK = C.LK;
@@ -321,8 +334,9 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
                 const uint32_t vc = VC[bb];
                 b = bb;
                 cb = vc & 0xFF;
-                t1 = (cb * NL + (rs.w & 0xFFFF)) * NLp;     // row of T_cb[endc(t)][.]
-                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb
+                t1 = TR ? cb * NL * NLp + (rs.w & 0xFFFF)    // column endc(t) of Tt_cb (row pick_m per m)
+                        : (cb * NL + (rs.w & 0xFFFF)) * NLp; // row endc(t) of T_cb (column pick_m per m)
+                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb (row del_m per m)
                 dw = -rs.x;                                  // -dep(pred t)
                 kk = rs.z - rs.y;                            // svco(t) - inc(t)
                 wsv = cs.x - rs.z;                           // w(t) - svco(t)
@@ -348,25 +362,25 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
         const int Fa = F[a];
         const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
         const int intra_lim = P - Fa - rem;
-        const int w_m = cm.x, pick_m = cm.y & 0xFFFF, rowD = ((uint32_t)cm.y >> 16) * NLp;
+        const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : (cm.y & 0xFFFF), rowD = ((uint32_t)cm.y >> 16) * NLp;
         const ET *Erow = TABU ? E + m * V : nullptr;
         const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
         if (MH[m])
-            reloc_row_fast<TABU, true>(Ts, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
-                                       intra_lim, w_m, pick_m, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
+            reloc_row_fast<TABU, true, TR>(Ts, Tt, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
+                                       intra_lim, w_m, rowP, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
                                        bidx);
         else
-            reloc_row_fast<TABU, false>(Ts, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
-                                        intra_lim, w_m, pick_m, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
+            reloc_row_fast<TABU, false, TR>(Ts, Tt, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
+                                        intra_lim, w_m, rowP, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
                                         bidx);
     }
     return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
 }
 
-template <bool TABU, class TT, class ET>
+template <bool TABU, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, int hi, int m1_lo, int m1_hi, int it,
                                                     int asp, int lane) {
-    const TT *Ts = C.Ts;
+    const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
     const uint32_t *VC = C.VC, *LK = C.LK;
@@ -398,8 +412,10 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 p2m = c2.y & 0xFFFF;                              // pick2
                 sv0 = c2.z;
                 dsv = c2.w - c2.z;
-                d2 = ((uint32_t)c2.y >> 16) * NLp;               // row del2 (any class)
-                e2 = (cb * NL + (r2.w & 0xFFFF)) * NLp;           // row T_cb[endc2]
+                d2 = TR ? (int)((uint32_t)c2.y >> 16)              // column del2 of Tt (row pick(s1) per m1)
+                        : (int)((uint32_t)c2.y >> 16) * NLp;       // row del2 of T (column pick(s1) per m1)
+                e2 = TR ? cb * NL * NLp + (r2.w & 0xFFFF)          // column endc2 of Tt_cb (row pick1 per m1)
+                        : (cb * NL + (r2.w & 0xFFFF)) * NLp;       // row endc2 of T_cb (column pick1 per m1)
                 p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
                 w2 = c2.x;
                 dep2 = r2.x;
@@ -424,8 +440,9 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
         const uint32_t vca = VC[a];
         const int ca = vca & 0xFF;
         const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
-        const int col_ta2 = ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
-        const int pick1 = c1.y & 0xFFFF, row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+        const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp   // Tt_ca[pick(s1)][.]
+                               : ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
+        const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : (c1.y & 0xFFFF), row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
         const int ndepc1 = -r1.x, w1 = c1.x, nw1 = -c1.x;
         const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
         const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
@@ -443,8 +460,8 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
             const int bf = q_bf[k];
             const int b = (int)(int16_t)(bf & 0xFFFF);
             const int ya1 = madd(q_dsv[k], ca, madd((int)Ts[madd(row_ya1, one, q_p2m[k])], one, q_sv0[k]));  // p1 -> m2
-            const int Ta2 = (int)Ts[madd(col_ta2, one, q_d2[k])];                                        // m2 -> s1
-            const int yb1 = madd(q_cb[k], dsv1, madd((int)Ts[madd(q_e2[k], one, pick1)], one, sv10));    // p2 -> m1
+            const int Ta2 = (int)(TR ? Tt : Ts)[madd(row_ta2, one, q_d2[k])];                                // m2 -> s1
+            const int yb1 = madd(q_cb[k], dsv1, madd((int)(TR ? Tt : Ts)[madd(q_e2[k], one, rowp1)], one, sv10));  // p2 -> m1
             const int Tb2 = (int)Ts[madd(q_p2[k], one, row_tb2)];                                       // m1 -> s2
             const int da = madd(ya1, one, madd(Ta2, one, ka));
             const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
@@ -497,7 +514,7 @@ __host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
 }
 
 // Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
-template <bool TABU, bool FULL, class TT, class ET, class MV, class RV>
+template <bool TABU, bool FULL, bool TR, class TT, class ET, class MV, class RV>
 __device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
                                                 const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
                                                 int it, long long cur, long long best, int lane) {
@@ -509,16 +526,16 @@ __device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, cons
         if (tile < GT.n_reloc) {
             const int c = tile % GT.nTC, g = tile / GT.nTC;
             const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
-            kb = FULL ? score_reloc_fast<TABU>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane)
-                      : score_reloc<TABU, FULL>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
+            kb = FULL ? score_reloc_fast<TABU, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane)
+                      : score_reloc<TABU, FULL, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
         } else if (tile < GT.n_reloc + GT.n_swap) {
             const int r = tile - GT.n_reloc;
             const int j = r % GT.nSC, g = r / GT.nSC;
             const int hi = n - j * 32 * KS;
             const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
             if (m_lo < m_hi)
-                kb = FULL ? score_swap_fast<TABU>(SC, hi, m_lo, m_hi, it, asp, lane)
-                          : score_swap<TABU, FULL>(SC, hi, m_lo, m_hi, it, asp, lane);
+                kb = FULL ? score_swap_fast<TABU, TR>(SC, hi, m_lo, m_hi, it, asp, lane)
+                          : score_swap<TABU, FULL, TR>(SC, hi, m_lo, m_hi, it, asp, lane);
         } else {
             const int x = (tile - GT.n_reloc - GT.n_swap) * 32 + lane;
             if (x < n && (FULL || (SC.mask & 8u))) {

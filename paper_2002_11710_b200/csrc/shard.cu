@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(768, 1) k_shard_eval(SearchArgs A, ShardViews 
     CompactRV<int32_t> R;
     shard_views<TT>(I, SV, M, R);
     ScoreCtx<TT, int32_t> SC;
-    SC.Ts = reinterpret_cast<const TT *>(SV.T); SC.CS4 = SV.CS4; SC.MH = SV.MH; SC.VC = SV.VC; SC.RS4 = SV.RS4;
+    SC.Ts = reinterpret_cast<const TT *>(SV.T);
+    SC.Tt = A.inst.tsym ? SC.Ts : reinterpret_cast<const TT *>(A.inst.TpadT);
+    SC.CS4 = SV.CS4; SC.MH = SV.MH; SC.VC = SV.VC; SC.RS4 = SV.RS4;
     SC.LK = SV.LK; SC.F = SV.F; SC.E = SV.E;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = I.NL; SC.NLp = SV.NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(768, 1) k_shard_eval(SearchArgs A, ShardViews 
     const GridTiles GT = grid_tiles(n, V, G);
     const int it = ctl->it;
     const long long cur = ctl->cur, best = ctl->best;
-    uint64_t kmin = score_tiles<TABU, FULL>(SC, M, R, GT, tlo, thi, blockIdx.x * nwarps + warp, gridDim.x * nwarps,
+    uint64_t kmin = score_tiles<TABU, FULL, true>(SC, M, R, GT, tlo, thi, blockIdx.x * nwarps + warp, gridDim.x * nwarps,
                                             it, cur, best, lane);
     kmin = wmin(kmin);
     if (lane == 0) red[warp] = kmin;

@@ -380,6 +380,8 @@ def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch):
     _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
     monkeypatch.setenv("AIRSCHED_GRID_G", "3")
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+    monkeypatch.setenv("AIRSCHED_GRID_T_GLOBAL", "1")   # table in global memory: row-local reads
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
 
 
 def test_surge_run_parity_prefix(A, ctx, oracle_mod):
@@ -524,3 +526,52 @@ def test_sweep_mode_parity(A, ctx, oracle_mod, cfg, steps):
         o = O.sweep(p, m, mode=1, tenure=c.tenure, max_steps=steps, seed=int(seeds[r]))
         assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == o["iters_done"]
         assert res[r]["best_iter"] == o["best_iter"]
+
+
+def _asymmetric(cfg, seed=5):
+    """The configuration with a seeded asymmetric travel-time table (T[c][a][b] !=
+    T[c][b][a]); the kernels then read the transposed padded copy (score.cuh)."""
+    inst = instgen.generate(cfg)
+    rng = np.random.default_rng(seed)
+    T = inst.travel_s.astype(np.int64)
+    T = T + rng.integers(0, 120, size=T.shape)
+    for c in range(T.shape[0]):
+        np.fill_diagonal(T[c], 0)
+    inst.travel_s = T.astype(np.int32)
+    return inst
+
+
+@pytest.mark.parametrize("cfg,iters", [("ontario", 400), ("batched", 300), ("large", 25)])
+def test_asymmetric_table_parity(A, ctx, oracle_mod, cfg, iters, monkeypatch):
+    """Every scorer path (one-CTA and whole-GPU k_grid, k_batch, the sharded kernels)
+    on an asymmetric table, where T and its transpose differ."""
+    inst = _asymmetric(cfg)
+    assert any((inst.travel_s[c] != inst.travel_s[c].T).any() for c in range(inst.travel_s.shape[0]))
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=4, kick=4)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    with monkeypatch.context() as mp:
+        mp.setenv("AIRSCHED_GRID", "1")
+        _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+        mp.setenv("AIRSCHED_GRID_T_GLOBAL", "1")   # row-local reads of the global table (TR)
+        _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+        _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    with monkeypatch.context() as mp:
+        mp.setenv("AIRSCHED_SHARDED", "1")
+        mp.setenv("AIRSCHED_SHARD_EMULATE", "3")
+        _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+    R = 40
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    prm = A.params(mode=1, tenure=c.tenure, max_iters=iters, kick=c.kick or 4)
+    A.as_batch_run(ctx, h, R, p, m, prm, seeds, shared_start=True, results=res)
+    for r in (0, R - 1):
+        o = O.search(p, m, mode=1, tenure=c.tenure, max_iters=iters, seed=int(seeds[r]), kick=c.kick or 4)
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == o["iters_done"]
+        assert res[r]["best_iter"] == o["best_iter"]
+    d, f, key = A.as_eval_moves(ctx, h, p, m, mode=0)
+    od, of, ok = O.eval_moves(p, m, mode=0)
+    assert (d == od).all() and (f == of).all()
