@@ -716,10 +716,21 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     if ((st = scratch(ctx, "g_E", (size_t)n * V * 4 + 4, &p)) != AS_OK) return st;
                     GA.Eglobal = (int32_t *)p;
                 }
-                const int warps_all = grid_blocks * 24;
-                const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
-                const int64_t pairs = (int64_t)n * nTC + (int64_t)n * nSC / 2;
-                GA.G = (int)std::max<int64_t>(1, pairs / ((one_cta ? 1 : 4) * (int64_t)warps_all));
+                // rows per tile: the tiles go round-robin over the warps, so an iteration costs about
+                // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
+                // overhead), the larger G on ties.  A global table caps G at 8 so a row group's table rows
+                // (~3.4 KB per row at C5) stay L1-resident for the CTA (measured: DESIGN.md §7).
+                const int64_t warps_all = (int64_t)grid_blocks * 24;
+                const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
+                const int gmax = GA.T_smem ? 256 : 8;
+                double best_cost = 1e300;
+                GA.G = 1;
+                for (int g = 1; g <= gmax && g <= std::max(1, n); g++) {
+                    const int64_t tiles = (nTC + nSC) * ((n + g - 1) / g) + nAdj;
+                    const int64_t rounds = (tiles + warps_all - 1) / warps_all;
+                    const double cost = (double)rounds * g + 0.3 * (double)rounds;
+                    if (cost <= best_cost) { best_cost = cost; GA.G = g; }
+                }
                 GA.G = std::max(1, env_int("AIRSCHED_GRID_G", GA.G));
             }
         }
