@@ -46,6 +46,24 @@ __device__ __forceinline__ int madd(int a, int mul, int b) {   // a * mul + b
     return r;
 }
 
+// Shared-memory table read at a 32-bit shared-window byte address (the FAST
+// scorers fold the table base and the element size into their cached offsets,
+// so one integer add forms each address).
+template <class TT>
+__device__ __forceinline__ int lds_t(uint32_t addr);
+template <>
+__device__ __forceinline__ int lds_t<uint16_t>(uint32_t addr) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return (int)v;
+}
+template <>
+__device__ __forceinline__ int lds_t<int32_t>(uint32_t addr) {
+    int v;
+    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 template <class TT, class ET>
 struct ScoreCtx {
     const TT *Ts;          // [NC][NL][NLp] travel times
@@ -285,8 +303,9 @@ __device__ __forceinline__ void reloc_row_fast(const TT *Ts, const TT *Tt, const
     const int wm_neg = madd(w_m, neg, 0);
 #pragma unroll
     for (int k = 0; k < KR; k++) {
-        const int T1 = (int)(TR ? Tt : Ts)[madd(c_t1[k], one, rowP)];     // T_cb[endc t][pick m]
-        const int T2 = (int)Ts[madd(c_t2[k], one, rowD)];     // T_cb[del m][pick t]
+        // T_cb[endc t][pick m], T_cb[del m][pick t]; shared table: byte addresses (score_reloc_fast)
+        const int T1 = TR ? (int)Tt[madd(c_t1[k], one, rowP)] : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
+        const int T2 = TR ? (int)Ts[madd(c_t2[k], one, rowD)] : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
         const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));                 // d(c, m)
         const int ins = madd(x1, one, madd(T2, one, c_k[k]));
         const int delta = madd(rem, one, ins);
@@ -322,10 +341,12 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
     const int V = C.V, S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
     const int one = C.one, neg = C.neg;
     int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
+    // shared table (TR false): cached offsets are byte addresses in the shared window
+    const int tsm = TR ? 0 : (int)__cvta_generic_to_shared(Ts), tsz = TR ? 1 : (int)sizeof(TT);
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
-        int t1 = 0, t2 = 0, dw = 0, kk = 0, wsv = NEG, slk = 0, b = -1, cb = 0;
+        int t1 = tsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = -1, cb = 0;
         if (t < S) {
             const int4 rs = RS4[t];
             const int bb = (int16_t)((uint32_t)rs.w >> 16);
@@ -335,8 +356,8 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
                 b = bb;
                 cb = vc & 0xFF;
                 t1 = TR ? cb * NL * NLp + (rs.w & 0xFFFF)    // column endc(t) of Tt_cb (row pick_m per m)
-                        : (cb * NL + (rs.w & 0xFFFF)) * NLp; // row endc(t) of T_cb (column pick_m per m)
-                t2 = cb * NL * NLp + (cs.y & 0xFFFF);        // column pick(t) of T_cb (row del_m per m)
+                        : tsm + tsz * ((cb * NL + (rs.w & 0xFFFF)) * NLp); // row endc(t) of T_cb (column pick_m)
+                t2 = tsm + tsz * (cb * NL * NLp + (cs.y & 0xFFFF)); // column pick(t) of T_cb (row del_m per m)
                 dw = -rs.x;                                  // -dep(pred t)
                 kk = rs.z - rs.y;                            // svco(t) - inc(t)
                 wsv = cs.x - rs.z;                           // w(t) - svco(t)
@@ -362,7 +383,8 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
         const int Fa = F[a];
         const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
         const int intra_lim = P - Fa - rem;
-        const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : (cm.y & 0xFFFF), rowD = ((uint32_t)cm.y >> 16) * NLp;
+        const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : tsz * (cm.y & 0xFFFF),
+                  rowD = tsz * (int)((uint32_t)cm.y >> 16) * NLp;
         const ET *Erow = TABU ? E + m * V : nullptr;
         const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
         if (MH[m])
@@ -394,10 +416,12 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
     int q_p2m[KS], q_sv0[KS], q_dsv[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS],
         q_slk[KS], q_bf[KS];
     int q_cb[KS];
+    // shared table (TR false): offsets are byte addresses in the shared window, the base on one side of each pair
+    const int tsm = TR ? 0 : (int)__cvta_generic_to_shared(Ts), tsz = TR ? 1 : (int)sizeof(TT);
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
-        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = 0, p2 = 0, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
+        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = tsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
             bf = -1, cb = 0;
         if (m2 >= 0) {
             const int4 r2 = RS4[m2];
@@ -409,14 +433,14 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 const int s2 = LK[m2] & 0xFFFF;
                 const int4 rs2 = RS4[s2];
                 const int4 cs2 = CS4[s2];
-                p2m = c2.y & 0xFFFF;                              // pick2
+                p2m = tsz * (c2.y & 0xFFFF);                      // pick2
                 sv0 = c2.z;
                 dsv = c2.w - c2.z;
                 d2 = TR ? (int)((uint32_t)c2.y >> 16)              // column del2 of Tt (row pick(s1) per m1)
-                        : (int)((uint32_t)c2.y >> 16) * NLp;       // row del2 of T (column pick(s1) per m1)
+                        : tsz * (int)((uint32_t)c2.y >> 16) * NLp; // row del2 of T (column pick(s1) per m1)
                 e2 = TR ? cb * NL * NLp + (r2.w & 0xFFFF)          // column endc2 of Tt_cb (row pick1 per m1)
-                        : (cb * NL + (r2.w & 0xFFFF)) * NLp;       // row endc2 of T_cb (column pick1 per m1)
-                p2 = cb * NL * NLp + (cs2.y & 0xFFFF);            // column pick(s2) of T_cb
+                        : tsm + tsz * ((cb * NL + (r2.w & 0xFFFF)) * NLp); // row endc2 of T_cb (column pick1)
+                p2 = tsm + tsz * (cb * NL * NLp + (cs2.y & 0xFFFF)); // column pick(s2) of T_cb
                 w2 = c2.x;
                 dep2 = r2.x;
                 kb = rs2.z - r2.y - rs2.y;                        // svco(s2) - inc2 - inc(s2)
@@ -439,10 +463,11 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
         const int4 cs1 = CS4[s1];
         const uint32_t vca = VC[a];
         const int ca = vca & 0xFF;
-        const int row_ya1 = (ca * NL + (r1.w & 0xFFFF)) * NLp;  // T_ca[endc1][.]
-        const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp   // Tt_ca[pick(s1)][.]
-                               : ca * NL * NLp + (cs1.y & 0xFFFF);    // T_ca[.][pick(s1)]
-        const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : (c1.y & 0xFFFF), row_tb2 = ((uint32_t)c1.y >> 16) * NLp;
+        const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * NLp);  // T_ca[endc1][.]
+        const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp            // Tt_ca[pick(s1)][.]
+                               : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF)); // T_ca[.][pick(s1)]
+        const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : tsz * (c1.y & 0xFFFF);
+        const int row_tb2 = tsz * (int)((uint32_t)c1.y >> 16) * NLp;
         const int ndepc1 = -r1.x, w1 = c1.x, nw1 = -c1.x;
         const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
         const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
@@ -459,10 +484,14 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
             const int m2 = lo + lane + 32 * k;
             const int bf = q_bf[k];
             const int b = (int)(int16_t)(bf & 0xFFFF);
-            const int ya1 = madd(q_dsv[k], ca, madd((int)Ts[madd(row_ya1, one, q_p2m[k])], one, q_sv0[k]));  // p1 -> m2
-            const int Ta2 = (int)(TR ? Tt : Ts)[madd(row_ta2, one, q_d2[k])];                                // m2 -> s1
-            const int yb1 = madd(q_cb[k], dsv1, madd((int)(TR ? Tt : Ts)[madd(q_e2[k], one, rowp1)], one, sv10));  // p2 -> m1
-            const int Tb2 = (int)Ts[madd(q_p2[k], one, row_tb2)];                                       // m1 -> s2
+            const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
+            const int a_yb1 = madd(q_e2[k], one, rowp1), a_tb2 = madd(q_p2[k], one, row_tb2);
+            const int Tya1 = TR ? (int)Ts[a_ya1] : lds_t<TT>((uint32_t)a_ya1);
+            const int Ta2 = TR ? (int)Tt[a_ta2] : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
+            const int Tyb1 = TR ? (int)Tt[a_yb1] : lds_t<TT>((uint32_t)a_yb1);
+            const int Tb2 = TR ? (int)Ts[a_tb2] : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
+            const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));                    // p1 -> m2
+            const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                       // p2 -> m1
             const int da = madd(ya1, one, madd(Ta2, one, ka));
             const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
             const int delta = madd(da, one, db);
