@@ -720,7 +720,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
                 // overhead), the larger G on ties.  A global table caps G at 8 so a row group's table rows
                 // (~3.4 KB per row at C5) stay L1-resident for the CTA (measured: DESIGN.md §7).
-                const int64_t warps_all = (int64_t)grid_blocks * 24;
+                const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS;
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
                 const int gmax = GA.T_smem ? 256 : 8;
                 double best_cost = 1e300;
@@ -742,7 +742,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_grid) {
-        CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, 768, grid_smem, ctx->stream));
+        CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, GRID_WARPS * 32, grid_smem,
+                             ctx->stream));
         ctx->launches += A.best_ptr ? 2 : 1;
         ctx->launches--;   // counted once below
     } else if (use_batch) {

@@ -27,7 +27,7 @@
 
 namespace cg = cooperative_groups;
 
-constexpr int GRID_THREADS = 768;   // 24 warps per SM: ~85 registers per thread
+constexpr int GRID_THREADS = airsched::GRID_WARPS * 32;
 
 namespace airsched {
 

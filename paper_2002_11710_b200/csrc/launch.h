@@ -37,6 +37,8 @@ struct SearchArgs {
     int32_t *tabu_out;                     // [R][n][V]
 };
 
+constexpr int GRID_WARPS = 24;   // k_grid warps per CTA (one CTA per SM; <= 85 registers per thread; 28 measured slower)
+
 struct GridLayout {
     int T, CS, MH, VC, CH, RS, LK, F, E, red, total;   // shared-memory byte offsets per CTA
 };
