@@ -267,14 +267,15 @@ def run_gpu(args):
     h2d = p.nbytes + m.nbytes + seeds_np.nbytes
     d2h = R * 40
 
-    # ---- roofline of the dominant kernel (k_search = the whole step)
+    # ---- roofline of the dominant kernel (k_batch: the step is k_batch + the tiny k_batch_best)
     ops = (inst.n_missions * (inst.n_missions + inst.n_vehicles - 2) * OPS_RELOCATE +
            inst.n_missions * (inst.n_missions - 1) // 2 * OPS_SWAP)
     f_mhz = clocks.get("sm_mhz") or 1965.0
     peak_gops = 148 * 128 * f_mhz * 1e6 / 1e9
     achieved_gops = (iters_total * ops) / (t_ms / 1e3) / 1e9 if world == 1 else (iters_all * ops) / (t_ms / 1e3) / world / 1e9
     roof = {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
-            "frac": achieved_gops / peak_gops, "traffic": args.traffic,
+            "frac": achieved_gops / peak_gops, "traffic": args.traffic if args.traffic is not None else
+            measured_traffic(args.workload),
             "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"}
 
     if rank != 0:
@@ -307,6 +308,18 @@ def run_gpu(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def measured_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/r01/traffic.json); None when that workload was not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(workload)
+        return None if rec is None else float(rec["bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def run_single(args):
