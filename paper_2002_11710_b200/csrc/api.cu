@@ -681,7 +681,12 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     if (single && compact_ok && !P->sweep) {
         const int want_grid = env_int("AIRSCHED_GRID", -1);
         const bool kfits = kfit;
-        const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000);
+        // CTAs: one per single-row tile up to the SM count (an iteration's floor is one tile's
+        // latency + the grid barrier + the apply; an SM scoring many tiles at once is issue-bound,
+        // DESIGN.md §7); ONE CTA (no grid barrier) when one CTA's warps take every tile
+        const int64_t tiles1 = (int64_t)((S + 127) / 128 + (n > 1 ? (n - 1 + 63) / 64 : 0)) * n + (n + 31) / 32;
+        const int need_blocks = (int)std::min<int64_t>(ctx->n_sm, tiles1);   // tiles spread one per CTA first
+        const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000) || tiles1 > GRID_WARPS;
         // small single runs: the same kernel on ONE CTA (no grid barrier)
         const bool one_cta = !big && kfits && want_grid != 1 && env_int("AIRSCHED_ONE_CTA", 1) == 1;
         if (want_grid == 1 || one_cta || (want_grid == -1 && (big || !kfits))) {
@@ -704,7 +709,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;
-                grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS", ctx->n_sm)));
+                grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS",
+                                                                                      want_grid == 1 ? ctx->n_sm : need_blocks)));
                 GA.Tglobal = D.Tpad;
                 void *p;
                 if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;

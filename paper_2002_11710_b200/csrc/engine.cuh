@@ -378,72 +378,121 @@ __device__ __forceinline__ MoveEval eval_index(const MV &M, const RV &R, uint32_
     return swap_eval<NW>(M, R, m1, m2, mask, it);
 }
 
-// Apply a VALID move whose per-route deltas are in e (single thread).
-// Relinks the lists, refreshes the incoming-link records of the touched slots,
-// updates route flight totals and the tabu expiry of the 'from' pairs (O8).
-template <bool NW = false, class MV, class RV>
-__device__ inline void apply_move(const MV &M, const RV &R, uint32_t idx, const MoveEval &e, int it, int tenure,
-                                  bool write_tabu) {
+// Per-route split of a VALID move's delta (read BEFORE the move is applied):
+// a, b = the routes of m (m1) and t (m2); da, db = their flight-time changes
+// (db = 0 when a == b).  The scorers already proved validity and feasibility, so
+// only the removal side (relocate) or route a's two new links (swap) are needed.
+struct MoveSplit {
+    int a, b;
+    int32_t da, db;
+};
+
+template <class MV, class RV>
+__device__ __forceinline__ MoveSplit move_split(const MV &M, const RV &R, uint32_t idx, int32_t delta) {
     const int n = M.n, S = M.n + M.V;
-    uint32_t Rb = (uint32_t)n * (uint32_t)S;
+    const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+    MoveSplit r;
     if (idx < Rb) {
-        int m = idx / S, t = idx % S;
-        int a = R.veh[m];
-        int b = R.veh[t];
-        int p = R.pred[m], s = R.succ[m];
+        const int m = idx / S, t = idx % S;
+        r.a = R.veh[m];
+        r.b = R.veh[t];
+        if (r.a == r.b) { r.da = delta; r.db = 0; return r; }
+        const int s = R.succ[m];
+        const int Dps = Tget(M, M.cls(r.a), R.endc[m], R.pick_s[s]) + R.svco[s];
+        r.da = Dps - R.inc[m] - R.inc[s];
+        r.db = delta - r.da;
+        return r;
+    }
+    const uint32_t k = idx - Rb;
+    const int m1 = k / n, m2 = k % n;
+    r.a = R.veh[m1];
+    r.b = R.veh[m2];
+    const int s1 = R.succ[m1];
+    if (r.a == r.b) { r.da = delta; r.db = 0; return r; }   // (adjacent pairs share a route)
+    const int ca = M.cls(r.a);
+    const int ya1 = Tget(M, ca, R.endc[m1], R.pick_s[m2]) + M.sv(ca, m2);
+    const int ya2 = Tget(M, ca, M.dl(m2), R.pick_s[s1]) + R.svco[s1];
+    r.da = ya1 + ya2 - R.inc[m1] - R.inc[s1];
+    r.db = delta - r.da;
+    return r;
+}
+
+// Relink the lists for a VALID move (pre-move routes a, b from move_split) and
+// list the slots whose incoming-link record must be refreshed (<= 4).  Route
+// totals and records are the caller's.
+template <class MV, class RV>
+__device__ __forceinline__ int move_relink(const MV &M, const RV &R, uint32_t idx, int a, int b, int *touched) {
+    const int n = M.n, S = M.n + M.V;
+    const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+    if (idx < Rb) {
+        const int m = idx / S, t = idx % S;
+        const int p = R.pred[m], s = R.succ[m];
         R.succ[p] = s;
         R.pred[s] = p;
-        int c = R.pred[t];
+        const int c = R.pred[t];
         R.succ[c] = m;
         R.pred[m] = c;
         R.succ[m] = t;
         R.pred[t] = m;
         R.veh[m] = b;
-        if constexpr (NW) {
-            nw_refresh_route(M, R, a);
-            if (b != a) nw_refresh_route(M, R, b);
-        } else {
-            refresh_slot(M, R, s);
-            refresh_slot(M, R, m);
-            refresh_slot(M, R, t);
-        }
-        if (a == b) R.F[a] += e.delta;
-        else { R.F[a] += e.da; R.F[b] += e.db; }
-        if (write_tabu && R.E) R.E[m * M.V + a] = it + tenure;
-    } else {
-        uint32_t k = idx - Rb;
-        int m1 = k / n, m2 = k % n;
-        int a = R.veh[m1], b = R.veh[m2];
-        int p1 = R.pred[m1], s1 = R.succ[m1], p2 = R.pred[m2], s2 = R.succ[m2];
-        if (s1 == m2) {          // p1 m1 m2 s2 -> p1 m2 m1 s2
-            R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = m1; R.pred[m1] = m2; R.succ[m1] = s2; R.pred[s2] = m1;
-            if constexpr (NW) nw_refresh_route(M, R, a);
-            else { refresh_slot(M, R, m2); refresh_slot(M, R, m1); refresh_slot(M, R, s2); }
-            R.F[a] += e.delta;
-        } else if (s2 == m1) {   // p2 m2 m1 s1 -> p2 m1 m2 s1
-            R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = m2; R.pred[m2] = m1; R.succ[m2] = s1; R.pred[s1] = m2;
-            if constexpr (NW) nw_refresh_route(M, R, a);
-            else { refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1); }
-            R.F[a] += e.delta;
-        } else {
-            R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = s1; R.pred[s1] = m2;
-            R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = s2; R.pred[s2] = m1;
-            R.veh[m1] = b;
-            R.veh[m2] = a;
-            if constexpr (NW) {
-                nw_refresh_route(M, R, a);
-                if (b != a) nw_refresh_route(M, R, b);
-            } else {
-                refresh_slot(M, R, m1); refresh_slot(M, R, m2); refresh_slot(M, R, s1); refresh_slot(M, R, s2);
-            }
-            if (a == b) R.F[a] += e.delta;
-            else { R.F[a] += e.da; R.F[b] += e.db; }
-        }
-        if (write_tabu && R.E) {
-            R.E[m1 * M.V + a] = it + tenure;
-            R.E[m2 * M.V + b] = it + tenure;
-        }
+        touched[0] = s; touched[1] = m; touched[2] = t;
+        return 3;
     }
+    const uint32_t k = idx - Rb;
+    const int m1 = k / n, m2 = k % n;
+    const int p1 = R.pred[m1], s1 = R.succ[m1], p2 = R.pred[m2], s2 = R.succ[m2];
+    if (s1 == m2) {          // p1 m1 m2 s2 -> p1 m2 m1 s2
+        R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = m1; R.pred[m1] = m2; R.succ[m1] = s2; R.pred[s2] = m1;
+        touched[0] = m2; touched[1] = m1; touched[2] = s2;
+        return 3;
+    }
+    if (s2 == m1) {          // p2 m2 m1 s1 -> p2 m1 m2 s1
+        R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = m2; R.pred[m2] = m1; R.succ[m2] = s1; R.pred[s1] = m2;
+        touched[0] = m1; touched[1] = m2; touched[2] = s1;
+        return 3;
+    }
+    R.succ[p1] = m2; R.pred[m2] = p1; R.succ[m2] = s1; R.pred[s1] = m2;
+    R.succ[p2] = m1; R.pred[m1] = p2; R.succ[m1] = s2; R.pred[s2] = m1;
+    R.veh[m1] = b;
+    R.veh[m2] = a;
+    touched[0] = m1; touched[1] = m2; touched[2] = s1; touched[3] = s2;
+    return 4;
+}
+
+// Route totals (con6) and the tabu expiry of the 'from' pairs (O8) after a move.
+template <class MV, class RV>
+__device__ __forceinline__ void move_totals(const MV &M, const RV &R, uint32_t idx, const MoveSplit &ms, int it,
+                                            int tenure, bool write_tabu) {
+    R.F[ms.a] += ms.da;
+    if (ms.b != ms.a) R.F[ms.b] += ms.db;
+    if (!(write_tabu && R.E)) return;
+    const int n = M.n, S = M.n + M.V;
+    const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+    if (idx < Rb) {
+        R.E[(idx / S) * M.V + ms.a] = it + tenure;
+    } else {
+        const uint32_t k = idx - Rb;
+        R.E[(k / n) * M.V + ms.a] = it + tenure;
+        R.E[(k % n) * M.V + ms.b] = it + tenure;
+    }
+}
+
+// Apply a VALID move whose delta is e.delta (single thread): split, relink,
+// refresh the touched incoming-link records (no-wait: recompute the touched
+// routes), route totals, tabu expiries.
+template <bool NW = false, class MV, class RV>
+__device__ inline void apply_move(const MV &M, const RV &R, uint32_t idx, const MoveEval &e, int it, int tenure,
+                                  bool write_tabu) {
+    const MoveSplit ms = move_split(M, R, idx, e.delta);
+    int touched[4];
+    const int nt = move_relink(M, R, idx, ms.a, ms.b, touched);
+    if constexpr (NW) {
+        nw_refresh_route(M, R, ms.a);
+        if (ms.b != ms.a) nw_refresh_route(M, R, ms.b);
+    } else {
+        for (int q = 0; q < nt; q++) refresh_slot(M, R, touched[q]);
+    }
+    move_totals(M, R, idx, ms, it, tenure, write_tabu);
 }
 
 __host__ __device__ __forceinline__ uint64_t splitmix64_next(uint64_t &s) {

@@ -54,6 +54,10 @@ size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, boo
     return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
 }
 
+__device__ __forceinline__ bool GT_spread(int n, int V, int G, int nwarps_all) {
+    return grid_tiles(n, V, G).n_total < nwarps_all;
+}
+
 // TR: the table is read from global memory (row-local reads, score.cuh).
 template <bool TABU, class TT, class ET, bool FULL, bool TR>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
@@ -178,7 +182,11 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
     const GridTiles GT = grid_tiles(n, V, GA.G);
-    const int gwarp = blockIdx.x * nwarps + warp, nwarps_all = gridDim.x * nwarps;
+    // tile -> warp: CTA-major (consecutive tiles = the same row group on one CTA: the table rows
+    // of that group are shared in L1) when the tiles fill the grid; spread over the CTAs first when
+    // there are fewer tiles than warps, so every SM scores at most ~one tile (latency-bound sizes)
+    const int nwarps_all = gridDim.x * nwarps;
+    const int gwarp = GT_spread(n, V, GA.G, nwarps_all) ? warp * gridDim.x + blockIdx.x : blockIdx.x * nwarps + warp;
     const bool one = gridDim.x == 1;
     unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
 
@@ -199,35 +207,46 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             }
         }
         if (!one) grid.sync();   // a single CTA (small instances) needs no grid barrier
-        if (tid == 0) {
-            const uint64_t k = one ? kcta : __ldcg(&gkey[it % 3]);
-            int stop = 0;
-            if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
-            else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
-            ctrl[0] = stop;
-            ctrl[1] = 0;
-            if (!stop) {
-                const uint32_t idx = key_idx(k);
-                MoveEval e = eval_index(M, R, idx, A.mask, it);
-                apply_move(M, R, idx, e, it, A.tenure, TABU);
-                const long long c = s_cur + e.delta;
-                s_cur = c;
-                if (c < s_best) {
-                    s_best = c;
-                    s_best_it = it;
-                    ctrl[1] = 1;
-                }
-                if (blockIdx.x == 0 && A.trace) {
-                    as_trace_rec tr;
-                    tr.cur = c;
-                    tr.best = s_best;
-                    tr.idx = idx;
-                    tr.delta = e.delta;
-                    tr.cls = key_cls(k);
-                    tr.it = it;
-                    A.trace[it] = tr;
+        if (warp == 0) {
+            // apply (every CTA, identical arithmetic): lane 0 splits the delta (from the key: the
+            // scorers proved the move valid and feasible), relinks and updates the route totals and
+            // the tabu matrix; the touched incoming-link records are then refreshed one per lane
+            int nt = 0;
+            if (lane == 0) {
+                const uint64_t k = one ? kcta : __ldcg(&gkey[it % 3]);
+                int stop = 0;
+                if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
+                else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
+                ctrl[0] = stop;
+                ctrl[1] = 0;
+                if (!stop) {
+                    const uint32_t idx = key_idx(k);
+                    const int32_t delta = key_delta(k);
+                    const MoveSplit ms = move_split(M, R, idx, delta);
+                    nt = move_relink(M, R, idx, ms.a, ms.b, ctrl + 4);
+                    move_totals(M, R, idx, ms, it, A.tenure, TABU);
+                    const long long c = s_cur + delta;
+                    s_cur = c;
+                    if (c < s_best) {
+                        s_best = c;
+                        s_best_it = it;
+                        ctrl[1] = 1;
+                    }
+                    if (blockIdx.x == 0 && A.trace) {
+                        as_trace_rec tr;
+                        tr.cur = c;
+                        tr.best = s_best;
+                        tr.idx = idx;
+                        tr.delta = delta;
+                        tr.cls = key_cls(k);
+                        tr.it = it;
+                        A.trace[it] = tr;
+                    }
                 }
             }
+            nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
+            __syncwarp();
+            if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
         }
         __syncthreads();
         if (ctrl[0]) break;
