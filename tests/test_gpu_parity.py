@@ -459,6 +459,7 @@ def test_per_cta_kernel_still_exact(A, ctx, oracle_mod, monkeypatch):
     """k_search (one run per CTA, int32 layout) -- the path for tabu digests and
     for instances outside the compact layout -- forced for a plain run."""
     monkeypatch.setenv("AIRSCHED_ONE_CTA", "0")
+    monkeypatch.setenv("AIRSCHED_GRID", "0")
     inst = instgen.generate("ontario")
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
