@@ -237,6 +237,31 @@ as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, int3
                        int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out,
                        int64_t *best_run_out);
 
+/* Several instances in one launch ("independent multi-start runs or instances",
+ * BASELINE north_star): job j runs jobs[j].n_runs independent runs of
+ * jobs[j].inst from jobs[j]'s start (host or device CSR), all with *params; the
+ * runs are numbered job after job (run = sum of the earlier jobs' n_runs + r)
+ * and seeds / results / trace are indexed by that number.  Each CTA of the
+ * batched kernel stages the instance of the job it serves, so many small
+ * instances fill the GPU together.  Every instance must fit the compact layout
+ * (NL and n+V < 65536, <= 2 classes, waiting model), else AS_ERR_UNSUPPORTED.
+ * best_ptr_out / best_missions_out (nullable): the runs' best schedules packed
+ * job after job ([n_runs][V_j+1] and [n_runs][n_j] per job).  best_run_out: the
+ * run with the smallest (best objective, run number), over every rank with a
+ * communicator (run numbers then offset by rank x total runs). */
+typedef struct {
+    const as_instance *inst;
+    const int32_t *start_ptr;       /* [V+1] */
+    const int32_t *start_missions;  /* [n] */
+    int32_t n_runs;                 /* >= 1 */
+    int32_t reserved;               /* 0 */
+} as_job;
+
+as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_jobs, const as_job *jobs,
+                            const as_run_params *params, const uint64_t *seeds, as_run_result *results,
+                            int32_t *best_ptr_out, int32_t *best_missions_out, as_trace_rec *trace_out,
+                            int64_t *best_run_out);
+
 /* ------------------------------------------------------------- multi-GPU --
  * One process per GPU.  Rank 0 creates a 128-byte NCCL unique id, the caller
  * shares it (e.g. through torch.distributed), every rank calls as_comm_init on

@@ -29,7 +29,7 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
            "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
-           "as_init_greedy_batch"]
+           "as_init_greedy_batch", "as_batch_run_jobs"]
 
 
 class AirschedError(RuntimeError):
@@ -51,6 +51,11 @@ class as_run_params(C.Structure):
     _fields_ = [("mode", C.c_int32), ("tenure", C.c_int32), ("max_iters", C.c_int32), ("kick", C.c_int32),
                 ("move_mask", C.c_uint32), ("strict_tabu_stop", C.c_int32), ("trace_level", C.c_int32),
                 ("seed", C.c_uint64), ("sweep", C.c_int32), ("reserved", C.c_int32)]
+
+
+class as_job(C.Structure):
+    _fields_ = [("inst", C.c_void_p), ("start_ptr", C.c_void_p), ("start_missions", C.c_void_p),
+                ("n_runs", C.c_int32), ("reserved", C.c_int32)]
 
 
 class as_run_result(C.Structure):
@@ -84,6 +89,7 @@ def _load():
         "as_instance_upload": (i32, [vp, vp]),
         "as_init_greedy": (i32, [vp, vp, i32, i32, vp, vp, vp]),
         "as_init_greedy_batch": (i32, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "as_batch_run_jobs": (i32, [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
         "as_eval_moves": (i32, [vp, vp, vp, vp, i32, vp, i32, i64, u32, vp, vp, vp]),
         "as_tabu_run": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "as_nbhd_run": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -332,6 +338,27 @@ def as_tabu_run(ctx, inst, route_ptr, route_missions, prm, **kw):
 
 def as_nbhd_run(ctx, inst, route_ptr, route_missions, prm, **kw):
     return _run(lib.as_nbhd_run, ctx, inst, route_ptr, route_missions, prm, **kw)
+
+
+def as_batch_run_jobs(ctx, jobs, prm, seeds=None, results=None, best_ptr_out=None, best_missions_out=None,
+                      trace_out=None, want_best_run=False, comm=None):
+    """Marshalling for as_batch_run_jobs.  jobs: list of (Instance, start_ptr, start_missions, n_runs);
+    runs are numbered job after job.  Returns the best run's number (or -1) when want_best_run."""
+    keep = []
+    arr = (as_job * len(jobs))()
+    for j, (inst, sp, sm, nr) in enumerate(jobs):
+        if isinstance(sp, np.ndarray):
+            sp = np.ascontiguousarray(sp, np.int32)
+            sm = np.ascontiguousarray(sm, np.int32)
+        keep.append((sp, sm))
+        arr[j] = as_job(inst.handle, _ptr(sp), _ptr(sm), int(nr), 0)
+    if isinstance(seeds, np.ndarray):
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+    best_run = C.c_int64(-1)
+    _check(lib.as_batch_run_jobs(ctx.handle, comm.handle if comm is not None else None, len(jobs), arr, C.byref(prm),
+                                 _ptr(seeds), _ptr(results), _ptr(best_ptr_out), _ptr(best_missions_out),
+                                 _ptr(trace_out), C.byref(best_run) if want_best_run else None))
+    return int(best_run.value)
 
 
 def as_batch_gather_best(ctx, inst, n_runs, run_best_ptr=None, run_best_ms=None, comm=None):

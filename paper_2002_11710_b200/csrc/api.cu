@@ -856,6 +856,142 @@ extern "C" as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance 
     return AS_OK;
 }
 
+extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_jobs, const as_job *jobs,
+                                       const as_run_params *P, const uint64_t *seeds, as_run_result *results,
+                                       int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace,
+                                       int64_t *best_run_out) {
+    if (!ctx || !jobs || !P || n_jobs < 1) return fail(AS_ERR_INVALID_ARG, "null argument or no jobs");
+    if (P->mode != AS_MODE_NS && P->mode != AS_MODE_TABU) return fail(AS_ERR_INVALID_ARG, "mode must be NS or TABU");
+    if (P->max_iters < 0 || P->tenure < 0 || P->kick < 0) return fail(AS_ERR_INVALID_ARG, "negative parameter");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    const bool tabu = P->mode == AS_MODE_TABU;
+    int64_t total = 0, bp_total = 0, bm_total = 0;
+    int tbytes = 2;
+    bool all_svcpos = true;
+    for (int j = 0; j < n_jobs; j++) {
+        const as_instance *I = jobs[j].inst;
+        if (!I || !jobs[j].start_ptr || jobs[j].n_runs < 1) return fail(AS_ERR_INVALID_ARG, "job %d: null instance/start or n_runs < 1", j);
+        if (I->NL > 65535 || I->n + I->V > 65535 || I->V > 32767 || I->NC > 2 || I->no_wait)
+            return fail(AS_ERR_UNSUPPORTED, "job %d: the multi-instance batch needs the compact layout (NL, n+V < 65536, <= 2 classes, waiting model)", j);
+        if (I->maxT > 65535) tbytes = 4;
+        total += jobs[j].n_runs;
+        bp_total += (int64_t)jobs[j].n_runs * (I->V + 1);
+        bm_total += (int64_t)jobs[j].n_runs * I->n;
+    }
+    if (total >= (1ll << 31)) return fail(AS_ERR_INVALID_ARG, "too many runs");
+    const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
+    // per-job device instance, layout, runs per CTA, packed start
+    std::vector<BatchJob> J(n_jobs);
+    std::vector<int4> cta;
+    size_t smem = 0;
+    int threads = 32;
+    std::vector<int32_t> packed;           // host starts, uploaded once
+    std::vector<std::pair<int64_t, int64_t>> poff(n_jobs, {-1, -1});
+    int64_t run0 = 0, bp0 = 0, bm0 = 0;
+    for (int j = 0; j < n_jobs; j++) {
+        const as_instance *I = jobs[j].inst;
+        const DevInst *D;
+        if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
+        if (!D->svcpos) all_svcpos = false;
+        BatchJob &b = J[j];
+        b.inst = *D;
+        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu);
+        b.NLp = padded_stride_host(I->NL, tbytes);
+        if ((size_t)b.L.shared_bytes + b.L.run_bytes > ctx->max_smem)
+            return fail(AS_ERR_UNSUPPORTED, "job %d: instance too large for the batched kernel", j);
+        const int fit = (int)((ctx->max_smem - b.L.shared_bytes) / b.L.run_bytes);
+        b.RPC = std::max(1, std::min({28, fit, jobs[j].n_runs}));
+        b.run0 = (int)run0;
+        b.bp_off = bp0;
+        b.bm_off = bm0;
+        if (is_device_ptr(jobs[j].start_ptr)) {
+            b.start_ptr = jobs[j].start_ptr;
+            b.start_ms = jobs[j].start_missions;
+        } else {
+            HostSched S;
+            if ((st = parse_csr(I, jobs[j].start_ptr, jobs[j].start_missions, false, S)) != AS_OK) return st;
+            poff[j].first = (int64_t)packed.size();
+            packed.insert(packed.end(), jobs[j].start_ptr, jobs[j].start_ptr + I->V + 1);
+            poff[j].second = (int64_t)packed.size();
+            if (I->n > 0) packed.insert(packed.end(), jobs[j].start_missions, jobs[j].start_missions + I->n);
+        }
+        for (int r = 0; r < jobs[j].n_runs; r += b.RPC) cta.push_back(make_int4(j, r, std::min(b.RPC, jobs[j].n_runs - r), 0));
+        smem = std::max(smem, (size_t)b.L.shared_bytes + (size_t)b.RPC * b.L.run_bytes);
+        threads = std::max(threads, b.RPC * 32);
+        run0 += jobs[j].n_runs;
+        bp0 += (int64_t)jobs[j].n_runs * (I->V + 1);
+        bm0 += (int64_t)jobs[j].n_runs * I->n;
+    }
+    if (!packed.empty()) {
+        const void *dp;
+        if ((st = dev_in(ctx, "jobs_starts", packed.data(), packed.size() * 4, &dp)) != AS_OK) return st;
+        for (int j = 0; j < n_jobs; j++)
+            if (poff[j].first >= 0) {
+                J[j].start_ptr = (const int32_t *)dp + poff[j].first;
+                J[j].start_ms = (const int32_t *)dp + poff[j].second;
+            }
+    }
+    const void *djobs, *dcta, *ds = nullptr;
+    if ((st = dev_in(ctx, "jobs_table", J.data(), J.size() * sizeof(BatchJob), &djobs)) != AS_OK) return st;
+    if ((st = dev_in(ctx, "jobs_cta", cta.data(), cta.size() * sizeof(int4), &dcta)) != AS_OK) return st;
+    if (seeds && (st = dev_in(ctx, "jobs_seeds", seeds, (size_t)total * 8, &ds)) != AS_OK) return st;
+    as_run_result *res = results;
+    if (!res || !is_device_ptr(res)) {
+        void *p;
+        if ((st = scratch(ctx, "jobs_res", (size_t)total * sizeof(as_run_result), &p)) != AS_OK) return st;
+        res = (as_run_result *)p;
+    }
+    OutBuf o_bp, o_bm, o_tr;
+    if (best_ptr && !best_ms && bm_total > 0) return fail(AS_ERR_INVALID_ARG, "best_ptr_out needs best_missions_out");
+    if ((st = dev_out(ctx, "jobs_bp", best_ptr, (size_t)bp_total * 4, o_bp)) != AS_OK) return st;
+    if ((st = dev_out(ctx, "jobs_bm", best_ptr ? best_ms : nullptr, std::max<size_t>((size_t)bm_total * 4, 4), o_bm)) != AS_OK) return st;
+    const bool want_trace = trace && P->trace_level >= 1 && P->max_iters > 0;
+    if ((st = dev_out(ctx, "jobs_tr", want_trace ? trace : nullptr, (size_t)total * P->max_iters * sizeof(as_trace_rec), o_tr)) != AS_OK) return st;
+    SearchArgs A;
+    memset(&A, 0, sizeof(A));
+    A.one = 1;
+    A.n_runs = (int32_t)total;
+    A.seeds = (const uint64_t *)ds;
+    A.seed = P->seed;
+    A.kick = P->kick;
+    A.tenure = P->tenure;
+    A.max_iters = P->max_iters;
+    A.strict_tabu_stop = P->strict_tabu_stop;
+    A.mask = P->sweep ? 1u : P->move_mask;
+    A.sweep = P->sweep ? 1 : 0;
+    A.results = res;
+    A.best_ptr = (int32_t *)o_bp.dev;
+    A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
+    A.trace = (as_trace_rec *)o_tr.dev;
+    const bool full = (A.mask & 15u) == 15u && all_svcpos;
+    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+    CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, (int)cta.size(), threads, smem,
+                               tabu ? 1 : 0, tbytes, ebytes, full, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->timed = true;
+    ctx->launches++;
+    void *kp;
+    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
+    const int64_t offset = comm ? (int64_t)comm->rank * total : 0;
+    CUDA_TRY(launch_batch_best(res, (int)total, offset, (unsigned long long *)kp, ctx->stream));
+    ctx->launches++;
+    if (comm && comm->nranks > 1)
+        NCCL_TRY(ncclAllReduce(kp, kp, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream));
+    ctx->batch_runs = -1;   // as_batch_gather_best is for single-instance batches
+    if (results && res != results)
+        CUDA_TRY(cudaMemcpyAsync(results, res, (size_t)total * sizeof(as_run_result), cudaMemcpyDeviceToHost, ctx->stream));
+    if ((st = finish_out(ctx, {&o_bp, &o_bm, &o_tr})) != AS_OK) return st;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (best_run_out) {
+        unsigned long long k;
+        CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        *best_run_out = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
+    }
+    return AS_OK;
+}
+
 extern "C" as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_runs, const int32_t *run_best_ptr,
                                           const int32_t *run_best_ms, int64_t *best_run_out, int64_t *best_obj_out,
                                           int32_t *ptr_out, int32_t *ms_out) {

@@ -30,13 +30,6 @@ namespace airsched {
 
 constexpr int MAXTHREADS = 896;    // <= 28 runs per CTA (one wave of 4096 runs on 148 SMs)
 
-struct BatchLayout {
-    int T, CS, MH, VC, CH;   // CTA-wide part
-    int shared_bytes;
-    int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
-    int run_bytes;
-};
-
 __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu) {
     BatchLayout L;
     const int S = n + V;
@@ -67,8 +60,11 @@ void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
     *run_bytes = L.run_bytes;
 }
 
+// One CTA of the batched executor: stage A.inst, then run this CTA's runs
+// cta_run0 .. cta_run0 + RPC - 1 (one per warp; A's per-run arrays are indexed by
+// that run number).
 template <bool TABU, class TT, class ET, bool FULL>
-__global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, BatchLayout L, int NLp) {
+__device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const BatchLayout &L, int NLp, int cta_run0) {
     extern __shared__ __align__(16) unsigned char smem[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC, NL = I.NL;
@@ -108,7 +104,7 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
     for (int i = tid; i < NC; i += blockDim.x) CH[i] = I.cls_heli[i];
     __syncthreads();
 
-    const int run = blockIdx.x * RPC + warp;
+    const int run = cta_run0 + warp;
     if (warp >= RPC || run >= A.n_runs) return;
 
     unsigned char *rb = smem + L.shared_bytes + warp * L.run_bytes;
@@ -408,6 +404,35 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, 
 }
 
 template <bool TABU, class TT, class ET, bool FULL>
+__global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, BatchLayout L, int NLp) {
+    batch_cta<TABU, TT, ET, FULL>(A, RPC, L, NLp, blockIdx.x * RPC);
+}
+
+// Several instances in one launch (as_batch_run_jobs): CTA b runs cta[b] = {job, first run
+// of the job, runs} with that job's instance staged in its shared memory; the per-run
+// output arrays are re-based to the CTA's first run.
+template <bool TABU, class TT, class ET, bool FULL>
+__global__ void __launch_bounds__(MAXTHREADS, 1) k_batch_jobs(SearchArgs A, const BatchJob *jobs, const int4 *cta) {
+    const int4 c = cta[blockIdx.x];
+    const BatchJob &J = jobs[c.x];
+    SearchArgs B = A;
+    const size_t r = (size_t)J.run0 + c.y;
+    B.inst = J.inst;
+    B.start_ptr = J.start_ptr;
+    B.start_ms = J.start_ms;
+    B.shared_start = 1;
+    B.n_runs = c.z;
+    B.seeds = A.seeds ? A.seeds + r : nullptr;
+    B.results = A.results ? A.results + r : nullptr;
+    B.best_ptr = A.best_ptr ? A.best_ptr + J.bp_off + (size_t)c.y * (J.inst.V + 1) : nullptr;
+    B.best_ms = A.best_ms ? A.best_ms + J.bm_off + (size_t)c.y * J.inst.n : nullptr;
+    B.trace = A.trace ? A.trace + r * (size_t)A.max_iters : nullptr;
+    B.digest = nullptr;
+    B.tabu_out = nullptr;
+    batch_cta<TABU, TT, ET, FULL>(B, J.RPC, J.L, J.NLp, 0);
+}
+
+template <bool TABU, class TT, class ET, bool FULL>
 static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStream_t st) {
     auto kern = k_batch<TABU, TT, ET, FULL>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -418,6 +443,36 @@ static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStr
     int grid = (A.n_runs + RPC - 1) / RPC;
     kern<<<grid, RPC * 32, smem, st>>>(A, RPC, L, NLp);
     return cudaGetLastError();
+}
+
+template <bool TABU, class TT, class ET, bool FULL>
+static cudaError_t launch_jobs_t(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
+                                 size_t smem, cudaStream_t st) {
+    auto kern = k_batch_jobs<TABU, TT, ET, FULL>;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    kern<<<n_cta, threads, smem, st>>>(A, jobs, cta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
+                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st) {
+    if (mode == 1) {
+        if (tbytes == 2 && ebytes == 2)
+            return full ? launch_jobs_t<true, uint16_t, int16_t, true>(A, jobs, cta, n_cta, threads, smem, st)
+                        : launch_jobs_t<true, uint16_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st);
+        if (tbytes == 2) return launch_jobs_t<true, uint16_t, int32_t, false>(A, jobs, cta, n_cta, threads, smem, st);
+        return ebytes == 2 ? launch_jobs_t<true, int32_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st)
+                           : launch_jobs_t<true, int32_t, int32_t, false>(A, jobs, cta, n_cta, threads, smem, st);
+    }
+    if (tbytes == 2)
+        return full ? launch_jobs_t<false, uint16_t, int16_t, true>(A, jobs, cta, n_cta, threads, smem, st)
+                    : launch_jobs_t<false, uint16_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st);
+    return launch_jobs_t<false, int32_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st);
+}
+
+BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu) {
+    return batch_layout(n, V, NL, NC, tbytes, ebytes, tabu);
 }
 
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,

@@ -39,6 +39,23 @@ struct SearchArgs {
 
 constexpr int GRID_WARPS = 24;   // k_grid warps per CTA (one CTA per SM; <= 85 registers per thread; 28 measured slower)
 
+struct BatchLayout {
+    int T, CS, MH, VC, CH;   // CTA-wide part
+    int shared_bytes;
+    int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
+    int run_bytes;
+};
+
+// One instance of a multi-instance batch (as_batch_run_jobs).
+struct BatchJob {
+    DevInst inst;
+    const int32_t *start_ptr, *start_ms;   // the job's start schedule (device)
+    BatchLayout L;
+    int NLp, RPC;                           // padded table stride, runs per CTA
+    int run0;                               // global index of the job's first run
+    int64_t bp_off, bm_off;                 // offsets of its runs' best schedules in the packed outputs
+};
+
 struct GridLayout {
     int T, CS, MH, VC, CH, RS, LK, F, E, red, total;   // shared-memory byte offsets per CTA
 };
@@ -96,6 +113,9 @@ cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
                 size_t *run_bytes);
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st);
+BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu);
+cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
+                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st);
 size_t greedy_smem_bytes(const DevInst &I, int warps, bool T_smem, bool state_smem);
 size_t greedy_state_bytes(const DevInst &I);
 cudaError_t launch_greedy(const DevInst &I, int n_starts, int insert_mode, int max_repairs, const uint64_t *seeds,

@@ -576,3 +576,71 @@ def test_asymmetric_table_parity(A, ctx, oracle_mod, cfg, iters, monkeypatch):
     d, f, key = A.as_eval_moves(ctx, h, p, m, mode=0)
     od, of, ok = O.eval_moves(p, m, mode=0)
     assert (d == od).all() and (f == of).all()
+
+
+def test_batch_run_jobs(A, ctx, oracle_mod):
+    """as_batch_run_jobs: several instances (different n, V, tables) in ONE launch, each CTA
+    staging its job's instance; sampled runs of every job against the oracle, packed best
+    schedules, traces, the best-run reduction, and the unsupported cases."""
+    import dataclasses
+    insts = [instgen.generate("tiny"), instgen.generate("ontario"), instgen.generate("batched"), _asymmetric("ontario", 9)]
+    cfg = instgen.Config("j", 30, 4, 2, 3, 2, 20, "ontario", 5, 10, 3)
+    insts += [instgen.generate(cfg, seed=s) for s in (1, 2)]
+    runs = [8, 20, 40, 5, 3, 30]
+    jobs, starts = [], []
+    for inst, nr in zip(insts, runs):
+        O = oracle_mod.Oracle(inst)
+        p, m = start_of(O, inst)
+        starts.append((O, p, m))
+        jobs.append((A.Instance(inst), p, m, nr))
+    total = sum(runs)
+    iters = 120
+    seeds = np.arange(101, 101 + total, dtype=np.uint64)
+    for mode in (1, 0):
+        prm = A.params(mode=mode, tenure=5, max_iters=iters, kick=3, trace_level=1)
+        res = np.zeros(total, A.RESULT_DTYPE)
+        bp = np.zeros(sum(nr * (inst.n_vehicles + 1) for inst, nr in zip(insts, runs)), np.int32)
+        bm = np.zeros(sum(nr * inst.n_missions for inst, nr in zip(insts, runs)), np.int32)
+        tr = np.zeros((total, iters), A.TRACE_DTYPE)
+        best = A.as_batch_run_jobs(ctx, jobs, prm, seeds, results=res, best_ptr_out=bp, best_missions_out=bm,
+                                   trace_out=tr, want_best_run=True)
+        assert best == int(np.lexsort((np.arange(total), res["best_obj"]))[0])
+        run0 = bpo = bmo = 0
+        for (O, p, m), inst, nr in zip(starts, insts, runs):
+            V, n = inst.n_vehicles, inst.n_missions
+            for r in sorted({0, nr - 1}):
+                g = run0 + r
+                o = O.search(p, m, mode=mode, tenure=5, max_iters=iters, seed=int(seeds[g]), kick=3)
+                assert res[g]["best_obj"] == o["best_obj"] and res[g]["iters_done"] == o["iters_done"]
+                assert res[g]["best_iter"] == o["best_iter"] and res[g]["kicks_applied"] == o["kicks_applied"]
+                assert (tr[g]["idx"][:o["iters_done"]] == o["trace"]["idx"]).all()
+                ptr = bp[bpo + r * (V + 1): bpo + (r + 1) * (V + 1)]
+                ms = bm[bmo + r * n: bmo + (r + 1) * n]
+                assert routes_of(ptr, ms) == routes_of(*o["best"])
+            run0 += nr
+            bpo += nr * (V + 1)
+            bmo += nr * n
+    # device-resident starts and results
+    import torch
+    dev = torch.device("cuda:0")
+    djobs = [(h, torch.from_numpy(p).to(dev), torch.from_numpy(m).to(dev), nr) for (h, p, m, nr) in jobs]
+    tres = torch.zeros((total, 40), dtype=torch.uint8, device=dev)
+    prm = A.params(mode=1, tenure=5, max_iters=iters, kick=3)
+    A.as_batch_run_jobs(ctx, djobs, prm, torch.from_numpy(seeds.view(np.int64)).to(dev), results=tres)
+    torch.cuda.synchronize()
+    res2 = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(total)
+    res1 = np.zeros(total, A.RESULT_DTYPE)
+    A.as_batch_run_jobs(ctx, jobs, prm, seeds, results=res1)
+    assert (res1 == res2).all()
+    # the same runs through the single-instance entry point
+    run0 = 0
+    for (h, p, m, nr) in jobs:
+        r3 = np.zeros(nr, A.RESULT_DTYPE)
+        A.as_batch_run(ctx, h, nr, p, m, prm, seeds[run0:run0 + nr], results=r3)
+        assert (r3 == res1[run0:run0 + nr]).all()
+        run0 += nr
+    # unsupported: the no-wait variant and > 2 classes
+    nw = dataclasses.replace(insts[1], no_wait=1)
+    with pytest.raises(A.AirschedError) as e:
+        A.as_batch_run_jobs(ctx, [(A.Instance(nw), starts[1][1], starts[1][2], 2)], prm)
+    assert e.value.status == A.AS_ERR_UNSUPPORTED
