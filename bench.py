@@ -310,6 +310,116 @@ def run_gpu(args):
     return 0
 
 
+def run_jobs(args):
+    """Multi-instance batch (`--workload instances`): 148 distinct C3-shaped instances
+    (20 vehicles / 100 missions, generator seeds C3 + 1..148) x 28 tabu runs each -- one
+    CTA per instance, one wave on 148 SMs -- one `as_batch_run_jobs` call per step (each
+    CTA stages the instance of its job).  Same metric as the default line; under
+    torchrun every rank runs its own 4144 runs."""
+    import torch
+    import torch.distributed as dist
+    from paper_2002_11710_b200 import airsched as A
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    base = instgen.CONFIGS["batched"]
+    n_inst = 148
+    per = max(1, (args.runs or 4144) // n_inst)
+    iters = args.iters or base.max_iters
+    insts = [instgen.generate(base, seed=2002117103 + 1 + i) for i in range(n_inst)]
+    stream = torch.cuda.current_stream(dev)
+    ctx = A.Ctx(local, stream.cuda_stream)
+    hs = [A.Instance(x) for x in insts]
+    jobs, djobs = [], []
+    for h, x in zip(hs, insts):
+        ctx.upload(h)
+        try:
+            p, m, _ = A.as_init_greedy(ctx, h, insert_mode=1)
+        except A.AirschedError:      # Alg. 1 can fail (P:166): the generator's planted schedule then
+            p, m = x.planted_ptr, x.planted_missions
+        jobs.append((h, p, m, per))
+        djobs.append((h, torch.from_numpy(p).to(dev), torch.from_numpy(m).to(dev), per))
+    R = n_inst * per
+    seeds_np = np.arange(1 + rank * R, 1 + (rank + 1) * R, dtype=np.uint64)
+    ts = torch.from_numpy(seeds_np.view(np.int64)).to(dev)
+    tres = torch.zeros((R, 40), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    prm = A.params(mode=A.AS_MODE_TABU, tenure=base.tenure, max_iters=iters, kick=base.kick)
+    comm = A.Comm.from_torch_distributed(ctx) if world > 1 else None
+
+    def step():
+        A.as_batch_run_jobs(ctx, djobs, prm, ts, results=tres, comm=comm)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.mark()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - launches0
+    res = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(R)
+    moves = sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) * valid_moves(insts[j]) for j in range(n_inst))
+    ops = sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) *
+              (insts[j].n_missions * (insts[j].n_missions + insts[j].n_vehicles - 2) * OPS_RELOCATE +
+               insts[j].n_missions * (insts[j].n_missions - 1) // 2 * OPS_SWAP) for j in range(n_inst))
+    t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if world > 1:
+        tt = torch.tensor([t_ms, 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt[0].item())
+    value = moves * args.steps * world / (t_ms / 1e3)
+    # e2e: host starts, seeds and results (the marshalling copies them inside the call)
+    hres = np.zeros(R, A.RESULT_DTYPE)
+    e2e_ms = []
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A.as_batch_run_jobs(ctx, jobs, prm, seeds_np, results=hres, comm=comm)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_moves = sum(int(hres["iters_done"][j * per:(j + 1) * per].sum()) * valid_moves(insts[j]) for j in range(n_inst))
+    f_mhz = clocks.get("sm_mhz") or 1965.0
+    peak = 148 * 128 * f_mhz * 1e6 / 1e9
+    ach = ops * args.steps / (t_ms / 1e3) / 1e9
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    h2d = sum(p.nbytes + m.nbytes for _, p, m, _ in jobs) + seeds_np.nbytes
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{n_inst} distinct 20-vehicle/100-mission instances x {per} tabu runs/GPU, "
+                                   f"{iters} iters, tenure {base.tenure}, kick {base.kick} (as_batch_run_jobs)",
+                       "runs_per_gpu": R, "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"runs sharded over {world} GPU(s)"},
+            "tabu_iters_per_s": int(res["iters_done"].sum()) * args.steps * world / (t_ms / 1e3),
+            "e2e": {"value": e2e_moves * world / (float(np.mean(e2e_ms)) / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(R * 40)},
+            "gpu_launches": int(launches), "clocks": clocks,
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gop/s", "frac": ach / peak,
+                         "traffic": None,
+                         "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"},
+            "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def measured_traffic(workload):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     capture (profiles/r01/traffic.json); None when that workload was not captured."""
@@ -406,6 +516,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "instances":
+        return run_jobs(args)
     if instgen.CONFIGS[args.workload].n_runs == 1:
         return run_single(args)
     return run_gpu(args)

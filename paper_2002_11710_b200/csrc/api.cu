@@ -868,7 +868,6 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     const bool tabu = P->mode == AS_MODE_TABU;
     int64_t total = 0, bp_total = 0, bm_total = 0;
     int tbytes = 2;
-    bool all_svcpos = true;
     for (int j = 0; j < n_jobs; j++) {
         const as_instance *I = jobs[j].inst;
         if (!I || !jobs[j].start_ptr || jobs[j].n_runs < 1) return fail(AS_ERR_INVALID_ARG, "job %d: null instance/start or n_runs < 1", j);
@@ -893,7 +892,6 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         const as_instance *I = jobs[j].inst;
         const DevInst *D;
         if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
-        if (!D->svcpos) all_svcpos = false;
         BatchJob &b = J[j];
         b.inst = *D;
         b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu);
@@ -901,7 +899,11 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         if ((size_t)b.L.shared_bytes + b.L.run_bytes > ctx->max_smem)
             return fail(AS_ERR_UNSUPPORTED, "job %d: instance too large for the batched kernel", j);
         const int fit = (int)((ctx->max_smem - b.L.shared_bytes) / b.L.run_bytes);
-        b.RPC = std::max(1, std::min({28, fit, jobs[j].n_runs}));
+        {   // runs per CTA: as few CTAs as fit (<= 28 runs each), the job's runs spread evenly over them
+            const int rmax = std::max(1, std::min(28, fit));
+            const int nct = (jobs[j].n_runs + rmax - 1) / rmax;
+            b.RPC = (jobs[j].n_runs + nct - 1) / nct;
+        }
         b.run0 = (int)run0;
         b.bp_off = bp0;
         b.bm_off = bm0;
@@ -916,7 +918,8 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
             poff[j].second = (int64_t)packed.size();
             if (I->n > 0) packed.insert(packed.end(), jobs[j].start_missions, jobs[j].start_missions + I->n);
         }
-        for (int r = 0; r < jobs[j].n_runs; r += b.RPC) cta.push_back(make_int4(j, r, std::min(b.RPC, jobs[j].n_runs - r), 0));
+        for (int r = 0; r < jobs[j].n_runs; r += b.RPC)
+            cta.push_back(make_int4(j, r, std::min(b.RPC, jobs[j].n_runs - r), D->svcpos ? 1 : 0));
         smem = std::max(smem, (size_t)b.L.shared_bytes + (size_t)b.RPC * b.L.run_bytes);
         threads = std::max(threads, b.RPC * 32);
         run0 += jobs[j].n_runs;
@@ -932,6 +935,12 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
                 J[j].start_ms = (const int32_t *)dp + poff[j].second;
             }
     }
+    // the FAST scorers need every pickup->delivery leg > 0 (svcpos): with every move kind enabled the
+    // CTAs of such jobs go first in one launch, the others in a second launch on a side stream
+    const bool all_moves = ((P->sweep ? 1u : P->move_mask) & 15u) == 15u;
+    std::stable_sort(cta.begin(), cta.end(), [&](const int4 &x, const int4 &y) { return (all_moves && x.w) > (all_moves && y.w); });
+    int n_fast = 0;
+    for (const int4 &c : cta) n_fast += all_moves && c.w;
     const void *djobs, *dcta, *ds = nullptr;
     if ((st = dev_in(ctx, "jobs_table", J.data(), J.size() * sizeof(BatchJob), &djobs)) != AS_OK) return st;
     if ((st = dev_in(ctx, "jobs_cta", cta.data(), cta.size() * sizeof(int4), &dcta)) != AS_OK) return st;
@@ -964,13 +973,30 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     A.best_ptr = (int32_t *)o_bp.dev;
     A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
     A.trace = (as_trace_rec *)o_tr.dev;
-    const bool full = (A.mask & 15u) == 15u && all_svcpos;
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, (int)cta.size(), threads, smem,
-                               tabu ? 1 : 0, tbytes, ebytes, full, ctx->stream));
+    const int n_gen = (int)cta.size() - n_fast;
+    if (n_gen > 0 && n_fast > 0) {   // fork the general-scorer CTAs onto the side stream
+        CUDA_TRY(cudaEventRecord(ctx->evj, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->cap, ctx->evj, 0));
+        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta + n_fast, n_gen, threads, smem,
+                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->cap));
+        ctx->launches++;
+    }
+    if (n_fast > 0) {
+        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_fast, threads, smem,
+                                   tabu ? 1 : 0, tbytes, ebytes, true, ctx->stream));
+        ctx->launches++;
+    } else {
+        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_gen, threads, smem,
+                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->stream));
+        ctx->launches++;
+    }
+    if (n_gen > 0 && n_fast > 0) {   // join
+        CUDA_TRY(cudaEventRecord(ctx->evj, ctx->cap));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evj, 0));
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
     ctx->timed = true;
-    ctx->launches++;
     void *kp;
     if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
     const int64_t offset = comm ? (int64_t)comm->rank * total : 0;
