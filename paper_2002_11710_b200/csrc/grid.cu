@@ -198,10 +198,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
         uint64_t kcta = KEY_NONE;
-        if (tid == 0) {
-            kcta = red[0];
-            for (int w2 = 1; w2 < nwarps; w2++) kcta = red[w2] < kcta ? red[w2] : kcta;
-            if (!one) {
+        if (warp == 0) {   // CTA minimum by one warp (parallel loads + shuffles, not a serial loop)
+            kcta = wmin(lane < nwarps ? red[lane] : KEY_NONE);
+            if (lane == 0 && !one) {
                 if (kcta != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)kcta);
                 if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
             }

@@ -385,9 +385,10 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
         kmin = warp_min_u64(kmin);
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
+        uint64_t kc = KEY_NONE;
+        if (warp == 0) kc = warp_min_u64(lane < nwarps ? red[lane] : KEY_NONE);   // CTA minimum by one warp
         if (tid == 0) {
-            uint64_t k = red[0];
-            for (int w2 = 1; w2 < nwarps; w2++) k = red[w2] < k ? red[w2] : k;
+            uint64_t k = kc;
             int stop = 0;
             if (k == KEY_NONE) stop = 2;                       // no feasible move
             else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? 2 : 1;

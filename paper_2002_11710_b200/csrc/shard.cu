@@ -159,10 +159,9 @@ __global__ void __launch_bounds__(768, 1) k_shard_eval(SearchArgs A, ShardViews 
     kmin = wmin(kmin);
     if (lane == 0) red[warp] = kmin;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t k = red[0];
-        for (int w = 1; w < nwarps; w++) k = red[w] < k ? red[w] : k;
-        if (k != KEY_NONE) atomicMin(&SV.ctl->key, (unsigned long long)k);
+    if (warp == 0) {   // CTA minimum by one warp
+        const uint64_t k = wmin(lane < nwarps ? red[lane] : KEY_NONE);
+        if (lane == 0 && k != KEY_NONE) atomicMin(&SV.ctl->key, (unsigned long long)k);
     }
 }
 
