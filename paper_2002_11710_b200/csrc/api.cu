@@ -273,6 +273,7 @@ extern "C" as_status as_ctx_create(int32_t device, void *stream, as_ctx **out) {
     if (prop.major < 10) return fail(AS_ERR_DEVICE, "this build targets sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
     c->n_sm = prop.multiProcessorCount;
     c->max_smem = prop.sharedMemPerBlockOptin;
+    if (getenv("AIRSCHED_SMEM_LIMIT")) c->max_smem = std::min<size_t>(c->max_smem, (size_t)atol(getenv("AIRSCHED_SMEM_LIMIT")));   // test knob
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
     CUDA_TRY(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
@@ -799,6 +800,12 @@ extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *
         return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
     }
     st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, digest, tabu_out, true);
+    if (st == AS_ERR_UNSUPPORTED && !P->sweep && !I->no_wait && !(digest && P->trace_level >= 2) && I->NL <= 65535 &&
+        I->n + I->V <= 65535 && I->NC <= 2) {
+        // no on-chip kernel holds this instance's state: the sharded kernels keep it in global
+        // memory (L2-resident), here with one rank
+        return sharded_run(ctx, nullptr, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
+    }
     if (st != AS_OK) return st;
     if (result->stop_reason == AS_STOP_INFEASIBLE_START)
         return fail(AS_ERR_INFEASIBLE_START, "device rejected the start schedule");

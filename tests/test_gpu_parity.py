@@ -644,3 +644,41 @@ def test_batch_run_jobs(A, ctx, oracle_mod):
     with pytest.raises(A.AirschedError) as e:
         A.as_batch_run_jobs(ctx, [(A.Instance(nw), starts[1][1], starts[1][2], 2)], prm)
     assert e.value.status == A.AS_ERR_UNSUPPORTED
+
+
+def test_state_too_large_for_shared_memory(A, oracle_mod, monkeypatch):
+    """When no on-chip kernel can hold an instance's state, as_tabu_run runs the sharded
+    kernels on one rank (state in global memory).  Forced here by capping the usable shared
+    memory of a fresh context; the trace must still equal the oracle's."""
+    monkeypatch.setenv("AIRSCHED_SMEM_LIMIT", "12000")
+    small = A.Ctx(0)
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    _compare_run(A, small, O, h, p, m, 1, 10, 400, seed=6, kick=3)
+    _compare_run(A, small, O, h, p, m, 0, 0, 400)
+
+
+def test_largest_single_instance(A, ctx, oracle_mod):
+    """n = 9000 missions, V = 100 (state ~330 KB: beyond shared memory, so the one-rank sharded
+    path; 171 M indices per iteration).  Checked at this size: the first selected move equals the
+    evaluation dump's minimum (itself parity-tested), the oracle re-evaluates that move to the
+    same delta and feasibility, and the best schedule is feasible with the reported objective."""
+    cfg = instgen.Config("max", 9000, 67, 33, 17, 8, 400, "disaster", 20, 5, 10)
+    inst = instgen.generate(cfg, seed=77)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = inst.planted_ptr, inst.planted_missions
+    r = A.as_tabu_run(ctx, h, p, m, A.params(mode=1, tenure=10, max_iters=5, trace_level=1), want_trace=True)
+    assert r["iters_done"] == 5
+    d, f, key = A.as_eval_moves(ctx, h, p, m, mode=1, tabu_expiry=np.full((inst.n_missions, inst.n_vehicles), -1, np.int32),
+                                iter=0, best_obj=O.objective(p, m))
+    c0, dl0, i0 = decode_key(key)
+    tr = r["trace"]
+    assert (int(tr["idx"][0]), int(tr["delta"][0]), int(tr["cls"][0])) == (i0, dl0, c0)
+    od, of = O.eval_indices(p, m, np.array([i0], np.int64), mode=1, E=None, it=0, best_obj=O.objective(p, m))
+    assert od[0] == dl0 and of[0] & 2
+    bp, bm = r["best"]
+    assert O.feasible(bp, bm) and O.objective(bp, bm) == r["best_obj"]
+    assert r["best_obj"] == int(tr["best"][-1])
