@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include "airsched.h"
 #include "engine.cuh"
@@ -245,6 +246,19 @@ struct as_ctx {
 struct as_comm {
     int nranks = 1, rank = 0, device = 0;
     ncclComm_t nccl = nullptr;
+    // NCCL device API state for the fused sharded kernel (set up on first use, collectively)
+    int dev_state = 0;             // 0 untried, 1 ready, -1 unavailable (LSA team != all ranks, or setup failed)
+    void *xbuf = nullptr;          // symmetric buffer (ncclMemAlloc) holding the [3][nranks] key slots
+    ncclWindow_t win = nullptr;
+    ncclDevComm devc{};
+    ncclDevComm *devc_dev = nullptr;   // device copy
+};
+
+// Grid-kernel options of a fused sharded run (run_core).
+struct GridXr {
+    int nranks, rank;
+    const ncclDevComm *devc;
+    ncclWindow_t win;
 };
 
 #define NCCL_TRY(expr)                                                                              \
@@ -590,7 +604,8 @@ static int env_int(const char *name, int dflt) {
 static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, const int32_t *start_ptr,
                           const int32_t *start_ms, int32_t shared_start, const as_run_params *P,
                           const uint64_t *seeds, as_run_result *results, int32_t *best_ptr, int32_t *best_ms,
-                          as_trace_rec *trace, uint64_t *digest, int32_t *tabu_out, bool single) {
+                          as_trace_rec *trace, uint64_t *digest, int32_t *tabu_out, bool single,
+                          const GridXr *xr = nullptr) {
     if (!P) return fail(AS_ERR_INVALID_ARG, "null params");
     if (P->mode != AS_MODE_NS && P->mode != AS_MODE_TABU) return fail(AS_ERR_INVALID_ARG, "mode must be NS or TABU");
     if (P->max_iters < 0 || P->tenure < 0 || P->kick < 0) return fail(AS_ERR_INVALID_ARG, "negative parameter");
@@ -679,8 +694,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     memset(&GA, 0, sizeof(GA));
     size_t grid_smem = 0;
     int grid_blocks = 0;
+    if (xr && !(single && compact_ok && !P->sweep))
+        return fail(AS_ERR_UNSUPPORTED, "fused sharded run needs the compact layout");
     if (single && compact_ok && !P->sweep) {
-        const int want_grid = env_int("AIRSCHED_GRID", -1);
+        const int want_grid = xr ? 1 : env_int("AIRSCHED_GRID", -1);
         const bool kfits = kfit;
         // CTAs: one per single-row tile up to the SM count (an iteration's floor is one tile's
         // latency + the grid barrier + the apply; an SM scoring many tiles at once is issue-bound,
@@ -712,6 +729,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 use_grid = coop != 0;
                 grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS",
                                                                                       want_grid == 1 ? ctx->n_sm : need_blocks)));
+                if (xr) grid_blocks = std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS", ctx->n_sm)));
                 GA.Tglobal = D.Tpad;
                 void *p;
                 if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
@@ -727,7 +745,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
                 // overhead), the larger G on ties.  A global table caps G at 8 so a row group's table rows
                 // (~3.4 KB per row at C5) stay L1-resident for the CTA (measured: DESIGN.md §7).
-                const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS;
+                const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS * (xr ? xr->nranks : 1);
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
                 const int gmax = GA.T_smem ? 256 : 8;
                 double best_cost = 1e300;
@@ -739,12 +757,25 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     if (cost <= best_cost) { best_cost = cost; GA.G = g; }
                 }
                 GA.G = std::max(1, env_int("AIRSCHED_GRID_G", GA.G));
+                GA.tlo = 0;
+                GA.thi = grid_tile_count(n, V, GA.G);
+                if (xr) {   // this rank's slice of the tile list (same weighted plan as the sharded kernels)
+                    shard_plan(n, V, GA.G, xr->nranks, xr->rank, &GA.tlo, &GA.thi, nullptr, nullptr);
+                    GA.xr = 1;
+                    GA.xr_nranks = xr->nranks;
+                    GA.xr_rank = xr->rank;
+                    GA.xr_comm = xr->devc;
+                    GA.xr_win = xr->win;
+                    if ((st = scratch(ctx, "g_key2", 3 * 8, &p)) != AS_OK) return st;
+                    GA.gkey2 = (unsigned long long *)p;
+                }
             }
         }
     }
+    if (xr && !use_grid) return fail(AS_ERR_UNSUPPORTED, "fused sharded run: the state does not fit the grid kernel");
     if (env_int("AIRSCHED_VERBOSE", 0))
         fprintf(stderr, "[airsched] n=%d V=%d runs=%d single=%d -> %s (blocks %d, G %d, T_smem %d, E_smem %d, smem %zu)\n",
-                n, V, n_runs, (int)single, use_grid ? (grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
+                n, V, n_runs, (int)single, use_grid ? (xr ? "k_grid fused-sharded" : grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
                 use_batch ? "k_batch" : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
                 use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -1160,6 +1191,12 @@ extern "C" void as_comm_destroy(as_comm *comm) {
     if (!comm) return;
     if (comm->nccl) {
         cudaSetDevice(comm->device);
+        if (comm->dev_state == 1) {
+            ncclDevCommDestroy(comm->nccl, &comm->devc);
+            ncclCommWindowDeregister(comm->nccl, comm->win);
+            cudaFree(comm->devc_dev);
+        }
+        if (comm->xbuf) ncclMemFree(comm->xbuf);
         ncclCommDestroy(comm->nccl);
     }
     delete comm;
@@ -1192,11 +1229,43 @@ extern "C" as_status as_shard_plan(const as_instance *I, int32_t nranks, int32_t
 
 // Sharded single-instance run: replica in global memory, K iterations per CUDA
 // graph of [eval slice -> ncclAllReduce(MIN, 8 B) -> apply].
+// NCCL device-API state of a communicator (collective: every rank calls it in the same order).
+static as_status comm_device_setup(as_comm *comm) {
+    if (comm->dev_state) return AS_OK;
+    comm->dev_state = -1;
+    if (ncclTeamLsa(comm->nccl).nRanks != comm->nranks) return AS_OK;   // not every peer load/store reachable
+    NCCL_TRY(ncclMemAlloc(&comm->xbuf, 4096));
+    NCCL_TRY(ncclCommWindowRegister(comm->nccl, comm->xbuf, 4096, &comm->win, NCCL_WIN_COLL_SYMMETRIC));
+    CUDA_TRY(cudaMemset(comm->xbuf, 0, 4096));
+    ncclDevCommRequirements reqs;
+    memset(&reqs, 0, sizeof(reqs));
+    reqs.lsaBarrierCount = 1;
+    NCCL_TRY(ncclDevCommCreate(comm->nccl, &reqs, &comm->devc));
+    CUDA_TRY(cudaMalloc(&comm->devc_dev, sizeof(ncclDevComm)));
+    CUDA_TRY(cudaMemcpy(comm->devc_dev, &comm->devc, sizeof(ncclDevComm), cudaMemcpyHostToDevice));
+    comm->dev_state = 1;
+    return AS_OK;
+}
+
 static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
                              const int32_t *start_ms, const as_run_params *P, as_run_result *result,
                              int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out) {
     as_status st = set_device(ctx);
     if (st != AS_OK) return st;
+    // Fused path (default with a communicator; AIRSCHED_SHARD_FUSED=0 disables it): one persistent
+    // k_grid per rank scores the rank's tile slice and exchanges the 8-byte winner with its peers
+    // through NVLink stores into a symmetric window + an LSA barrier inside the kernel, instead
+    // of [eval kernel, ncclAllReduce, apply kernel] per iteration.  Needs every peer in the LSA
+    // team and the state in shared memory; otherwise the NCCL path below runs.
+    if (comm && env_int("AIRSCHED_SHARD_FUSED", 1) == 1 && (comm->nranks > 1 || env_int("AIRSCHED_SHARD_FUSED_1", 0) == 1)) {
+        if ((st = comm_device_setup(comm)) != AS_OK) return st;
+        if (comm->dev_state == 1) {
+            GridXr xr{comm->nranks, comm->rank, comm->devc_dev, comm->win};
+            st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, nullptr,
+                          tabu_out, true, &xr);
+            if (st != AS_ERR_UNSUPPORTED) return st;
+        }
+    }
     const DevInst *D;
     if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
     InstDev &ID = ctx->insts[I];

@@ -16,7 +16,10 @@
 // The tabu matrix, when it lives in global memory, is written by every CTA with
 // identical values, so each CTA's own reads after its apply are up to date.
 #include <cooperative_groups.h>
+#include <cuda/atomic>
 #include <cuda_runtime.h>
+#include <nccl.h>
+#include <nccl_device.h>
 
 #include <cstdint>
 
@@ -54,8 +57,33 @@ size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, boo
     return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
 }
 
-__device__ __forceinline__ bool GT_spread(int n, int V, int G, int nwarps_all) {
-    return grid_tiles(n, V, G).n_total < nwarps_all;
+__device__ __forceinline__ bool GT_spread(int ntiles, int nwarps_all) { return ntiles < nwarps_all; }
+
+// Fused sharded run, one thread of CTA 0 per rank (after the grid minimum of this rank's tile
+// slice is in gkey[q]): store it into slot [q][rank] of EVERY rank's symmetric window through
+// the NVLink load/store mapping, meet the peers at the LSA barrier (release our stores, acquire
+// theirs), and fold the nranks slots of the local window into the all-ranks winner.  Slots are
+// triple-buffered by iteration: slot q is rewritten at it+3, after two more barriers, by which
+// time every rank has read it.
+__device__ __forceinline__ uint64_t rank_exchange(const GridArgs &GA, int q, uint64_t kl) {
+    const size_t off = (size_t)(q * GA.xr_nranks + GA.xr_rank) * sizeof(unsigned long long);
+    for (int p = 0; p < GA.xr_nranks; p++) {
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(ncclGetLsaPointer(GA.xr_win, off, p));
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_system>(*dst).store(kl, cuda::memory_order_relaxed);
+    }
+    {
+        ncclLsaBarrierSession<ncclCoopThread> bar(ncclCoopThread(), *GA.xr_comm, ncclTeamTagLsa(), 0);
+        bar.sync(ncclCoopThread(), cuda::memory_order_acq_rel);
+    }
+    unsigned long long *mine = reinterpret_cast<unsigned long long *>(
+        ncclGetLocalPointer(GA.xr_win, (size_t)q * GA.xr_nranks * sizeof(unsigned long long)));
+    uint64_t kg = KEY_NONE;
+    for (int p = 0; p < GA.xr_nranks; p++) {
+        const uint64_t v = cuda::atomic_ref<unsigned long long, cuda::thread_scope_system>(mine[p]).load(
+            cuda::memory_order_relaxed);
+        kg = v < kg ? v : kg;
+    }
+    return kg;
 }
 
 // TR: the table is read from global memory (row-local reads, score.cuh).
@@ -186,14 +214,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     // of that group are shared in L1) when the tiles fill the grid; spread over the CTAs first when
     // there are fewer tiles than warps, so every SM scores at most ~one tile (latency-bound sizes)
     const int nwarps_all = gridDim.x * nwarps;
-    const int gwarp = GT_spread(n, V, GA.G, nwarps_all) ? warp * gridDim.x + blockIdx.x : blockIdx.x * nwarps + warp;
+    const int gwarp = GT_spread(GA.thi - GA.tlo, nwarps_all) ? warp * gridDim.x + blockIdx.x : blockIdx.x * nwarps + warp;
     const bool one = gridDim.x == 1;
     unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
 
     int it = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
-        uint64_t kmin = score_tiles<TABU, FULL, TR>(SC, M, R, GT, 0, GT.n_total, gwarp, nwarps_all, it, cur, best, lane);
+        uint64_t kmin = score_tiles<TABU, FULL, TR>(SC, M, R, GT, GA.tlo, GA.thi, gwarp, nwarps_all, it, cur, best, lane);
         kmin = wmin(kmin);
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
@@ -206,13 +234,22 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             }
         }
         if (!one) grid.sync();   // a single CTA (small instances) needs no grid barrier
+        if (GA.xr) {   // fused sharded run: the all-ranks minimum over NVLink, then every CTA reads it
+            if (blockIdx.x == 0 && tid == 0) {
+                const int q = it % 3;
+                const uint64_t kl = one ? kcta : __ldcg(&gkey[q]);
+                GA.gkey2[q] = rank_exchange(GA, q, kl);
+            }
+            if (one) __syncthreads();
+            else grid.sync();
+        }
         if (warp == 0) {
             // apply (every CTA, identical arithmetic): lane 0 splits the delta (from the key: the
             // scorers proved the move valid and feasible), relinks and updates the route totals and
             // the tabu matrix; the touched incoming-link records are then refreshed one per lane
             int nt = 0;
             if (lane == 0) {
-                const uint64_t k = one ? kcta : __ldcg(&gkey[it % 3]);
+                const uint64_t k = GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
                 int stop = 0;
                 if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
                 else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;

@@ -6,8 +6,12 @@
 #include <cstdint>
 #include <vector>
 
+#include <nccl.h>
+
 #include "airsched.h"
 #include "engine.cuh"
+
+struct ncclDevComm;
 
 namespace airsched {
 
@@ -69,6 +73,13 @@ struct GridArgs {
     int32_t *BS;                   // [S] best-schedule successor array
     unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
     int G;                         // rows per tile
+    int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
+    // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
+    // into every peer's symmetric window slot over NVLink and meets the peers at an LSA barrier
+    int xr, xr_nranks, xr_rank;
+    const ncclDevComm *xr_comm;    // device copy of the NCCL device communicator
+    ncclWindow_t xr_win;           // symmetric window: [3][nranks] u64 slots
+    unsigned long long *gkey2;     // [3] the all-ranks winner per slot
 };
 
 // Sharded single-instance run (shard.cu): replica state in global memory.
@@ -96,6 +107,7 @@ cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_
                               cudaStream_t st);
 void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
                 int64_t *weight_rank);
+int grid_tile_count(int n, int V, int G);
 
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,

@@ -328,6 +328,8 @@ cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_
 }
 
 // Tile weights (scored moves per tile, approximately) for the rank split.
+int grid_tile_count(int n, int V, int G) { return grid_tiles(n, V, G).n_total; }
+
 void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
                 int64_t *weight_rank) {
     const GridTiles GT = grid_tiles(n, V, G);

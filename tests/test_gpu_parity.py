@@ -682,3 +682,30 @@ def test_largest_single_instance(A, ctx, oracle_mod):
     bp, bm = r["best"]
     assert O.feasible(bp, bm) and O.objective(bp, bm) == r["best_obj"]
     assert r["best_obj"] == int(tr["best"][-1])
+
+
+@pytest.mark.parametrize("cfg,iters", [("ontario", 400), ("large", 30), ("surge", 2)])
+def test_sharded_fused_one_rank(A, ctx, oracle_mod, cfg, iters, monkeypatch):
+    """The fused sharded kernel (k_grid per rank; the 8-byte winner exchanged through NVLink
+    stores into an NCCL symmetric window + an LSA barrier inside the kernel), run with a
+    one-rank communicator on this GPU: its tile slice, exchange and apply against the oracle."""
+    monkeypatch.setenv("AIRSCHED_SHARD_FUSED_1", "1")
+    comm = A.Comm(ctx, 1, 0, A.as_comm_unique_id())
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    ctx.upload(h)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    for mode in ((1,) if cfg == "surge" else (1, 0)):
+        prm = A.params(mode=mode, tenure=c.tenure, max_iters=iters, trace_level=1, seed=3, kick=2)
+        l0 = ctx.kernel_launches
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=(mode == 1), comm=comm)
+        assert ctx.kernel_launches - l0 <= 3   # one persistent kernel (+ CSR of the best), not per-iteration graphs
+        o = O.search(p, m, mode=mode, tenure=c.tenure, max_iters=iters, seed=3, kick=2)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and (g["trace"]["cur"] == o["trace"]["cur"]).all()
+        assert g["best_obj"] == o["best_obj"] and g["best_iter"] == o["best_iter"]
+        if mode == 1:
+            assert (g["tabu"] == o["E"]).all()
+        assert routes_of(*g["best"]) == routes_of(*o["best"])
