@@ -277,6 +277,10 @@ def run_gpu(args):
             "frac": achieved_gops / peak_gops, "traffic": args.traffic if args.traffic is not None else
             measured_traffic(args.workload),
             "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"}
+    prof = measured_profile(args.workload)
+    if "issue_slots_busy" in prof:   # the issue-slot view of the same kernel (ncu): it is issue-bound
+        roof["ncu_issue_slots_busy"] = prof["issue_slots_busy"]
+        roof["ncu_alu_fma_pipe"] = [prof.get("alu_pipe"), prof.get("fma_pipe")]
 
     if rank != 0:
         if world > 1:
@@ -420,16 +424,21 @@ def run_jobs(args):
     return 0
 
 
-def measured_traffic(workload):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
-    capture (profiles/r01/traffic.json); None when that workload was not captured."""
+def measured_profile(workload):
+    """The committed ncu --set full capture of the dominant kernel for this workload
+    (profiles/r01/traffic.json), or {}."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
     try:
         with open(path) as f:
-            rec = json.load(f).get(workload)
-        return None if rec is None else float(rec["bytes_per_launch"])
-    except (OSError, ValueError, KeyError):
-        return None
+            return json.load(f).get(workload) or {}
+    except (OSError, ValueError):
+        return {}
+
+
+def measured_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel (ncu capture), or None."""
+    rec = measured_profile(workload)
+    return float(rec["bytes_per_launch"]) if "bytes_per_launch" in rec else None
 
 
 def run_single(args):
