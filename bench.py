@@ -281,6 +281,8 @@ def run_gpu(args):
     if "issue_slots_busy" in prof:   # the issue-slot view of the same kernel (ncu): it is issue-bound
         roof["ncu_issue_slots_busy"] = prof["issue_slots_busy"]
         roof["ncu_alu_fma_pipe"] = [prof.get("alu_pipe"), prof.get("fma_pipe")]
+    if "shared_wavefronts_pct_of_peak" in prof:   # the memory level that binds (HBM/L2 are ~0 by design)
+        roof["ncu_shared_mem_pct_of_peak"] = prof["shared_wavefronts_pct_of_peak"]
 
     if rank != 0:
         if world > 1:
