@@ -709,3 +709,26 @@ def test_sharded_fused_one_rank(A, ctx, oracle_mod, cfg, iters, monkeypatch):
         if mode == 1:
             assert (g["tabu"] == o["E"]).all()
         assert routes_of(*g["best"]) == routes_of(*o["best"])
+
+
+def test_solver_one_call(A, oracle_mod):
+    """paper_2002_11710_b200.solver.solve: the best of a batch equals the oracle's run with that
+    seed, and the schedule is feasible with the reported objective (both start kinds)."""
+    from paper_2002_11710_b200 import solver
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    out = solver.solve(inst, runs=32, iters=300, tenure=10, kick=6)
+    ptr, ms = np.zeros(inst.n_vehicles + 1, np.int32), []
+    for v, r in enumerate(out["routes"]):
+        ptr[v + 1] = ptr[v] + len(r)
+        ms += r
+    ms = np.array(ms, np.int32)
+    assert O.feasible(ptr, ms) and O.objective(ptr, ms) == out["objective"]
+    st, (p, m), _, _ = O.greedy(insert_mode=1)
+    o = O.search(p, m, mode=1, tenure=10, max_iters=300, seed=out["seed"], kick=6)
+    assert o["best_obj"] == out["objective"] and routes_of(*o["best"]) == out["routes"]
+    assert out["objective"] == int(out["results"]["best_obj"].min())
+    out2 = solver.solve(inst, runs=32, iters=300, starts="seeded", mode="ns")
+    st, (p2, m2), _, _ = O.greedy(insert_mode=1, seed=out2["seed"])
+    o2 = O.search(p2, m2, mode=0, max_iters=300, seed=out2["seed"])
+    assert o2["best_obj"] == out2["objective"]
