@@ -732,3 +732,35 @@ def test_solver_one_call(A, oracle_mod):
     st, (p2, m2), _, _ = O.greedy(insert_mode=1, seed=out2["seed"])
     o2 = O.search(p2, m2, mode=0, max_iters=300, seed=out2["seed"])
     assert o2["best_obj"] == out2["objective"]
+
+
+def test_jobs_and_greedy_degenerate(A, ctx, oracle_mod):
+    """Degenerate jobs: an instance with no missions, one with one mission and one vehicle,
+    next to a normal one; and Alg. 1 batches on them."""
+    base = instgen.generate("tiny")
+    empty = instgen.Instance(base.travel_s, base.class_is_heli, base.base_location, base.vehicle_base,
+                             base.vehicle_class, np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32),
+                             np.zeros(0, np.uint8))
+    one = instgen.generate(instgen.Config("one", 1, 1, 0, 1, 0, 4, "ontario", 3, 10, 2), seed=3)
+    insts = [empty, one, base]
+    jobs = []
+    for inst in insts:
+        h = A.Instance(inst)
+        ptr, ms, status, nrep = A.as_init_greedy_batch(ctx, h, 4, seeds=np.arange(4, dtype=np.uint64), insert_mode=1)
+        O = oracle_mod.Oracle(inst)
+        for r in range(4):
+            st, (op, om), nr, _ = O.greedy(insert_mode=1, seed=r)
+            assert (status[r] == 0) == (st == 0)
+            if st == 0:
+                assert routes_of(ptr[r], ms[r][:inst.n_missions]) == routes_of(op, om)
+        jobs.append((h, ptr[0], ms[0][:inst.n_missions], 3))
+    prm = A.params(mode=1, tenure=3, max_iters=50, kick=2)
+    res = np.zeros(9, A.RESULT_DTYPE)
+    A.as_batch_run_jobs(ctx, jobs, prm, np.arange(1, 10, dtype=np.uint64), results=res)
+    assert (res["best_obj"][:3] == 0).all() and (res["stop_reason"][:3] == A.AS_STOP_NO_MOVE).all()
+    for j, inst in enumerate(insts[1:], start=1):
+        O = oracle_mod.Oracle(inst)
+        h, p, m, _ = jobs[j]
+        for r in range(3):
+            o = O.search(p, m, mode=1, tenure=3, max_iters=50, seed=3 * j + r + 1, kick=2)
+            assert res[3 * j + r]["best_obj"] == o["best_obj"] and res[3 * j + r]["iters_done"] == o["iters_done"]
