@@ -711,9 +711,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             auto &D = ctx->insts[I];
             const int tb = D.tpad_bytes;
             struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
-            const bool t_global = env_int("AIRSCHED_GRID_T_GLOBAL", 0) == 1;   // test knob
+            const bool t_global = env_int("AIRSCHED_GRID_T_GLOBAL", 0) == 1;   // test knobs
+            const bool e_global = env_int("AIRSCHED_GRID_E_GLOBAL", 0) == 1;
             for (auto o : gopts) {
-                if (t_global && o.t) continue;
+                if ((t_global && o.t) || (e_global && o.e)) continue;
                 size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, 4, o.t, o.e && tabu, tabu);
                 if (b <= ctx->max_smem) {
                     GA.T_smem = o.t;
@@ -740,6 +741,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 if (tabu && !GA.E_smem) {
                     if ((st = scratch(ctx, "g_E", (size_t)n * V * 4 + 4, &p)) != AS_OK) return st;
                     GA.Eglobal = (int32_t *)p;
+                    if ((st = scratch(ctx, "g_Et", (size_t)n * V * 4 + 4, &p)) != AS_OK) return st;
+                    GA.Etglobal = (int32_t *)p;
                 }
                 // rows per tile: the tiles go round-robin over the warps, so an iteration costs about
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round

@@ -149,6 +149,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     for (int x = tid; x < S; x += blockDim.x) R.veh[x] = x < n ? (int16_t)-1 : (int16_t)(x - n);
     if (TABU && (GA.E_smem || blockIdx.x == 0))
         for (int i = tid; i < n * V; i += blockDim.x) E[i] = (ET)-1;
+    if (TABU && !GA.E_smem && blockIdx.x == 0)
+        for (int i = tid; i < n * V; i += blockDim.x) reinterpret_cast<ET *>(GA.Etglobal)[i] = (ET)-1;
     if (tid == 0) ctrl[0] = ctrl[1] = 0;
     __syncthreads();
     const int32_t *ptr = A.start_ptr, *ms = A.start_ms;
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
 
     ScoreCtx<TT, ET> SC;
     SC.Ts = Ts; SC.Tt = I.tsym ? Ts : reinterpret_cast<const TT *>(I.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
+    ET *Et = TABU && !GA.E_smem ? reinterpret_cast<ET *>(GA.Etglobal) : nullptr;
+    SC.Et = Et;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
@@ -261,6 +265,15 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
                     const MoveSplit ms = move_split(M, R, idx, delta);
                     nt = move_relink(M, R, idx, ms.a, ms.b, ctrl + 4);
                     move_totals(M, R, idx, ms, it, A.tenure, TABU);
+                    if (TABU && Et) {   // the transposed copy gets the same expiries (every CTA, identical values)
+                        const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+                        if (idx < Rb) {
+                            Et[(size_t)ms.a * n + idx / S] = (ET)(it + A.tenure);
+                        } else {
+                            Et[(size_t)ms.a * n + (idx - Rb) / n] = (ET)(it + A.tenure);
+                            Et[(size_t)ms.b * n + (idx - Rb) % n] = (ET)(it + A.tenure);
+                        }
+                    }
                     const long long c = s_cur + delta;
                     s_cur = c;
                     if (c < s_best) {

@@ -70,6 +70,7 @@ struct GridArgs {
     int T_smem, E_smem;            // table / tabu matrix staged in shared memory?
     const void *Tglobal;           // padded table in global memory (uint16 or int32)
     int32_t *Eglobal;              // [n][V] tabu matrix when !E_smem
+    int32_t *Etglobal;             // [V][n] its transpose (identical values), when !E_smem
     int32_t *BS;                   // [S] best-schedule successor array
     unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
     int G;                         // rows per tile

@@ -75,6 +75,7 @@ struct ScoreCtx {
     const uint32_t *LK;    // [S] succ | pred << 16
     const int32_t *F;      // [V] route flight time
     const ET *E;           // [n][V] tabu expiry (TABU only)
+    const ET *Et;          // [V][n] its transpose when E is in global memory (row-local E[m2][a] reads), else null
     int n, V, S, NL, NLp, P;
     uint32_t Rb, mask;
     int one, neg;          // 1 and -1, opaque to the compiler (see madd)
@@ -242,6 +243,9 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
         const int slkA = P - F[a];
         const int sv10 = c1.z, sv11 = c1.w;
         const ET *Erow = TABU ? E + m1 * V : nullptr;
+        // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
+        const ET *ecol = TABU ? ((TR && C.Et) ? C.Et + (size_t)a * C.n : E + a) : nullptr;
+        const int estr = (TR && C.Et) ? 1 : V;
         const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
         const int one = C.one, neg = C.neg;
         const int ndepc1 = madd(depc1, neg, 0), nw1 = madd(w1, neg, 0);
@@ -272,7 +276,7 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
             const bool ok = (mg >= 0) & (m2 > m1) & (s1 != m2) & (s2 != m1) &
                             (FULL || (same ? en_intra_s : en_inter_s)) & (!h2 | hoka) & (!heli1 | hokb);
             bool adm;
-            if (TABU) adm = (((int)Erow[max(b, 0)] < it) & ((int)E[max(m2, 0) * V + a] < it)) | (delta < asp);
+            if (TABU) adm = (((int)Erow[max(b, 0)] < it) & ((int)ecol[max(m2, 0) * estr] < it)) | (delta < asp);
             else adm = delta < 0;
             uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | (adm ? 0u : 0x80000000u);
             k32 = ok ? k32 : 0xFFFFFFFFu;
@@ -476,6 +480,9 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
         // compatibility mask over q_bf: m1 heli-only needs bit 21 clear; m2 heli-only (bit 20) needs route a heli-ok
         const int cmask = (MH[m1] ? (1 << 21) : 0) | (((vca >> 8) & 1) ? 0 : (1 << 20));
         const ET *Erow = TABU ? E + m1 * V : nullptr;
+        // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
+        const ET *ecol = TABU ? ((TR && C.Et) ? C.Et + (size_t)a * C.n : E + a) : nullptr;
+        const int estr = (TR && C.Et) ? 1 : V;
         const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
         const int tri = -m1 - 1;
 #pragma unroll
@@ -504,7 +511,7 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
             uint32_t nadm;
             if (TABU) {
                 const int t1 = madd(it, neg, (int)Erow[b]);                      // E[m1][b] - it
-                const int t2 = madd(it, neg, (int)E[max(m2, 0) * V + a]);        // E[m2][a] - it
+                const int t2 = madd(it, neg, (int)ecol[max(m2, 0) * estr]);      // E[m2][a] - it
                 const int e2 = madd(asp, neg, delta);
                 nadm = ~(uint32_t)((t1 & t2) | e2) & 0x80000000u;
             } else {

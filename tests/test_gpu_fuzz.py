@@ -90,6 +90,7 @@ PATHS = {
     "k_grid_1cta": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_BLOCKS": "1"},
     "k_grid_all": {"AIRSCHED_GRID": "1"},
     "k_grid_tglobal": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_T_GLOBAL": "1", "AIRSCHED_GRID_G": "2"},
+    "k_grid_teglobal": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_T_GLOBAL": "1", "AIRSCHED_GRID_E_GLOBAL": "1"},
     "k_batch": {"AIRSCHED_BATCH_KERNEL": "1"},
     "sharded2": {"AIRSCHED_SHARDED": "1", "AIRSCHED_SHARD_EMULATE": "2", "AIRSCHED_SHARD_K": "3"},
 }

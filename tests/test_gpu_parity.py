@@ -382,6 +382,8 @@ def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch):
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
     monkeypatch.setenv("AIRSCHED_GRID_T_GLOBAL", "1")   # table in global memory: row-local reads
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+    monkeypatch.setenv("AIRSCHED_GRID_E_GLOBAL", "1")   # tabu matrix (and its transpose) in global memory
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=5, kick=4)
 
 
 def test_surge_run_parity_prefix(A, ctx, oracle_mod):
