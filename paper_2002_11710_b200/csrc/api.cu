@@ -677,8 +677,12 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int S = n + V;
     const int tbytes = I->maxT <= 65535 ? 2 : 4;
     const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
+    // window scorers (window.cuh) for the batched kernel: every move kind, positive service legs, uint16 table,
+    // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
+    const bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && V <= 32 && !P->sweep &&
+                     (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
     size_t sh_b = 0, run_b = 0;
-    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b);
+    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
     // the compact-layout kernels (k_batch, k_grid) score the waiting model only;
     // the no-wait variant (f3) runs on k_search
@@ -779,7 +783,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     if (env_int("AIRSCHED_VERBOSE", 0))
         fprintf(stderr, "[airsched] n=%d V=%d runs=%d single=%d -> %s (blocks %d, G %d, T_smem %d, E_smem %d, smem %zu)\n",
                 n, V, n_runs, (int)single, use_grid ? (xr ? "k_grid fused-sharded" : grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
-                use_batch ? "k_batch" : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
+                use_batch ? (win ? "k_batch/window" : "k_batch") : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
                 use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_grid) {
@@ -792,7 +796,12 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
         rpc = std::max(1, env_int("AIRSCHED_RPC", rpc));
         rpc = std::min(rpc, std::min(28, rpc_fit));
         size_t smem_b = sh_b + (size_t)rpc * run_b;
-        CUDA_TRY(launch_batch(A, tabu ? 1 : 0, rpc, tbytes, ebytes, smem_b, ctx->stream));
+        if (win && tabu) {   // the window path keeps each run's tabu matrix in global memory
+            void *e;
+            if ((st = scratch(ctx, "E_win", (size_t)n_runs * n * V * 4 + 4, &e)) != AS_OK) return st;
+            A.E_global = (int32_t *)e;
+        }
+        CUDA_TRY(launch_batch(A, tabu ? 1 : 0, rpc, tbytes, ebytes, smem_b, ctx->stream, win));
     } else {
         if (!kfit) return fail(AS_ERR_UNSUPPORTED, "instance too large for the per-CTA kernel (n=%d, V=%d)", n, V);
         int threads;
@@ -928,14 +937,25 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     int threads = 32;
     std::vector<int32_t> packed;           // host starts, uploaded once
     std::vector<std::pair<int64_t, int64_t>> poff(n_jobs, {-1, -1});
-    int64_t run0 = 0, bp0 = 0, bm0 = 0;
+    // window scorers (window.cuh) for the FAST launch when every FAST job qualifies (V <= 32)
+    bool win = ((P->sweep ? 1u : P->move_mask) & 15u) == 15u && !P->sweep && tbytes == 2 &&
+               (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
+    for (int j = 0; j < n_jobs && win; j++) {
+        const DevInst *D;
+        if ((st = get_dev_inst(ctx, jobs[j].inst, &D)) != AS_OK) return st;
+        if (D->svcpos && jobs[j].inst->V > 32) win = false;
+    }
+    int64_t run0 = 0, bp0 = 0, bm0 = 0, e0 = 0;
     for (int j = 0; j < n_jobs; j++) {
         const as_instance *I = jobs[j].inst;
         const DevInst *D;
         if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
         BatchJob &b = J[j];
         b.inst = *D;
-        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu);
+        const bool wj = win && D->svcpos;
+        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu, wj, P->tenure);
+        b.e_off = e0;
+        if (wj && tabu) e0 += (int64_t)jobs[j].n_runs * I->n * I->V;
         b.NLp = padded_stride_host(I->NL, tbytes);
         if ((size_t)b.L.shared_bytes + b.L.run_bytes > ctx->max_smem)
             return fail(AS_ERR_UNSUPPORTED, "job %d: instance too large for the batched kernel", j);
@@ -1014,6 +1034,11 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     A.best_ptr = (int32_t *)o_bp.dev;
     A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
     A.trace = (as_trace_rec *)o_tr.dev;
+    if (e0 > 0) {   // tabu matrices of the window-path runs (global memory)
+        void *e;
+        if ((st = scratch(ctx, "E_win_jobs", (size_t)e0 * 4 + 4, &e)) != AS_OK) return st;
+        A.E_global = (int32_t *)e;
+    }
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     const int n_gen = (int)cta.size() - n_fast;
     if (n_gen > 0 && n_fast > 0) {   // fork the general-scorer CTAs onto the side stream
@@ -1025,7 +1050,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     }
     if (n_fast > 0) {
         CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_fast, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, true, ctx->stream));
+                                   tabu ? 1 : 0, tbytes, ebytes, true, ctx->stream, win));
         ctx->launches++;
     } else {
         CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_gen, threads, smem,

@@ -25,12 +25,17 @@
 #include "launch.h"
 #include "score.cuh"
 #include "compact.cuh"
+#include "window.cuh"
 
 namespace airsched {
 
 constexpr int MAXTHREADS = 896;    // <= 28 runs per CTA (one wave of 4096 runs on 148 SMs)
 
-__host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu) {
+// win: the WINDOW scorers (window.cuh) -- the tabu matrix lives in global memory, the run block
+// holds the tabu bits TB[n], the ring of the last tenure + 1 iterations' tabu writes and the
+// warp's window buffer instead.
+__host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
+                                                   bool win = false, int tenure = 0) {
     BatchLayout L;
     const int S = n + V;
     const int NLp = padded_stride(NL, tbytes);
@@ -46,16 +51,19 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.LK = r; r = al16(r + S * 4);
     L.BS = r; r = al16(r + S * 2);
     L.F = r; r = al16(r + V * 4);
-    L.E = r; r = al16(r + (tabu ? n * V * ebytes : 0));
-    L.PM = r; r = al16(r + V * 2);
-    L.SN = r; r = al16(r + n * 2);
+    L.E = r; r = al16(r + (tabu && !win ? n * V * ebytes : 0));
+    L.PM = r; r = al16(r + (win ? 0 : V * 2));
+    L.SN = r; r = al16(r + (win ? 0 : n * 2));
+    L.TB = r; r = al16(r + (win && tabu ? n * 4 : 0));
+    L.RG = r; r = al16(r + (win && tabu ? 2 * (tenure + 1) * 4 : 0));
+    L.WB = r; r = al16(r + (win ? WIN_ROWS * WIN_REC_INT4 * 16 : 0));
     L.run_bytes = r;
     return L;
 }
 
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes) {
-    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu);
+                size_t *run_bytes, bool win, int tenure) {
+    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure);
     *shared_bytes = L.shared_bytes;
     *run_bytes = L.run_bytes;
 }
@@ -63,8 +71,9 @@ void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
 // One CTA of the batched executor: stage A.inst, then run this CTA's runs
 // cta_run0 .. cta_run0 + RPC - 1 (one per warp; A's per-run arrays are indexed by
 // that run number).
-template <bool TABU, class TT, class ET, bool FULL>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN>
 __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const BatchLayout &L, int NLp, int cta_run0) {
+    static_assert(!WIN || (FULL && sizeof(TT) == 2 && sizeof(ET) == 4), "window scorers: FAST, uint16 table, int32 E");
     extern __shared__ __align__(16) unsigned char smem[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC, NL = I.NL;
@@ -113,7 +122,11 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     uint32_t *LK = reinterpret_cast<uint32_t *>(rb + L.LK);
     uint16_t *BS = reinterpret_cast<uint16_t *>(rb + L.BS);
     int32_t *F = reinterpret_cast<int32_t *>(rb + L.F);
-    ET *E = TABU ? reinterpret_cast<ET *>(rb + L.E) : nullptr;
+    // tabu expiry matrix: shared memory, or (window scorers) this run's block of E_global
+    ET *E = TABU ? (WIN ? reinterpret_cast<ET *>(A.E_global + (size_t)run * n * V) : reinterpret_cast<ET *>(rb + L.E))
+                 : nullptr;
+    uint32_t *TB = WIN && TABU ? reinterpret_cast<uint32_t *>(rb + L.TB) : nullptr;   // tabu bits (window.cuh)
+    uint32_t *RG = WIN && TABU ? reinterpret_cast<uint32_t *>(rb + L.RG) : nullptr;   // tabu-write ring
 
     CompactMV<TT> M;
     M.T = Ts; M.CS = CS; M.MH = MH; M.VC = VC; M.CH = CH;
@@ -123,6 +136,8 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
     R.pick_s.base = CS; R.w_s.base = CS;
     R.F = F; R.E = E;
+    CompactRV<ET> R0 = R;   // evaluation view: the window path takes tabu from TB, not from E in global memory
+    if (WIN) R0.E = nullptr;
 
     // ---- start schedule (CSR) -> linked lists --------------------------------
     const int32_t *ptr = A.start_ptr + (A.shared_start ? 0 : (size_t)run * (V + 1));
@@ -130,6 +145,10 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     for (int x = lane; x < S; x += 32) R.veh[x] = x < n ? (int16_t)-1 : (int16_t)(x - n);
     if (TABU)
         for (int i = lane; i < n * V; i += 32) E[i] = (ET)-1;
+    if (WIN && TABU) {
+        for (int i = lane; i < n; i += 32) TB[i] = 0u;
+        for (int i = lane; i < 2 * (A.tenure + 1); i += 32) RG[i] = 0xFFFFFFFFu;
+    }
     __syncwarp();
     int bad = 0;
     if (ptr[V] != n || ptr[0] != 0) bad = 1;
@@ -195,7 +214,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
             for (int k = 0; k < A.kick; k++)
                 for (int tr = 0; tr < 64; tr++) {
                     uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
-                    MoveEval e = eval_index(M, R, idx, 0xFu, 0);
+                    MoveEval e = eval_index(M, R0, idx, 0xFu, 0);
                     if (e.valid && e.feasible) {
                         apply_move(M, R, idx, e, 0, 0, false);
                         kicks++;
@@ -220,6 +239,10 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     SC.Ts = Ts; SC.Tt = A.inst.tsym ? Ts : reinterpret_cast<const TT *>(A.inst.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E; SC.Et = nullptr;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = Rb; SC.mask = mask;
     SC.one = A.one; SC.neg = -A.one;
+    WinCtx W;
+    W.WB = WIN ? reinterpret_cast<int4 *>(rb + L.WB) : nullptr;
+    W.TB = TB;
+    const int ring = A.tenure + 1;
     int it = 0, stop = 0;
     if (A.sweep) {
         // ---- f1: the paper-literal (i, j) sweep of Alg. 2 / Alg. 3 (oracle or_sweep) ----
@@ -307,12 +330,37 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         __syncwarp();
         uint64_t kmin = KEY_NONE;
         const int asp = (int)(best - cur);   // aspiration: cur + delta < best  <=>  delta < asp
+        if (WIN && TABU) {
+            // tabu bits in force at iteration it: drop the pairs written at it - 1 - tenure (E = it - 1)
+            // unless a later iteration of the ring wrote the same pair again (O8)
+            const int slot = it % ring;
+            const uint32_t o0 = RG[2 * slot], o1 = RG[2 * slot + 1];
+            if (o0 != 0xFFFFFFFFu) {
+                bool h0 = false, h1 = false;
+                for (int e = lane; e < 2 * ring; e += 32) {
+                    if ((e >> 1) == slot) continue;
+                    const uint32_t x = RG[e];
+                    h0 |= x == o0;
+                    h1 |= x == o1;
+                }
+                h0 = __any_sync(0xFFFFFFFFu, h0);
+                h1 = __any_sync(0xFFFFFFFFu, h1);
+                if (lane == 0) {
+                    if (!h0) TB[o0 & 0xFFFF] &= ~(0x80000000u >> (o0 >> 16));
+                    if (o1 != 0xFFFFFFFFu && !h1) TB[o1 & 0xFFFF] &= ~(0x80000000u >> (o1 >> 16));
+                    RG[2 * slot] = RG[2 * slot + 1] = 0xFFFFFFFFu;
+                }
+                __syncwarp();
+            }
+        }
 
         // Per-lane best inside a tile (score.cuh); tiles merged through the 64-bit key.
         // ============================ relocate block ============================
         for (int t0 = 0; t0 < S; t0 += 32 * KR) {
-            const uint64_t kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
-                                     : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
+            uint64_t kb;
+            if constexpr (WIN) kb = score_reloc_win<TABU>(SC, W, t0, 0, n, it, asp, lane);
+            else kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
+                           : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
         }
         // ============================== swap block ==============================
@@ -320,8 +368,10 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         // lowest chunk is ragged; adjacent pairs are excluded there and scored exactly
         // by the generic three-link formula below.
         for (int hi = n; hi > 1; hi -= 32 * KS) {
-            const uint64_t kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
-                                     : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
+            uint64_t kb;
+            if constexpr (WIN) kb = score_swap_win<TABU>(SC, W, hi, 0, hi - 1, it, asp, lane);
+            else kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
+                           : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
         }
         // adjacent pairs (x, succ x): the exact three-link formula (engine.cuh)
@@ -330,7 +380,11 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
                 const int g = LK[x] & 0xFFFF;
                 if (R.veh[x] < 0 || g >= n) continue;
                 const int m1 = min(x, g), m2 = max(x, g);
-                const MoveEval e = swap_eval(M, R, m1, m2, mask, it);
+                MoveEval e = swap_eval(M, R0, m1, m2, mask, it);
+                if (WIN && TABU) {   // placed-into pairs (m1, veh m2), (m2, veh m1): the same route here
+                    const int v = R.veh[x];
+                    e.tabu = ((TB[m1] | TB[m2]) << v) >> 31;
+                }
                 const int cls = move_class<TABU>(e, cur, best);
                 if (cls >= 0) {
                     const uint64_t key = make_key(cls, e.delta, Rb + (uint32_t)m1 * (uint32_t)n + (uint32_t)m2);
@@ -347,7 +401,26 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
             else if (key_cls(kmin) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
             if (!stop) {
                 const uint32_t idx = key_idx(kmin);
-                MoveEval e = eval_index(M, R, idx, mask, it);
+                MoveEval e = eval_index(M, R0, idx, mask, it);
+                if (WIN && TABU) {
+                    // the 'from' pairs this move writes (O8): relocate (m, veh m); swap (m1, veh m1), (m2, veh m2)
+                    uint32_t p0, p1 = 0xFFFFFFFFu;
+                    if (idx < Rb) {
+                        const int m = idx / S;
+                        p0 = (uint32_t)m | ((uint32_t)R.veh[m] << 16);
+                    } else {
+                        const int m1 = (idx - Rb) / n, m2 = (idx - Rb) % n;
+                        p0 = (uint32_t)m1 | ((uint32_t)R.veh[m1] << 16);
+                        p1 = (uint32_t)m2 | ((uint32_t)R.veh[m2] << 16);
+                    }
+                    const int slot = it % ring;
+                    RG[2 * slot] = p0;
+                    RG[2 * slot + 1] = p1;
+                    if (A.tenure > 0) {   // E = it + tenure >= it + 1: tabu from the next iteration on
+                        TB[p0 & 0xFFFF] |= 0x80000000u >> (p0 >> 16);
+                        if (p1 != 0xFFFFFFFFu) TB[p1 & 0xFFFF] |= 0x80000000u >> (p1 >> 16);
+                    }
+                }
                 apply_move(M, R, idx, e, it, A.tenure, TABU);
                 cur += e.delta;
                 if (cur < best) {
@@ -403,15 +476,15 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         for (int i = lane; i < n * V; i += 32) A.tabu_out[(size_t)run * n * V + i] = (int32_t)E[i];
 }
 
-template <bool TABU, class TT, class ET, bool FULL>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN>
 __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, BatchLayout L, int NLp) {
-    batch_cta<TABU, TT, ET, FULL>(A, RPC, L, NLp, blockIdx.x * RPC);
+    batch_cta<TABU, TT, ET, FULL, WIN>(A, RPC, L, NLp, blockIdx.x * RPC);
 }
 
 // Several instances in one launch (as_batch_run_jobs): CTA b runs cta[b] = {job, first run
 // of the job, runs} with that job's instance staged in its shared memory; the per-run
 // output arrays are re-based to the CTA's first run.
-template <bool TABU, class TT, class ET, bool FULL>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN>
 __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch_jobs(SearchArgs A, const BatchJob *jobs, const int4 *cta) {
     const int4 c = cta[blockIdx.x];
     const BatchJob &J = jobs[c.x];
@@ -426,29 +499,30 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch_jobs(SearchArgs A, cons
     B.results = A.results ? A.results + r : nullptr;
     B.best_ptr = A.best_ptr ? A.best_ptr + J.bp_off + (size_t)c.y * (J.inst.V + 1) : nullptr;
     B.best_ms = A.best_ms ? A.best_ms + J.bm_off + (size_t)c.y * J.inst.n : nullptr;
+    B.E_global = A.E_global ? A.E_global + J.e_off + (size_t)c.y * J.inst.n * J.inst.V : nullptr;
     B.trace = A.trace ? A.trace + r * (size_t)A.max_iters : nullptr;
     B.digest = nullptr;
     B.tabu_out = nullptr;
-    batch_cta<TABU, TT, ET, FULL>(B, J.RPC, J.L, J.NLp, 0);
+    batch_cta<TABU, TT, ET, FULL, WIN>(B, J.RPC, J.L, J.NLp, 0);
 }
 
-template <bool TABU, class TT, class ET, bool FULL>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN = false>
 static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStream_t st) {
-    auto kern = k_batch<TABU, TT, ET, FULL>;
+    auto kern = k_batch<TABU, TT, ET, FULL, WIN>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     const DevInst &I = A.inst;
-    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU);
+    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU, WIN, A.tenure);
     int NLp = padded_stride(I.NL, (int)sizeof(TT));
     int grid = (A.n_runs + RPC - 1) / RPC;
     kern<<<grid, RPC * 32, smem, st>>>(A, RPC, L, NLp);
     return cudaGetLastError();
 }
 
-template <bool TABU, class TT, class ET, bool FULL>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN = false>
 static cudaError_t launch_jobs_t(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
                                  size_t smem, cudaStream_t st) {
-    auto kern = k_batch_jobs<TABU, TT, ET, FULL>;
+    auto kern = k_batch_jobs<TABU, TT, ET, FULL, WIN>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     kern<<<n_cta, threads, smem, st>>>(A, jobs, cta);
@@ -456,7 +530,10 @@ static cudaError_t launch_jobs_t(const SearchArgs &A, const BatchJob *jobs, cons
 }
 
 cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
-                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st) {
+                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st, bool win) {
+    if (win)   // window scorers: FULL, uint16 table, tabu matrix in global memory (int32)
+        return mode == 1 ? launch_jobs_t<true, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st)
+                         : launch_jobs_t<false, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st);
     if (mode == 1) {
         if (tbytes == 2 && ebytes == 2)
             return full ? launch_jobs_t<true, uint16_t, int16_t, true>(A, jobs, cta, n_cta, threads, smem, st)
@@ -471,13 +548,16 @@ cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const i
     return launch_jobs_t<false, int32_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st);
 }
 
-BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu) {
-    return batch_layout(n, V, NL, NC, tbytes, ebytes, tabu);
+BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, bool win, int tenure) {
+    return batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure);
 }
 
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool win) {
     const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
+    if (win)   // window scorers: FULL, uint16 table, tabu matrix in global memory (int32)
+        return mode == 1 ? launch_one<true, uint16_t, int32_t, true, true>(A, RPC, smem, st)
+                         : launch_one<false, uint16_t, int32_t, true, true>(A, RPC, smem, st);
     if (mode == 1) {
         if (tbytes == 2 && ebytes == 2)
             return full ? launch_one<true, uint16_t, int16_t, true>(A, RPC, smem, st)

@@ -47,6 +47,7 @@ struct BatchLayout {
     int T, CS, MH, VC, CH;   // CTA-wide part
     int shared_bytes;
     int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
+    int TB, RG, WB;                 // window scorers: tabu bits, tabu-write ring, window buffer
     int run_bytes;
 };
 
@@ -58,6 +59,7 @@ struct BatchJob {
     int NLp, RPC;                           // padded table stride, runs per CTA
     int run0;                               // global index of the job's first run
     int64_t bp_off, bm_off;                 // offsets of its runs' best schedules in the packed outputs
+    int64_t e_off;                          // offset of its runs' tabu matrices in SearchArgs::E_global (window scorers)
 };
 
 struct GridLayout {
@@ -124,11 +126,17 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
                              int n_sm, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st);
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes);
-cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st);
-BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu);
+                size_t *run_bytes, bool win = false, int tenure = 0);
+// win: the WINDOW scorers (window.cuh): every move kind, svcpos, uint16 table, V <= 32, tenure <= WIN_MAX_TENURE,
+// not the sweep; the tabu matrix is SearchArgs::E_global ([R][n][V] int32)
+constexpr int WIN_MAX_TENURE = 64;
+cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st,
+                         bool win = false);
+BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, bool win = false,
+                              int tenure = 0);
 cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
-                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st);
+                              size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st,
+                              bool win = false);
 size_t greedy_smem_bytes(const DevInst &I, int warps, bool T_smem, bool state_smem);
 size_t greedy_state_bytes(const DevInst &I);
 cudaError_t launch_greedy(const DevInst &I, int n_starts, int insert_mode, int max_repairs, const uint64_t *seeds,

@@ -1,0 +1,324 @@
+// window.cuh -- the WINDOW scorers of the batched kernel (k_batch, one run per
+// warp): the same moves, formulas and keys as score.cuh's FAST scorers, with
+// the warp-uniform per-row work taken out of the scoring loops.
+//
+// In a tile every lane scores the same row m (m1) against its own targets, so
+// everything that depends only on the row is the same for all 32 lanes.  The
+// FAST scorers recompute it per row in every lane (~60 SASS instructions per
+// row, and the register pressure of 28 warps x 72 registers makes the compiler
+// rematerialise part of it inside the item loop).  Here the rows are taken 32
+// at a time: lane j builds row (w0 + j)'s record once (lane-parallel), stores it
+// in the warp's window buffer, and the row loop reads it back with broadcast
+// LDS.128s.  Four more changes cut the per-move instruction count:
+//
+//  * tabu test by bitmask: TB[m] bit (31 - v) is set iff E[m][v] >= it (O8), so
+//    "placed-into pair (m, b) is tabu" is the sign bit of TB[m] << b -- one shift
+//    instead of a gather of the expiry matrix (which moves to global memory:
+//    the scorers never read it; apply writes it; V <= 32);
+//  * per-lane 32-bit key with a local index: bit 31 = not admissible, bits
+//    7..30 = delta + 2^23, bits 0..6 = the lane's item number inside the window
+//    (row * KR + k or row * KS + k, increasing with the canonical index), so
+//    the running best is one unsigned min; the window's winner is turned into
+//    the 64-bit (class, delta, index) key at the window's end.  Needs |delta| <
+//    2^23: true for uint16 tables (|delta| < 8 * 2^16);
+//  * feasibility margins combined by OR (the sign of a | b | c is set iff one
+//    of them is negative) and the infeasible poison by an arithmetic shift;
+//  * no same-route branch (reading #42): with every pickup->delivery
+//    leg > 0 (svcpos, required by the FAST scorers) a feasible route is strictly
+//    deadline-sorted, so every intra-route relocate or swap fails
+//    one of its new-link checks; the flight-limit margins therefore use the
+//    inter-route form for every move, and a row whose removal leaves route a
+//    over the flight limit (F_a + rem > P) has no feasible move at all and is
+//    skipped.  Results are identical; the parity suite checks traces bit-exact.
+#pragma once
+#include <cstdint>
+
+#include "score.cuh"
+
+namespace airsched {
+
+constexpr int WIN_ROWS = 32;                 // rows per window (one per lane)
+constexpr int WIN_REC_INT4 = 5;              // record size (int4 words) of the larger (swap) record
+constexpr int WIN_KEY_SHIFT = 7;             // local-index bits of the 32-bit key
+constexpr int WIN_BIAS = 1 << 23;            // delta bias of the 32-bit key
+constexpr uint32_t WIN_NONE = 0xFFFFFFFFu;
+constexpr int WIN_HELI_OFF = 1 << 30;        // lane slack offset: vehicle may not fly a heli-only mission
+
+struct WinCtx {
+    int4 *WB;               // [WIN_ROWS][WIN_REC_INT4] this warp's window buffer (shared)
+    const uint32_t *TB;     // [n] tabu bits: bit (31 - v) of TB[m] <=> E[m][v] >= it (TABU only)
+};
+
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {   // x << s, 0 when s >= 32 (PTX shl)
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+
+// 32-bit window key -> 64-bit key (class << 63 | (delta + 2^30) << 32 | idx)
+__device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
+    const uint32_t d = ((bk >> WIN_KEY_SHIFT) & 0xFFFFFFu) + (uint32_t)(DELTA_BIAS - WIN_BIAS);
+    return ((uint64_t)((bk & 0x80000000u) | d) << 32) | idx;
+}
+
+// ---------------------------------------------------------------------------
+// Relocate block.  Record of row m (4 int4):
+//   q0 = {remk[0..3]}      (rem + 2^23) << 7 | (r * KR + k): the key base of item k
+//   q1 = {hmask, w_m, -w_m, rowP}   hmask = 0: row has no feasible move (skip);
+//                                   else 0x3FFFFFFF (m not heli-only) or ~0 (heli-only)
+//   q2 = {rowD, svc0_m, svc1_m - svc0_m, TB[m]}
+//   q3 = {rem - asp (TS) or rem (NS), 0, 0, 0}
+template <bool TABU>
+__device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m, int r,
+                                                 int asp, int tsz) {
+    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0), q3 = make_int4(0, 0, 0, 0);
+    const int4 rm = C.RS4[m];
+    const int a = (int16_t)((uint32_t)rm.w >> 16);
+    if (a >= 0) {
+        const int s = C.LK[m] & 0xFFFF;
+        const int4 rsx = C.RS4[s];
+        const int4 csx = C.CS4[s];
+        const int ca = C.VC[a] & 0xFF;
+        const int Dps = (int)C.Ts[(ca * C.NL + (rm.w & 0xFFFF)) * C.NLp + (csx.y & 0xFFFF)] + rsx.z;
+        const int rem = Dps - rm.y - rsx.y;   // removal delta d(p,s) - d(p,m) - d(m,s)
+        // link p->s (con7/con8) and route a's flight total after the removal (con6, reading #42)
+        if (rm.x + Dps <= csx.x && C.F[a] + rem <= C.P) {
+            const int4 cm = C.CS4[m];
+            const int kb = (rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR;
+            q0 = make_int4(kb, kb + 1, kb + 2, kb + 3);
+            q1 = make_int4(C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF, cm.x, -cm.x, tsz * (cm.y & 0xFFFF));
+            q2 = make_int4(tsz * (int)((uint32_t)cm.y >> 16) * C.NLp, cm.z, cm.w - cm.z, TABU ? (int)W.TB[m] : 0);
+            q3 = make_int4(TABU ? rem - asp : rem, 0, 0, 0);
+        }
+    }
+    int4 *rec = W.WB + r * WIN_REC_INT4;
+    rec[0] = q0; rec[1] = q1; rec[2] = q2; rec[3] = q3;
+}
+
+template <bool TABU>
+__device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int t0,
+                                                    int m_lo, int m_hi, int it, int asp, int lane) {
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint32_t *VC = C.VC;
+    const int S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
+    const int one = C.one, neg = C.neg;
+    const int tsm = (int)__cvta_generic_to_shared(C.Ts), tsz = 2;
+    // target-slot side, per lane (as score_reloc_fast); c_slk carries the heli offset
+    int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
+#pragma unroll
+    for (int k = 0; k < KR; k++) {
+        const int t = t0 + lane + 32 * k;
+        int t1 = tsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF, cb = 0;
+        if (t < S) {
+            const int4 rs = RS4[t];
+            const int bb = (int16_t)((uint32_t)rs.w >> 16);
+            if (bb >= 0) {
+                const int4 cs = CS4[t];
+                const uint32_t vc = VC[bb];
+                b = bb;
+                cb = vc & 0xFF;
+                t1 = tsm + tsz * ((cb * NL + (rs.w & 0xFFFF)) * NLp);   // row endc(t) of T_cb (column pick_m)
+                t2 = tsm + tsz * (cb * NL * NLp + (cs.y & 0xFFFF));     // column pick(t) of T_cb (row del_m)
+                dw = -rs.x;                                             // -dep(pred t)
+                kk = rs.z - rs.y;                                       // svco(t) - inc(t)
+                wsv = cs.x - rs.z;                                      // w(t) - svco(t)
+                slk = (P - C.F[bb]) - (((vc >> 8) & 1) ? 0 : WIN_HELI_OFF);
+            }
+        }
+        c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
+        c_cb[k] = cb;
+    }
+    uint64_t best = KEY_NONE;
+    for (int w0 = m_lo; w0 < m_hi; w0 += WIN_ROWS) {
+        __syncwarp();
+        if (w0 + lane < m_hi) win_reloc_record<TABU>(C, W, w0 + lane, lane, asp, tsz);
+        __syncwarp();
+        const int nr = min(WIN_ROWS, m_hi - w0);
+        uint32_t bk = WIN_NONE;
+        for (int r = 0; r < nr; r++) {
+            const int4 *rec = W.WB + r * WIN_REC_INT4;
+            const int4 q1 = rec[1];
+            const int hmask = q1.x;
+            if (hmask == 0) continue;
+            const int4 q0 = rec[0], q2 = rec[2], q3 = rec[3];
+            const int remk[KR] = {q0.x, q0.y, q0.z, q0.w};
+            const int w_m = q1.y, wm_neg = q1.z, rowP = q1.w;
+            const int rowD = q2.x, svm0 = q2.y, dsvm = q2.z;
+            const uint32_t tb = (uint32_t)q2.w;
+            const int remasp = q3.x;
+#pragma unroll
+            for (int k = 0; k < KR; k++) {
+                const int T1 = lds_t<uint16_t>((uint32_t)madd(c_t1[k], one, rowP));   // T_cb[endc t][pick m]
+                const int T2 = lds_t<uint16_t>((uint32_t)madd(c_t2[k], one, rowD));   // T_cb[del m][pick t]
+                const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));               // d(c, m)
+                const int ins = madd(x1, one, madd(T2, one, c_k[k]));                  // insertion delta
+                const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));                // dep(c) + d(c,m) <= w_m
+                const int mB = madd(T2, neg, madd(c_wsv[k], one, wm_neg));            // w_m + d(m,t) <= w(t)
+                const int mC = madd(ins, neg, c_slk[k] & hmask);                       // F_b + ins <= P (+ heli)
+                const int mg = mA | mB | mC;
+                const int e2 = madd(ins, one, remasp);                                 // delta - asp (TS) / delta (NS)
+                uint32_t nadm;
+                if (TABU) nadm = shl_clamp(tb, (uint32_t)c_b[k]) & ~(uint32_t)e2 & 0x80000000u;
+                else nadm = ~(uint32_t)e2 & 0x80000000u;
+                const uint32_t k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk[k]) | nadm | (uint32_t)(mg >> 31);
+                bk = min(bk, k32);
+            }
+        }
+        if (bk != WIN_NONE) {
+            const int lid = bk & ((1 << WIN_KEY_SHIFT) - 1);
+            const uint32_t idx = (uint32_t)(w0 + lid / KR) * (uint32_t)S + (uint32_t)(t0 + lane + 32 * (lid % KR));
+            const uint64_t key = win_key64(bk, idx);
+            best = key < best ? key : best;
+        }
+    }
+    return best;
+}
+
+// ---------------------------------------------------------------------------
+// Swap block (non-adjacent pairs m1 < m2; m2 over the lanes in a top-aligned chunk
+// of 32 * KS, as score_swap_fast).  Record of row m1 (5 int4):
+//   q0 = {a (-1: skip), ca, row_ya1, row_ta2}
+//   q1 = {rowP, rowD, -depc1, w1}
+//   q2 = {w(s1) - svco(s1), svco(s1) - inc1 - inc(s1), P - F_a, svc0_1}
+//   q3 = {svc1_1 - svc0_1, cmask, TB[m1], -m1 - 1}
+//   q4 = {keyb0, keyb1, hmask, -asp (TS) or 0 (NS)}
+template <bool TABU>
+__device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m1, int r,
+                                                int asp, int tsm, int tsz) {
+    int4 q0 = make_int4(-1, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0), q3 = make_int4(0, 0, 0, 0),
+         q4 = make_int4(0, 0, 0, 0);
+    const int4 r1 = C.RS4[m1];
+    const int a = (int16_t)((uint32_t)r1.w >> 16);
+    if (a >= 0) {
+        const int s1 = C.LK[m1] & 0xFFFF;
+        const int4 c1 = C.CS4[m1];
+        const int4 rs1 = C.RS4[s1];
+        const int4 cs1 = C.CS4[s1];
+        const uint32_t vca = C.VC[a];
+        const int ca = vca & 0xFF;
+        q0 = make_int4(a, ca, tsm + tsz * ((ca * C.NL + (r1.w & 0xFFFF)) * C.NLp),   // T_ca[endc1][.]
+                       tsm + tsz * (ca * C.NL * C.NLp + (cs1.y & 0xFFFF)));           // T_ca[.][pick(s1)]
+        q1 = make_int4(tsz * (c1.y & 0xFFFF), tsz * (int)((uint32_t)c1.y >> 16) * C.NLp, -r1.x, c1.x);
+        q2 = make_int4(cs1.x - rs1.z, rs1.z - r1.y - rs1.y, C.P - C.F[a], c1.z);
+        // m2 heli-only needs route a heli-capable: bit 31 of (bf & cmask)
+        q3 = make_int4(c1.w - c1.z, ((vca >> 8) & 1) ? 0 : (int)0x80000000, TABU ? (int)W.TB[m1] : 0, -m1 - 1);
+        const int kb = (1 << 30) + r * KS;    // (0 + 2^23) << 7 | local index
+        q4 = make_int4(kb, kb + 1, C.MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF, TABU ? -asp : 0);
+    }
+    int4 *rec = W.WB + r * WIN_REC_INT4;
+    rec[0] = q0; rec[1] = q1; rec[2] = q2; rec[3] = q3; rec[4] = q4;
+}
+
+template <bool TABU>
+__device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int hi,
+                                                   int m1_lo, int m1_hi, int it, int asp, int lane) {
+    const int4 *CS4 = C.CS4, *RS4 = C.RS4;
+    const uint8_t *MH = C.MH;
+    const uint32_t *VC = C.VC, *LK = C.LK;
+    const int n = C.n, NL = C.NL, NLp = C.NLp, P = C.P;
+    const uint32_t Rb = C.Rb;
+    const int one = C.one, neg = C.neg;
+    const int lo = hi - 32 * KS;
+    const int tsm = (int)__cvta_generic_to_shared(C.Ts), tsz = 2;
+    // m2 side, per lane (as score_swap_fast); q_bf = b | heli_only(m2) << 31, q_slk carries the heli offset
+    int q_p2m[KS], q_sv0[KS], q_dsv[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS],
+        q_slk[KS], q_bf[KS], q_cb[KS];
+    uint32_t q_tb[KS];
+#pragma unroll
+    for (int k = 0; k < KS; k++) {
+        const int m2 = lo + lane + 32 * k;
+        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = tsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0,
+            bf = 0xFFFF, cb = 0;
+        uint32_t tb = 0;
+        if (m2 >= 0) {
+            const int4 r2 = RS4[m2];
+            const int b = (int16_t)((uint32_t)r2.w >> 16);
+            if (b >= 0) {
+                const int4 c2 = CS4[m2];
+                const uint32_t vc = VC[b];
+                cb = vc & 0xFF;
+                const int s2 = LK[m2] & 0xFFFF;
+                const int4 rs2 = RS4[s2];
+                const int4 cs2 = CS4[s2];
+                p2m = tsz * (c2.y & 0xFFFF);                                // pick2
+                sv0 = c2.z;
+                dsv = c2.w - c2.z;
+                d2 = tsz * (int)((uint32_t)c2.y >> 16) * NLp;               // row del2 of T (column pick(s1))
+                e2 = tsm + tsz * ((cb * NL + (r2.w & 0xFFFF)) * NLp);       // row endc2 of T_cb (column pick1)
+                p2 = tsm + tsz * (cb * NL * NLp + (cs2.y & 0xFFFF));        // column pick(s2) of T_cb
+                w2 = c2.x;
+                dep2 = r2.x;
+                kb = rs2.z - r2.y - rs2.y;                                  // svco(s2) - inc2 - inc(s2)
+                ws2 = cs2.x - rs2.z;                                        // w(s2) - svco(s2)
+                slk = (P - C.F[b]) - (((vc >> 8) & 1) ? 0 : WIN_HELI_OFF);
+                bf = b | (MH[m2] ? (int)0x80000000 : 0);
+                if (TABU) tb = W.TB[m2];
+            }
+        }
+        q_p2m[k] = p2m; q_sv0[k] = sv0; q_dsv[k] = dsv; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2;
+        q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_cb[k] = cb; q_tb[k] = tb;
+    }
+    const int lane_lo = lo + lane;
+    uint64_t best = KEY_NONE;
+    for (int w0 = m1_lo; w0 < m1_hi; w0 += WIN_ROWS) {
+        __syncwarp();
+        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, asp, tsm, tsz);
+        __syncwarp();
+        const int nr = min(WIN_ROWS, m1_hi - w0);
+        uint32_t bk = WIN_NONE;
+        for (int r = 0; r < nr; r++) {
+            const int4 *rec = W.WB + r * WIN_REC_INT4;
+            const int4 q0 = rec[0];
+            const int a = q0.x;
+            if (a < 0) continue;
+            const int m1 = w0 + r;
+            const int4 q1 = rec[1], q2 = rec[2], q3 = rec[3], q4 = rec[4];
+            const int ca = q0.y, row_ya1 = q0.z, row_ta2 = q0.w;
+            const int rowP = q1.x, rowD = q1.y, ndepc1 = q1.z, w1 = q1.w;
+            const int wsv1 = q2.x, ka = q2.y, slkA = q2.z, sv10 = q2.w;
+            const int dsv1 = q3.x, cmask = q3.y;
+            const uint32_t tb1 = (uint32_t)q3.z;
+            const int tri = q3.w;
+            const int keyb[KS] = {q4.x, q4.y};
+            const int hmask = q4.z, nasp = q4.w;
+#pragma unroll
+            for (int k = 0; k < KS; k++) {
+                if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+                const int bf = q_bf[k];
+                const uint32_t b = (uint32_t)bf & 0xFFFFu;
+                const int Tya1 = lds_t<uint16_t>((uint32_t)madd(row_ya1, one, q_p2m[k]));   // T_ca[endc1][pick2]
+                const int Ta2 = lds_t<uint16_t>((uint32_t)madd(row_ta2, one, q_d2[k]));     // T_ca[del2][pick(s1)]
+                const int Tyb1 = lds_t<uint16_t>((uint32_t)madd(q_e2[k], one, rowP));       // T_cb[endc2][pick1]
+                const int Tb2 = lds_t<uint16_t>((uint32_t)madd(q_p2[k], one, rowD));        // T_cb[del1][pick(s2)]
+                const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));              // d_a(p1, m2)
+                const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                 // d_b(p2, m1)
+                const int da = madd(ya1, one, madd(Ta2, one, ka));
+                const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
+                const int delta = madd(da, one, db);
+                const int mfA = madd(da, neg, slkA);                                        // F_a + da <= P
+                const int mfB = madd(db, neg, q_slk[k] & hmask);                            // F_b + db <= P (+ heli)
+                const int l1 = madd(ya1, neg, madd(q_w2[k], one, ndepc1));                  // dep(p1) + ya1 <= w2
+                const int l2 = madd(Ta2, neg, madd(q_w2[k], neg, wsv1));                    // w2 + d(m2,s1) <= w(s1)
+                const int l3 = madd(yb1, neg, madd(q_dep2[k], neg, w1));                    // dep(p2) + yb1 <= w1
+                const int l4 = madd(Tb2, neg, madd(w1, neg, q_ws2[k]));                     // w1 + d(m1,s2) <= w(s2)
+                const int trim = lane_lo + 32 * k + tri;                                    // m2 - m1 - 1 >= 0
+                const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
+                const int e2 = madd(delta, one, nasp);
+                uint32_t nadm;
+                if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)e2 & 0x80000000u;
+                else nadm = ~(uint32_t)e2 & 0x80000000u;
+                const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb[k]) | nadm | (uint32_t)(mg >> 31);
+                bk = min(bk, k32);
+            }
+        }
+        if (bk != WIN_NONE) {
+            const int lid = bk & ((1 << WIN_KEY_SHIFT) - 1);
+            const uint32_t idx = Rb + (uint32_t)(w0 + lid / KS) * (uint32_t)n + (uint32_t)(lo + lane + 32 * (lid % KS));
+            const uint64_t key = win_key64(bk, idx);
+            best = key < best ? key : best;
+        }
+    }
+    return best;
+}
+
+}  // namespace airsched

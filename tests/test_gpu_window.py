@@ -1,0 +1,111 @@
+"""GPU parity of the batched kernel's WINDOW scorers (csrc/window.cuh).
+
+The window path (every move kind, positive service legs, uint16 table, V <= 32,
+tenure <= 64) keeps the tabu expiry matrix in global memory and tests tabu
+through per-mission bit masks maintained from a ring of the last tenure + 1
+iterations' writes (O8); it skips the same-route flight branch by the F2
+reading (#42).  Checked here, bit-exact against the CPU oracle:
+full traces, final tabu matrices and best schedules over tenures that stress
+the ring (0, 1, 2, the default 10, the limit 64, and 65 which falls back to the
+shared-memory tabu matrix), strict tabu stop, NS; and the window kernel against
+the FAST kernel (AIRSCHED_WIN=0) on whole batches.
+"""
+import numpy as np
+import pytest
+
+from paper_2002_11710_b200 import instgen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2002_11710_b200 import airsched
+    return airsched
+
+
+@pytest.fixture(scope="module")
+def ctx(A):
+    return A.Ctx(0)
+
+
+def routes_of(ptr, ms):
+    return [list(map(int, ms[ptr[v]:ptr[v + 1]])) for v in range(len(ptr) - 1)]
+
+
+def start_of(O, inst):
+    st, (p, m), _, _ = O.greedy()
+    if st != 0:
+        p, m = inst.planted_ptr, inst.planted_missions
+    return p, m
+
+
+@pytest.mark.parametrize("cfg,iters", [("tiny", 200), ("ontario", 600), ("batched", 400)])
+@pytest.mark.parametrize("tenure", [0, 1, 2, 10, 64, 65])
+def test_window_single_run_trace(A, ctx, oracle_mod, cfg, iters, tenure, monkeypatch):
+    """One run on the batched kernel: every chosen move, the objective trace, the
+    final tabu matrix and the best schedule equal the oracle's."""
+    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    for seed, kick in ((0, 0), (7, 5)):
+        prm = A.params(mode=1, tenure=tenure, max_iters=iters, trace_level=1, seed=seed, kick=kick)
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)
+        o = O.search(p, m, mode=1, tenure=tenure, max_iters=iters, seed=seed, kick=kick)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        assert (g["trace"]["idx"] == o["trace"]["idx"]).all()
+        assert (g["trace"]["cur"] == o["trace"]["cur"]).all() and (g["trace"]["cls"] == o["trace"]["cls"]).all()
+        assert (g["tabu"] == o["E"]).all()
+        assert g["best_obj"] == o["best_obj"] and g["best_iter"] == o["best_iter"]
+        assert routes_of(*g["best"]) == routes_of(*o["best"])
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "ontario"])
+def test_window_strict_stop_and_ns(A, ctx, oracle_mod, cfg, monkeypatch):
+    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    for tenure in (1, 5, 30):
+        prm = A.params(mode=1, tenure=tenure, max_iters=300, trace_level=1, strict_tabu_stop=1)
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)
+        o = O.search(p, m, mode=1, tenure=tenure, max_iters=300, strict_tabu_stop=True)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and (g["tabu"] == o["E"]).all()
+    for seed in (0, 3):
+        prm = A.params(mode=0, max_iters=500, trace_level=1, seed=seed, kick=6)
+        g = A.as_nbhd_run(ctx, h, p, m, prm, want_trace=True)
+        o = O.search(p, m, mode=0, max_iters=500, seed=seed, kick=6)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and g["best_obj"] == o["best_obj"]
+
+
+@pytest.mark.parametrize("mode,tenure", [(1, 10), (1, 0), (1, 64), (0, 0)])
+def test_window_equals_fast_kernel(A, ctx, mode, tenure, monkeypatch):
+    """Whole batches: the window kernel and the FAST kernel (AIRSCHED_WIN=0) give the
+    same results, traces and best schedules for every run."""
+    inst = instgen.generate("batched")
+    h = A.Instance(inst)
+    gp, gm, _ = A.as_init_greedy(ctx, h)
+    R, iters = 296, 150
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    out = []
+    for win in ("1", "0"):
+        monkeypatch.setenv("AIRSCHED_WIN", win)
+        res = np.zeros(R, A.RESULT_DTYPE)
+        tr = np.zeros((R, iters), A.TRACE_DTYPE)
+        bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
+        bm = np.zeros((R, inst.n_missions), np.int32)
+        prm = A.params(mode=mode, tenure=tenure, max_iters=iters, kick=8, trace_level=1)
+        A.as_batch_run(ctx, h, R, gp, gm, prm, seeds, shared_start=True, results=res, best_ptr_out=bp,
+                       best_missions_out=bm, trace_out=tr)
+        out.append((res, tr, bp, bm))
+    (r1, t1, p1, m1), (r0, t0, p0, m0) = out
+    assert (r1 == r0).all() and (t1 == t0).all() and (p1 == p0).all() and (m1 == m0).all()
+    assert len(set(r1["best_obj"].tolist())) > 1   # the runs differ (seeded kicks)
