@@ -53,6 +53,7 @@ struct as_instance {
     std::vector<uint8_t> cls_heli, heli, vcls8;
     int32_t maxT = 0;
     int32_t tsym = 1;      // T[c][a][b] == T[c][b][a] for every layer
+    int64_t tdmax = 0;     // max over c, x, m of T_c[x][pick_m] + T_c[pick_m][del_m]
 };
 
 static uint64_t g_uid = 1;
@@ -114,6 +115,15 @@ extern "C" as_status as_instance_create(const as_instance_desc *d, as_instance *
         if (I->w[m] < 1 || I->w[m] > d->day_length_s)
             return fail(AS_ERR_INVALID_ARG, "deadline of mission %lld outside [1, day_length] (S:111)", (long long)m);
         if (I->heli[m] > 1) return fail(AS_ERR_INVALID_ARG, "heli_only must be 0/1");
+    }
+    // largest node cost d_c(x, m) = T_c[x][pick_m] + T_c[pick_m][del_m] (O2): the window scorers stage
+    // these as uint16 (batch.cu), so they need tdmax <= 65535
+    for (int64_t c = 0; c < NC; c++) {
+        std::vector<int32_t> colmax(NL, 0);
+        for (int64_t a = 0; a < NL; a++)
+            for (int64_t b = 0; b < NL; b++) colmax[b] = std::max(colmax[b], I->T[(c * NL + a) * NL + b]);
+        for (int64_t m = 0; m < n; m++)
+            I->tdmax = std::max<int64_t>(I->tdmax, (int64_t)colmax[I->pick[m]] + I->T[(c * NL + I->pick[m]) * NL + I->del[m]]);
     }
     I->uid = __atomic_fetch_add(&g_uid, 1, __ATOMIC_RELAXED);
     *out = I.release();
@@ -679,10 +689,10 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
     // window scorers (window.cuh) for the batched kernel: every move kind, positive service legs, uint16 table,
     // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
-    const bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && V <= 32 && !P->sweep &&
+    const bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
                      (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
     size_t sh_b = 0, run_b = 0;
-    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure);
+    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure, I->tsym != 0);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
     // the compact-layout kernels (k_batch, k_grid) score the waiting model only;
     // the no-wait variant (f3) runs on k_search
@@ -943,7 +953,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     for (int j = 0; j < n_jobs && win; j++) {
         const DevInst *D;
         if ((st = get_dev_inst(ctx, jobs[j].inst, &D)) != AS_OK) return st;
-        if (D->svcpos && jobs[j].inst->V > 32) win = false;
+        if (D->svcpos && (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535)) win = false;
     }
     int64_t run0 = 0, bp0 = 0, bm0 = 0, e0 = 0;
     for (int j = 0; j < n_jobs; j++) {
@@ -953,7 +963,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         BatchJob &b = J[j];
         b.inst = *D;
         const bool wj = win && D->svcpos;
-        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu, wj, P->tenure);
+        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu, wj, P->tenure, I->tsym != 0);
         b.e_off = e0;
         if (wj && tabu) e0 += (int64_t)jobs[j].n_runs * I->n * I->V;
         b.NLp = padded_stride_host(I->NL, tbytes);

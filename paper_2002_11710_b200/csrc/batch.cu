@@ -35,7 +35,7 @@ constexpr int MAXTHREADS = 896;    // <= 28 runs per CTA (one wave of 4096 runs 
 // holds the tabu bits TB[n], the ring of the last tenure + 1 iterations' tabu writes and the
 // warp's window buffer instead.
 __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
-                                                   bool win = false, int tenure = 0) {
+                                                   bool win = false, int tenure = 0, bool tsym = true) {
     BatchLayout L;
     const int S = n + V;
     const int NLp = padded_stride(NL, tbytes);
@@ -45,6 +45,8 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.MH = o; o = al16(o + n);
     L.VC = o; o = al16(o + V * 4);
     L.CH = o; o = al16(o + NC);
+    L.TT = o; o = al16(o + (win && !tsym ? NC * NL * NLp * tbytes : 0));   // transposed table (window scorers)
+    L.TD = o; o = al16(o + (win ? NC * NL * padded_stride(n, 2) * 2 : 0));  // node costs d_c(x, m) (window scorers)
     L.shared_bytes = o;
     int r = 0;
     L.RS = r; r = al16(r + S * 16);
@@ -62,8 +64,8 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
 }
 
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes, bool win, int tenure) {
-    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure);
+                size_t *run_bytes, bool win, int tenure, bool tsym) {
+    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure, tsym);
     *shared_bytes = L.shared_bytes;
     *run_bytes = L.run_bytes;
 }
@@ -89,6 +91,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     for (int i = tid; i < NC * NL * NL; i += blockDim.x) {
         int c = i / (NL * NL), r = (i / NL) % NL, col = i % NL;
         Ts[(c * NL + r) * NLp + col] = (TT)I.T[i];
+        if (WIN && !I.tsym) reinterpret_cast<TT *>(smem + L.TT)[(c * NL + col) * NLp + r] = (TT)I.T[i];
     }
     for (int x = tid; x < S; x += blockDim.x) {
         int4 r;
@@ -111,6 +114,14 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         VC[i] = (uint32_t)c | ((uint32_t)I.cls_heli[c] << 8) | ((uint32_t)I.vloc[i] << 16);
     }
     for (int i = tid; i < NC; i += blockDim.x) CH[i] = I.cls_heli[i];
+    if (WIN) {   // node costs d_c(x, m) = T_c[x][pick_m] + T_c[pick_m][del_m] (O2), uint16 (tdmax checked on the host)
+        const int NTDp = padded_stride(n, 2);
+        uint16_t *TD = reinterpret_cast<uint16_t *>(smem + L.TD);
+        for (int i = tid; i < NC * NL * n; i += blockDim.x) {
+            const int c = i / (NL * n), x = (i / n) % NL, m = i % n;
+            TD[(c * NL + x) * NTDp + m] = (uint16_t)(I.T[(c * NL + x) * NL + I.pick[m]] + I.svc[c * n + m]);
+        }
+    }
     __syncthreads();
 
     const int run = cta_run0 + warp;
@@ -242,6 +253,9 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     WinCtx W;
     W.WB = WIN ? reinterpret_cast<int4 *>(rb + L.WB) : nullptr;
     W.TB = TB;
+    W.ttsm = (int)__cvta_generic_to_shared(WIN && !I.tsym ? (const void *)(smem + L.TT) : (const void *)Ts);
+    W.tdsm = (int)__cvta_generic_to_shared(smem + L.TD);
+    W.NTDp = padded_stride(n, 2);
     const int ring = A.tenure + 1;
     int it = 0, stop = 0;
     if (A.sweep) {
@@ -512,7 +526,7 @@ static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStr
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     const DevInst &I = A.inst;
-    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU, WIN, A.tenure);
+    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU, WIN, A.tenure, I.tsym);
     int NLp = padded_stride(I.NL, (int)sizeof(TT));
     int grid = (A.n_runs + RPC - 1) / RPC;
     kern<<<grid, RPC * 32, smem, st>>>(A, RPC, L, NLp);
@@ -548,8 +562,9 @@ cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const i
     return launch_jobs_t<false, int32_t, int16_t, false>(A, jobs, cta, n_cta, threads, smem, st);
 }
 
-BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, bool win, int tenure) {
-    return batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure);
+BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, bool win, int tenure,
+                              bool tsym) {
+    return batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure, tsym);
 }
 
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,

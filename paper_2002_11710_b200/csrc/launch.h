@@ -44,7 +44,8 @@ struct SearchArgs {
 constexpr int GRID_WARPS = 24;   // k_grid warps per CTA (one CTA per SM; <= 85 registers per thread; 28 measured slower)
 
 struct BatchLayout {
-    int T, CS, MH, VC, CH;   // CTA-wide part
+    int T, CS, MH, VC, CH, TT, TD;   // CTA-wide part (window scorers: TT transposed table when asymmetric,
+                                     // TD node costs d_c(x, m))
     int shared_bytes;
     int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
     int TB, RG, WB;                 // window scorers: tabu bits, tabu-write ring, window buffer
@@ -126,14 +127,14 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
                              int n_sm, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st);
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes, bool win = false, int tenure = 0);
+                size_t *run_bytes, bool win = false, int tenure = 0, bool tsym = true);
 // win: the WINDOW scorers (window.cuh): every move kind, svcpos, uint16 table, V <= 32, tenure <= WIN_MAX_TENURE,
 // not the sweep; the tabu matrix is SearchArgs::E_global ([R][n][V] int32)
 constexpr int WIN_MAX_TENURE = 64;
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem, cudaStream_t st,
                          bool win = false);
 BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, bool win = false,
-                              int tenure = 0);
+                              int tenure = 0, bool tsym = true);
 cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
                               size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st,
                               bool win = false);

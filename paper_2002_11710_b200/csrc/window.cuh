@@ -15,6 +15,16 @@
 //    "placed-into pair (m, b) is tabu" is the sign bit of TB[m] << b -- one shift
 //    instead of a gather of the expiry matrix (which moves to global memory:
 //    the scorers never read it; apply writes it; V <= 32);
+//  * node costs staged per CTA: TD_c[x][m] = d_c(x, m) = T_c[x][pick_m] +
+//    T_c[pick_m][del_m] (O2, uint16; the host checks the largest fits), so
+//    the cost of arriving at a mission is one gather instead of a gather, the
+//    service leg of the right class and two adds; the swap's d_a(p1, m2) reads
+//    one TD row over consecutive lanes (no bank conflicts);
+//  * row-local table read where a gather would read down a column: the swap's
+//    T_ca[del m2][pick s1] is read from the per-layer transpose (T itself when
+//    every layer is symmetric, else a transposed copy staged next to T);
+//  * sums as 3-input adds (IADD3, ALU pipe) or mad.lo (FMA pipe), split so
+//    neither half-rate pipe limits the issue rate;
 //  * per-lane 32-bit key with a local index: bit 31 = not admissible, bits
 //    7..30 = delta + 2^23, bits 0..6 = the lane's item number inside the window
 //    (row * KR + k or row * KS + k, increasing with the canonical index), so
@@ -38,7 +48,7 @@
 namespace airsched {
 
 constexpr int WIN_ROWS = 32;                 // rows per window (one per lane)
-constexpr int WIN_REC_INT4 = 5;              // record size (int4 words) of the larger (swap) record
+constexpr int WIN_REC_INT4 = 3;              // record size (int4 words) of the larger (swap) record
 constexpr int WIN_KEY_SHIFT = 7;             // local-index bits of the 32-bit key
 constexpr int WIN_BIAS = 1 << 23;            // delta bias of the 32-bit key
 constexpr uint32_t WIN_NONE = 0xFFFFFFFFu;
@@ -47,6 +57,9 @@ constexpr int WIN_HELI_OFF = 1 << 30;        // lane slack offset: vehicle may n
 struct WinCtx {
     int4 *WB;               // [WIN_ROWS][WIN_REC_INT4] this warp's window buffer (shared)
     const uint32_t *TB;     // [n] tabu bits: bit (31 - v) of TB[m] <=> E[m][v] >= it (TABU only)
+    int ttsm;               // shared-window byte address of the transposed table (== the table's when symmetric)
+    int tdsm;               // shared-window byte address of TD[NC][NL][NTDp] (uint16 node costs)
+    int NTDp;               // TD row stride (halfwords)
 };
 
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {   // x << s, 0 when s >= 32 (PTX shl)
@@ -62,16 +75,16 @@ __device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
 }
 
 // ---------------------------------------------------------------------------
-// Relocate block.  Record of row m (4 int4):
-//   q0 = {remk[0..3]}      (rem + 2^23) << 7 | (r * KR + k): the key base of item k
-//   q1 = {hmask, w_m, -w_m, rowP}   hmask = 0: row has no feasible move (skip);
-//                                   else 0x3FFFFFFF (m not heli-only) or ~0 (heli-only)
-//   q2 = {rowD, svc0_m, svc1_m - svc0_m, TB[m]}
-//   q3 = {rem - asp (TS) or rem (NS), 0, 0, 0}
+// Relocate block: move m (route a, p -> m -> s) to just before slot t (route b, c -> t).
+// Record of row m (2 int4):
+//   q0 = {remk, hmask, w_m, rowD}   remk = (rem + 2^23) << 7 | r * KR (key base; item k adds k);
+//        hmask = 0: row has no feasible move (skip); else 0x3FFFFFFF (m not heli-only) or ~0
+//        (heli-only); rowD = byte offset of table row del_m
+//   q1 = {TB[m], rem - asp (TS) or rem (NS), 2 m, 0}
 template <bool TABU>
 __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m, int r,
-                                                 int asp, int tsz) {
-    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0), q3 = make_int4(0, 0, 0, 0);
+                                                 int asp) {
+    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0);
     const int4 rm = C.RS4[m];
     const int a = (int16_t)((uint32_t)rm.w >> 16);
     if (a >= 0) {
@@ -84,15 +97,13 @@ __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_
         // link p->s (con7/con8) and route a's flight total after the removal (con6, reading #42)
         if (rm.x + Dps <= csx.x && C.F[a] + rem <= C.P) {
             const int4 cm = C.CS4[m];
-            const int kb = (rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR;
-            q0 = make_int4(kb, kb + 1, kb + 2, kb + 3);
-            q1 = make_int4(C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF, cm.x, -cm.x, tsz * (cm.y & 0xFFFF));
-            q2 = make_int4(tsz * (int)((uint32_t)cm.y >> 16) * C.NLp, cm.z, cm.w - cm.z, TABU ? (int)W.TB[m] : 0);
-            q3 = make_int4(TABU ? rem - asp : rem, 0, 0, 0);
+            q0 = make_int4((rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR, C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF,
+                           cm.x, 2 * (int)((uint32_t)cm.y >> 16) * C.NLp);
+            q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m, 0);
         }
     }
     int4 *rec = W.WB + r * WIN_REC_INT4;
-    rec[0] = q0; rec[1] = q1; rec[2] = q2; rec[3] = q3;
+    rec[0] = q0; rec[1] = q1;
 }
 
 template <bool TABU>
@@ -102,65 +113,61 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
     const uint32_t *VC = C.VC;
     const int S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
     const int one = C.one, neg = C.neg;
-    const int tsm = (int)__cvta_generic_to_shared(C.Ts), tsz = 2;
-    // target-slot side, per lane (as score_reloc_fast); c_slk carries the heli offset
-    int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
+    const int tsm = (int)__cvta_generic_to_shared(C.Ts);
+    // target-slot side, per lane; c_slk carries the heli offset
+    int c_x1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR];
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
-        int t1 = tsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF, cb = 0;
+        int x1 = W.tdsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF;
         if (t < S) {
             const int4 rs = RS4[t];
             const int bb = (int16_t)((uint32_t)rs.w >> 16);
             if (bb >= 0) {
                 const int4 cs = CS4[t];
                 const uint32_t vc = VC[bb];
+                const int cb = vc & 0xFF;
                 b = bb;
-                cb = vc & 0xFF;
-                t1 = tsm + tsz * ((cb * NL + (rs.w & 0xFFFF)) * NLp);   // row endc(t) of T_cb (column pick_m)
-                t2 = tsm + tsz * (cb * NL * NLp + (cs.y & 0xFFFF));     // column pick(t) of T_cb (row del_m)
-                dw = -rs.x;                                             // -dep(pred t)
-                kk = rs.z - rs.y;                                       // svco(t) - inc(t)
-                wsv = cs.x - rs.z;                                      // w(t) - svco(t)
+                x1 = W.tdsm + 2 * ((cb * NL + (rs.w & 0xFFFF)) * W.NTDp);   // TD_cb row endc(t) (column m)
+                t2 = tsm + 2 * (cb * NL * NLp + (cs.y & 0xFFFF));            // column pick(t) of T_cb (row del_m)
+                dw = -rs.x;                                                 // -dep(pred t)
+                kk = rs.z - rs.y;                                           // svco(t) - inc(t)
+                wsv = cs.x - rs.z;                                          // w(t) - svco(t)
                 slk = (P - C.F[bb]) - (((vc >> 8) & 1) ? 0 : WIN_HELI_OFF);
             }
         }
-        c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
-        c_cb[k] = cb;
+        c_x1[k] = x1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
     }
     uint64_t best = KEY_NONE;
     for (int w0 = m_lo; w0 < m_hi; w0 += WIN_ROWS) {
         __syncwarp();
-        if (w0 + lane < m_hi) win_reloc_record<TABU>(C, W, w0 + lane, lane, asp, tsz);
+        if (w0 + lane < m_hi) win_reloc_record<TABU>(C, W, w0 + lane, lane, asp);
         __syncwarp();
         const int nr = min(WIN_ROWS, m_hi - w0);
         uint32_t bk = WIN_NONE;
         for (int r = 0; r < nr; r++) {
             const int4 *rec = W.WB + r * WIN_REC_INT4;
-            const int4 q1 = rec[1];
-            const int hmask = q1.x;
+            const int4 q0 = rec[0];
+            const int hmask = q0.y;
             if (hmask == 0) continue;
-            const int4 q0 = rec[0], q2 = rec[2], q3 = rec[3];
-            const int remk[KR] = {q0.x, q0.y, q0.z, q0.w};
-            const int w_m = q1.y, wm_neg = q1.z, rowP = q1.w;
-            const int rowD = q2.x, svm0 = q2.y, dsvm = q2.z;
-            const uint32_t tb = (uint32_t)q2.w;
-            const int remasp = q3.x;
+            const int4 q1 = rec[1];
+            const int remk = q0.x, w_m = q0.z, rowD = q0.w;
+            const uint32_t tb = (uint32_t)q1.x;
+            const int remasp = q1.y, rowM = q1.z;
 #pragma unroll
             for (int k = 0; k < KR; k++) {
-                const int T1 = lds_t<uint16_t>((uint32_t)madd(c_t1[k], one, rowP));   // T_cb[endc t][pick m]
-                const int T2 = lds_t<uint16_t>((uint32_t)madd(c_t2[k], one, rowD));   // T_cb[del m][pick t]
-                const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));               // d(c, m)
-                const int ins = madd(x1, one, madd(T2, one, c_k[k]));                  // insertion delta
-                const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));                // dep(c) + d(c,m) <= w_m
-                const int mB = madd(T2, neg, madd(c_wsv[k], one, wm_neg));            // w_m + d(m,t) <= w(t)
-                const int mC = madd(ins, neg, c_slk[k] & hmask);                       // F_b + ins <= P (+ heli)
+                const int x1 = lds_t<uint16_t>((uint32_t)madd(c_x1[k], one, rowM));    // d_cb(c, m)
+                const int T2 = lds_t<uint16_t>((uint32_t)madd(c_t2[k], one, rowD));    // T_cb[del m][pick t]
+                const int ins = x1 + T2 + c_k[k];                                       // insertion delta
+                const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));                 // dep(c) + d(c,m) <= w_m
+                const int mB = c_wsv[k] - w_m - T2;                                     // w_m + d(m,t) <= w(t)
+                const int mC = madd(ins, neg, c_slk[k] & hmask);                        // F_b + ins <= P (+ heli)
                 const int mg = mA | mB | mC;
-                const int e2 = madd(ins, one, remasp);                                 // delta - asp (TS) / delta (NS)
+                const int e2 = madd(ins, one, remasp);                                  // delta - asp (TS) / delta (NS)
                 uint32_t nadm;
                 if (TABU) nadm = shl_clamp(tb, (uint32_t)c_b[k]) & ~(uint32_t)e2 & 0x80000000u;
                 else nadm = ~(uint32_t)e2 & 0x80000000u;
-                const uint32_t k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk[k]) | nadm | (uint32_t)(mg >> 31);
+                const uint32_t k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
             }
         }
@@ -175,18 +182,16 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 }
 
 // ---------------------------------------------------------------------------
-// Swap block (non-adjacent pairs m1 < m2; m2 over the lanes in a top-aligned chunk
-// of 32 * KS, as score_swap_fast).  Record of row m1 (5 int4):
-//   q0 = {a (-1: skip), ca, row_ya1, row_ta2}
-//   q1 = {rowP, rowD, -depc1, w1}
-//   q2 = {w(s1) - svco(s1), svco(s1) - inc1 - inc(s1), P - F_a, svc0_1}
-//   q3 = {svc1_1 - svc0_1, cmask, TB[m1], -m1 - 1}
-//   q4 = {keyb0, keyb1, hmask, -asp (TS) or 0 (NS)}
+// Swap block: exchange m1 (route a, p1 -> m1 -> s1) and m2 (route b, p2 -> m2 -> s2), non-adjacent,
+// m1 < m2; m2 over the lanes in a top-aligned chunk of 32 * KS (as score_swap_fast).
+// Record of row m1 (3 int4):
+//   q0 = {a (-1: skip), TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses / offsets)
+//   q1 = {-depc1, w1, w(s1) - svco(s1), svco(s1) - inc1 - inc(s1)}
+//   q2 = {P - F_a, cmask, TB[m1], hmask}   cmask = bit 31 when route a cannot fly heli-only missions
 template <bool TABU>
 __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m1, int r,
-                                                int asp, int tsm, int tsz) {
-    int4 q0 = make_int4(-1, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0), q3 = make_int4(0, 0, 0, 0),
-         q4 = make_int4(0, 0, 0, 0);
+                                                int tsm) {
+    int4 q0 = make_int4(-1, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
     const int4 r1 = C.RS4[m1];
     const int a = (int16_t)((uint32_t)r1.w >> 16);
     if (a >= 0) {
@@ -196,17 +201,15 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
         const int4 cs1 = C.CS4[s1];
         const uint32_t vca = C.VC[a];
         const int ca = vca & 0xFF;
-        q0 = make_int4(a, ca, tsm + tsz * ((ca * C.NL + (r1.w & 0xFFFF)) * C.NLp),   // T_ca[endc1][.]
-                       tsm + tsz * (ca * C.NL * C.NLp + (cs1.y & 0xFFFF)));           // T_ca[.][pick(s1)]
-        q1 = make_int4(tsz * (c1.y & 0xFFFF), tsz * (int)((uint32_t)c1.y >> 16) * C.NLp, -r1.x, c1.x);
-        q2 = make_int4(cs1.x - rs1.z, rs1.z - r1.y - rs1.y, C.P - C.F[a], c1.z);
-        // m2 heli-only needs route a heli-capable: bit 31 of (bf & cmask)
-        q3 = make_int4(c1.w - c1.z, ((vca >> 8) & 1) ? 0 : (int)0x80000000, TABU ? (int)W.TB[m1] : 0, -m1 - 1);
-        const int kb = (1 << 30) + r * KS;    // (0 + 2^23) << 7 | local index
-        q4 = make_int4(kb, kb + 1, C.MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF, TABU ? -asp : 0);
+        q0 = make_int4(a, W.tdsm + 2 * ((ca * C.NL + (r1.w & 0xFFFF)) * W.NTDp),    // TD_ca[endc1][.]
+                       W.ttsm + 2 * ((ca * C.NL + (cs1.y & 0xFFFF)) * C.NLp),       // Tt_ca[pick(s1)][.]
+                       2 * (int)((uint32_t)c1.y >> 16) * C.NLp);                    // T_.[del1][.]
+        q1 = make_int4(-r1.x, c1.x, cs1.x - rs1.z, rs1.z - r1.y - rs1.y);
+        q2 = make_int4(C.P - C.F[a], ((vca >> 8) & 1) ? 0 : (int)0x80000000, TABU ? (int)W.TB[m1] : 0,
+                       C.MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF);
     }
     int4 *rec = W.WB + r * WIN_REC_INT4;
-    rec[0] = q0; rec[1] = q1; rec[2] = q2; rec[3] = q3; rec[4] = q4;
+    rec[0] = q0; rec[1] = q1; rec[2] = q2;
 }
 
 template <bool TABU>
@@ -219,16 +222,15 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
     const uint32_t Rb = C.Rb;
     const int one = C.one, neg = C.neg;
     const int lo = hi - 32 * KS;
-    const int tsm = (int)__cvta_generic_to_shared(C.Ts), tsz = 2;
-    // m2 side, per lane (as score_swap_fast); q_bf = b | heli_only(m2) << 31, q_slk carries the heli offset
-    int q_p2m[KS], q_sv0[KS], q_dsv[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS],
-        q_slk[KS], q_bf[KS], q_cb[KS];
+    const int tsm = (int)__cvta_generic_to_shared(C.Ts);
+    const int nasp = TABU ? -asp : 0;
+    // m2 side, per lane; q_bf = b | heli_only(m2) << 31, q_slk carries the heli offset
+    int q_m2[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS], q_slk[KS], q_bf[KS];
     uint32_t q_tb[KS];
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
-        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = tsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0,
-            bf = 0xFFFF, cb = 0;
+        int d2 = 0, e2 = W.tdsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0, bf = 0xFFFF;
         uint32_t tb = 0;
         if (m2 >= 0) {
             const int4 r2 = RS4[m2];
@@ -236,16 +238,13 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             if (b >= 0) {
                 const int4 c2 = CS4[m2];
                 const uint32_t vc = VC[b];
-                cb = vc & 0xFF;
+                const int cb = vc & 0xFF;
                 const int s2 = LK[m2] & 0xFFFF;
                 const int4 rs2 = RS4[s2];
                 const int4 cs2 = CS4[s2];
-                p2m = tsz * (c2.y & 0xFFFF);                                // pick2
-                sv0 = c2.z;
-                dsv = c2.w - c2.z;
-                d2 = tsz * (int)((uint32_t)c2.y >> 16) * NLp;               // row del2 of T (column pick(s1))
-                e2 = tsm + tsz * ((cb * NL + (r2.w & 0xFFFF)) * NLp);       // row endc2 of T_cb (column pick1)
-                p2 = tsm + tsz * (cb * NL * NLp + (cs2.y & 0xFFFF));        // column pick(s2) of T_cb
+                d2 = 2 * (int)((uint32_t)c2.y >> 16);                       // column del2 of Tt (row pick(s1))
+                e2 = W.tdsm + 2 * ((cb * NL + (r2.w & 0xFFFF)) * W.NTDp);    // TD_cb row endc2 (column m1)
+                p2 = tsm + 2 * (cb * NL * NLp + (cs2.y & 0xFFFF));          // column pick(s2) of T_cb (row del1)
                 w2 = c2.x;
                 dep2 = r2.x;
                 kb = rs2.z - r2.y - rs2.y;                                  // svco(s2) - inc2 - inc(s2)
@@ -255,14 +254,14 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 if (TABU) tb = W.TB[m2];
             }
         }
-        q_p2m[k] = p2m; q_sv0[k] = sv0; q_dsv[k] = dsv; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2;
-        q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_cb[k] = cb; q_tb[k] = tb;
+        q_m2[k] = 2 * max(m2, 0); q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2; q_dep2[k] = dep2;
+        q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_tb[k] = tb;
     }
-    const int lane_lo = lo + lane;
+    const int lane_lo = lo + lane - 1;
     uint64_t best = KEY_NONE;
     for (int w0 = m1_lo; w0 < m1_hi; w0 += WIN_ROWS) {
         __syncwarp();
-        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, asp, tsm, tsz);
+        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, tsm);
         __syncwarp();
         const int nr = min(WIN_ROWS, m1_hi - w0);
         uint32_t bk = WIN_NONE;
@@ -272,42 +271,37 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const int a = q0.x;
             if (a < 0) continue;
             const int m1 = w0 + r;
-            const int4 q1 = rec[1], q2 = rec[2], q3 = rec[3], q4 = rec[4];
-            const int ca = q0.y, row_ya1 = q0.z, row_ta2 = q0.w;
-            const int rowP = q1.x, rowD = q1.y, ndepc1 = q1.z, w1 = q1.w;
-            const int wsv1 = q2.x, ka = q2.y, slkA = q2.z, sv10 = q2.w;
-            const int dsv1 = q3.x, cmask = q3.y;
-            const uint32_t tb1 = (uint32_t)q3.z;
-            const int tri = q3.w;
-            const int keyb[KS] = {q4.x, q4.y};
-            const int hmask = q4.z, nasp = q4.w;
+            const int4 q1 = rec[1], q2 = rec[2];
+            const int row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
+            const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
+            const int slkA = q2.x, cmask = q2.y, hmask = q2.w;
+            const uint32_t tb1 = (uint32_t)q2.z;
+            const int rowM1 = 2 * m1, keyb0 = (1 << 30) + r * KS;   // (0 + 2^23) << 7 | local index
 #pragma unroll
             for (int k = 0; k < KS; k++) {
                 if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
                 const int bf = q_bf[k];
                 const uint32_t b = (uint32_t)bf & 0xFFFFu;
-                const int Tya1 = lds_t<uint16_t>((uint32_t)madd(row_ya1, one, q_p2m[k]));   // T_ca[endc1][pick2]
+                const int ya1 = lds_t<uint16_t>((uint32_t)madd(row_ya1, one, q_m2[k]));     // d_a(p1, m2)
                 const int Ta2 = lds_t<uint16_t>((uint32_t)madd(row_ta2, one, q_d2[k]));     // T_ca[del2][pick(s1)]
-                const int Tyb1 = lds_t<uint16_t>((uint32_t)madd(q_e2[k], one, rowP));       // T_cb[endc2][pick1]
+                const int yb1 = lds_t<uint16_t>((uint32_t)madd(q_e2[k], one, rowM1));       // d_b(p2, m1)
                 const int Tb2 = lds_t<uint16_t>((uint32_t)madd(q_p2[k], one, rowD));        // T_cb[del1][pick(s2)]
-                const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));              // d_a(p1, m2)
-                const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                 // d_b(p2, m1)
-                const int da = madd(ya1, one, madd(Ta2, one, ka));
-                const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
+                const int da = ya1 + Ta2 + ka;
+                const int db = yb1 + Tb2 + q_kb[k];
                 const int delta = madd(da, one, db);
                 const int mfA = madd(da, neg, slkA);                                        // F_a + da <= P
                 const int mfB = madd(db, neg, q_slk[k] & hmask);                            // F_b + db <= P (+ heli)
                 const int l1 = madd(ya1, neg, madd(q_w2[k], one, ndepc1));                  // dep(p1) + ya1 <= w2
-                const int l2 = madd(Ta2, neg, madd(q_w2[k], neg, wsv1));                    // w2 + d(m2,s1) <= w(s1)
-                const int l3 = madd(yb1, neg, madd(q_dep2[k], neg, w1));                    // dep(p2) + yb1 <= w1
-                const int l4 = madd(Tb2, neg, madd(w1, neg, q_ws2[k]));                     // w1 + d(m1,s2) <= w(s2)
-                const int trim = lane_lo + 32 * k + tri;                                    // m2 - m1 - 1 >= 0
+                const int l2 = wsv1 - q_w2[k] - Ta2;                                        // w2 + d(m2,s1) <= w(s1)
+                const int l3 = w1 - q_dep2[k] - yb1;                                        // dep(p2) + yb1 <= w1
+                const int l4 = q_ws2[k] - w1 - Tb2;                                         // w1 + d(m1,s2) <= w(s2)
+                const int trim = lane_lo + 32 * k - m1;                                     // m2 - m1 - 1 >= 0
                 const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
                 const int e2 = madd(delta, one, nasp);
                 uint32_t nadm;
                 if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)e2 & 0x80000000u;
                 else nadm = ~(uint32_t)e2 & 0x80000000u;
-                const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb[k]) | nadm | (uint32_t)(mg >> 31);
+                const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
             }
         }
