@@ -689,11 +689,23 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
     // window scorers (window.cuh) for the batched kernel: every move kind, positive service legs, uint16 table,
     // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
-    const bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
-                     (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
+    bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
+               (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
     size_t sh_b = 0, run_b = 0;
     batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure, I->tsym != 0);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
+    if (win) {   // the window path stages more per CTA (node-cost tables): keep it only if it still fits the runs
+        const int need = (int)std::min<int64_t>(28, ((int64_t)n_runs + ctx->n_sm - 1) / ctx->n_sm);
+        size_t sh0 = 0, rb0 = 0;
+        batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh0, &rb0);
+        const int fit0 = rb0 > 0 && sh0 < ctx->max_smem ? (int)((ctx->max_smem - sh0) / rb0) : 0;
+        if (rpc_fit < need && fit0 > rpc_fit) {
+            win = false;
+            sh_b = sh0;
+            run_b = rb0;
+            rpc_fit = fit0;
+        }
+    }
     // the compact-layout kernels (k_batch, k_grid) score the waiting model only;
     // the no-wait variant (f3) runs on k_search
     const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !I->no_wait;

@@ -47,6 +47,7 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.CH = o; o = al16(o + NC);
     L.TT = o; o = al16(o + (win && !tsym ? NC * NL * NLp * tbytes : 0));   // transposed table (window scorers)
     L.TD = o; o = al16(o + (win ? NC * NL * padded_stride(n, 2) * 2 : 0));  // node costs d_c(x, m) (window scorers)
+    L.TDT = o; o = al16(o + (win ? NC * n * padded_stride(NL, 2) * 2 : 0)); // the same, [c][m][x]
     L.shared_bytes = o;
     int r = 0;
     L.RS = r; r = al16(r + S * 16);
@@ -119,7 +120,9 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         uint16_t *TD = reinterpret_cast<uint16_t *>(smem + L.TD);
         for (int i = tid; i < NC * NL * n; i += blockDim.x) {
             const int c = i / (NL * n), x = (i / n) % NL, m = i % n;
-            TD[(c * NL + x) * NTDp + m] = (uint16_t)(I.T[(c * NL + x) * NL + I.pick[m]] + I.svc[c * n + m]);
+            const uint16_t d = (uint16_t)(I.T[(c * NL + x) * NL + I.pick[m]] + I.svc[c * n + m]);
+            TD[(c * NL + x) * NTDp + m] = d;
+            reinterpret_cast<uint16_t *>(smem + L.TDT)[(c * n + m) * padded_stride(NL, 2) + x] = d;
         }
     }
     __syncthreads();
@@ -255,6 +258,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     W.TB = TB;
     W.ttsm = (int)__cvta_generic_to_shared(WIN && !I.tsym ? (const void *)(smem + L.TT) : (const void *)Ts);
     W.tdsm = (int)__cvta_generic_to_shared(smem + L.TD);
+    W.tdtsm = (int)__cvta_generic_to_shared(smem + L.TDT);
     W.NTDp = padded_stride(n, 2);
     const int ring = A.tenure + 1;
     int it = 0, stop = 0;

@@ -44,8 +44,8 @@ struct SearchArgs {
 constexpr int GRID_WARPS = 24;   // k_grid warps per CTA (one CTA per SM; <= 85 registers per thread; 28 measured slower)
 
 struct BatchLayout {
-    int T, CS, MH, VC, CH, TT, TD;   // CTA-wide part (window scorers: TT transposed table when asymmetric,
-                                     // TD node costs d_c(x, m))
+    int T, CS, MH, VC, CH, TT, TD, TDT;   // CTA-wide part (window scorers: TT transposed table when
+                                          // asymmetric, TD node costs d_c(x, m) as [c][x][m] and TDT as [c][m][x])
     int shared_bytes;
     int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
     int TB, RG, WB;                 // window scorers: tabu bits, tabu-write ring, window buffer

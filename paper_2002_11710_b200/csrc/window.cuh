@@ -19,7 +19,9 @@
 //    T_c[pick_m][del_m] (O2, uint16; the host checks the largest fits), so
 //    the cost of arriving at a mission is one gather instead of a gather, the
 //    service leg of the right class and two adds; the swap's d_a(p1, m2) reads
-//    one TD row over consecutive lanes (no bank conflicts);
+//    one TD row over consecutive lanes (no bank conflicts), and the gathers
+//    whose lanes vary the origin x read the transposed copy TDT_c[m][x] (one
+//    row per class instead of a column);
 //  * row-local table read where a gather would read down a column: the swap's
 //    T_ca[del m2][pick s1] is read from the per-layer transpose (T itself when
 //    every layer is symmetric, else a transposed copy staged next to T);
@@ -59,6 +61,7 @@ struct WinCtx {
     const uint32_t *TB;     // [n] tabu bits: bit (31 - v) of TB[m] <=> E[m][v] >= it (TABU only)
     int ttsm;               // shared-window byte address of the transposed table (== the table's when symmetric)
     int tdsm;               // shared-window byte address of TD[NC][NL][NTDp] (uint16 node costs)
+    int tdtsm;              // ... of TDT[NC][n][NLp] (the same, transposed per class)
     int NTDp;               // TD row stride (halfwords)
 };
 
@@ -80,7 +83,7 @@ __device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
 //   q0 = {remk, hmask, w_m, rowD}   remk = (rem + 2^23) << 7 | r * KR (key base; item k adds k);
 //        hmask = 0: row has no feasible move (skip); else 0x3FFFFFFF (m not heli-only) or ~0
 //        (heli-only); rowD = byte offset of table row del_m
-//   q1 = {TB[m], rem - asp (TS) or rem (NS), 2 m, 0}
+//   q1 = {TB[m], rem - asp (TS) or rem (NS), byte offset of TDT row m, 0}
 template <bool TABU>
 __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m, int r,
                                                  int asp) {
@@ -99,7 +102,7 @@ __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_
             const int4 cm = C.CS4[m];
             q0 = make_int4((rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR, C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF,
                            cm.x, 2 * (int)((uint32_t)cm.y >> 16) * C.NLp);
-            q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m, 0);
+            q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m * C.NLp, 0);
         }
     }
     int4 *rec = W.WB + r * WIN_REC_INT4;
@@ -119,7 +122,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
-        int x1 = W.tdsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF;
+        int x1 = W.tdtsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF;
         if (t < S) {
             const int4 rs = RS4[t];
             const int bb = (int16_t)((uint32_t)rs.w >> 16);
@@ -128,7 +131,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
                 const uint32_t vc = VC[bb];
                 const int cb = vc & 0xFF;
                 b = bb;
-                x1 = W.tdsm + 2 * ((cb * NL + (rs.w & 0xFFFF)) * W.NTDp);   // TD_cb row endc(t) (column m)
+                x1 = W.tdtsm + 2 * (cb * C.n * NLp + (rs.w & 0xFFFF));      // TDT_cb column endc(t) (row m)
                 t2 = tsm + 2 * (cb * NL * NLp + (cs.y & 0xFFFF));            // column pick(t) of T_cb (row del_m)
                 dw = -rs.x;                                                 // -dep(pred t)
                 kk = rs.z - rs.y;                                           // svco(t) - inc(t)
@@ -230,7 +233,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
-        int d2 = 0, e2 = W.tdsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0, bf = 0xFFFF;
+        int d2 = 0, e2 = W.tdtsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0, bf = 0xFFFF;
         uint32_t tb = 0;
         if (m2 >= 0) {
             const int4 r2 = RS4[m2];
@@ -243,7 +246,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const int4 rs2 = RS4[s2];
                 const int4 cs2 = CS4[s2];
                 d2 = 2 * (int)((uint32_t)c2.y >> 16);                       // column del2 of Tt (row pick(s1))
-                e2 = W.tdsm + 2 * ((cb * NL + (r2.w & 0xFFFF)) * W.NTDp);    // TD_cb row endc2 (column m1)
+                e2 = W.tdtsm + 2 * (cb * n * NLp + (r2.w & 0xFFFF));         // TDT_cb column endc2 (row m1)
                 p2 = tsm + 2 * (cb * NL * NLp + (cs2.y & 0xFFFF));          // column pick(s2) of T_cb (row del1)
                 w2 = c2.x;
                 dep2 = r2.x;
@@ -276,7 +279,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
             const int slkA = q2.x, cmask = q2.y, hmask = q2.w;
             const uint32_t tb1 = (uint32_t)q2.z;
-            const int rowM1 = 2 * m1, keyb0 = (1 << 30) + r * KS;   // (0 + 2^23) << 7 | local index
+            const int rowM1 = 2 * m1 * NLp, keyb0 = (1 << 30) + r * KS;   // TDT row m1; (0 + 2^23) << 7 | local index
 #pragma unroll
             for (int k = 0; k < KS; k++) {
                 if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
