@@ -639,6 +639,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     memset(&A, 0, sizeof(A));
     A.inst = *D;
     A.one = 1;
+    A.neg = -1;
     const size_t nst = shared_start ? 1 : (size_t)n_runs;
     const void *dp, *dm, *ds = nullptr;
     if ((st = dev_in(ctx, "start_ptr", start_ptr, nst * (V + 1) * 4, &dp)) != AS_OK) return st;
@@ -1043,6 +1044,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     SearchArgs A;
     memset(&A, 0, sizeof(A));
     A.one = 1;
+    A.neg = -1;
     A.n_runs = (int32_t)total;
     A.seeds = (const uint64_t *)ds;
     A.seed = P->seed;
@@ -1327,6 +1329,7 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
     memset(&A, 0, sizeof(A));
     A.inst = *D;
     A.one = 1;
+    A.neg = -1;
     A.n_runs = 1;
     const void *dp, *dm;
     if ((st = dev_in(ctx, "start_ptr", start_ptr, (size_t)(V + 1) * 4, &dp)) != AS_OK) return st;

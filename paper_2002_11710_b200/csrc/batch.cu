@@ -252,7 +252,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     ScoreCtx<TT, ET> SC;
     SC.Ts = Ts; SC.Tt = A.inst.tsym ? Ts : reinterpret_cast<const TT *>(A.inst.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E; SC.Et = nullptr;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = Rb; SC.mask = mask;
-    SC.one = A.one; SC.neg = -A.one;
+    SC.one = A.one; SC.neg = A.neg;
     WinCtx W;
     W.WB = WIN ? reinterpret_cast<int4 *>(rb + L.WB) : nullptr;
     W.TB = TB;

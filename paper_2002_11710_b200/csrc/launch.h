@@ -23,7 +23,7 @@ struct RunViewG {
 
 struct SearchArgs {
     DevInst inst;
-    int32_t one;                           // == 1 (opaque multiplier for FMA-pipe adds)
+    int32_t one, neg;                      // == 1, -1 (opaque multipliers for FMA-pipe adds; set by the host)
     int32_t n_runs;
     const int32_t *start_ptr, *start_ms;   // [R][V+1], [R][n] or shared
     int32_t shared_start;

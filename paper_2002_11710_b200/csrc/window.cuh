@@ -71,6 +71,14 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {   // x <
     return r;
 }
 
+// ld.shared.u16 at a 32-bit shared-window byte address plus an immediate offset (folded into the LDS)
+template <int OFF>
+__device__ __forceinline__ int lds_u16_off(uint32_t addr) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1+%2];" : "=h"(v) : "r"(addr), "n"(OFF));
+    return (int)v;
+}
+
 // 32-bit window key -> 64-bit key (class << 63 | (delta + 2^30) << 32 | idx)
 __device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
     const uint32_t d = ((bk >> WIN_KEY_SHIFT) & 0xFFFFFFu) + (uint32_t)(DELTA_BIAS - WIN_BIAS);
@@ -187,14 +195,16 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 // ---------------------------------------------------------------------------
 // Swap block: exchange m1 (route a, p1 -> m1 -> s1) and m2 (route b, p2 -> m2 -> s2), non-adjacent,
 // m1 < m2; m2 over the lanes in a top-aligned chunk of 32 * KS (as score_swap_fast).
-// Record of row m1 (3 int4):
-//   q0 = {a (-1: skip), TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses / offsets)
-//   q1 = {-depc1, w1, w(s1) - svco(s1), svco(s1) - inc1 - inc(s1)}
-//   q2 = {P - F_a, cmask, TB[m1], hmask}   cmask = bit 31 when route a cannot fly heli-only missions
+// Record of row m1 (3 int4); TS folds the aspiration threshold asp into ka, slkA and keyb, so the
+// scorer's "delta" is delta - asp (its sign is the aspiration test) and the key still encodes delta:
+//   q0 = {cmask | a, TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses / offsets);
+//        cmask = bit 31 when route a cannot fly heli-only missions
+//   q1 = {-depc1, w1, w(s1) - svco(s1), svco(s1) - inc1 - inc(s1) - asp}
+//   q2 = {P - F_a - asp, keyb = (2^23 + asp) << 7 | r * KS, TB[m1], hmask (0: skip the row)}
 template <bool TABU>
 __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m1, int r,
-                                                int tsm) {
-    int4 q0 = make_int4(-1, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
+                                                int tsm, int asp) {
+    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
     const int4 r1 = C.RS4[m1];
     const int a = (int16_t)((uint32_t)r1.w >> 16);
     if (a >= 0) {
@@ -204,12 +214,14 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
         const int4 cs1 = C.CS4[s1];
         const uint32_t vca = C.VC[a];
         const int ca = vca & 0xFF;
-        q0 = make_int4(a, W.tdsm + 2 * ((ca * C.NL + (r1.w & 0xFFFF)) * W.NTDp),    // TD_ca[endc1][.]
+        const int sa = TABU ? asp : 0;
+        q0 = make_int4((((vca >> 8) & 1) ? 0 : (int)0x80000000) | a,
+                       W.tdsm + 2 * ((ca * C.NL + (r1.w & 0xFFFF)) * W.NTDp),       // TD_ca[endc1][.]
                        W.ttsm + 2 * ((ca * C.NL + (cs1.y & 0xFFFF)) * C.NLp),       // Tt_ca[pick(s1)][.]
                        2 * (int)((uint32_t)c1.y >> 16) * C.NLp);                    // T_.[del1][.]
-        q1 = make_int4(-r1.x, c1.x, cs1.x - rs1.z, rs1.z - r1.y - rs1.y);
-        q2 = make_int4(C.P - C.F[a], ((vca >> 8) & 1) ? 0 : (int)0x80000000, TABU ? (int)W.TB[m1] : 0,
-                       C.MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF);
+        q1 = make_int4(-r1.x, c1.x, cs1.x - rs1.z, rs1.z - r1.y - rs1.y - sa);
+        q2 = make_int4(C.P - C.F[a] - sa, (WIN_BIAS + sa) * (1 << WIN_KEY_SHIFT) + r * KS,
+                       TABU ? (int)W.TB[m1] : 0, C.MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF);
     }
     int4 *rec = W.WB + r * WIN_REC_INT4;
     rec[0] = q0; rec[1] = q1; rec[2] = q2;
@@ -226,9 +238,8 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
     const int one = C.one, neg = C.neg;
     const int lo = hi - 32 * KS;
     const int tsm = (int)__cvta_generic_to_shared(C.Ts);
-    const int nasp = TABU ? -asp : 0;
     // m2 side, per lane; q_bf = b | heli_only(m2) << 31, q_slk carries the heli offset
-    int q_m2[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS], q_slk[KS], q_bf[KS];
+    int q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS], q_slk[KS], q_bf[KS];
     uint32_t q_tb[KS];
 #pragma unroll
     for (int k = 0; k < KS; k++) {
@@ -257,35 +268,37 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 if (TABU) tb = W.TB[m2];
             }
         }
-        q_m2[k] = 2 * max(m2, 0); q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2; q_dep2[k] = dep2;
+        q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2; q_dep2[k] = dep2;
         q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_tb[k] = tb;
     }
-    const int lane_lo = lo + lane - 1;
+    const int mlane = lo + lane;   // m2 of sub-chunk 0 (sub-chunk k: + 32 k)
     uint64_t best = KEY_NONE;
     for (int w0 = m1_lo; w0 < m1_hi; w0 += WIN_ROWS) {
         __syncwarp();
-        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, tsm);
+        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, tsm, asp);
         __syncwarp();
         const int nr = min(WIN_ROWS, m1_hi - w0);
         uint32_t bk = WIN_NONE;
         for (int r = 0; r < nr; r++) {
             const int4 *rec = W.WB + r * WIN_REC_INT4;
-            const int4 q0 = rec[0];
-            const int a = q0.x;
-            if (a < 0) continue;
+            const int4 q2 = rec[2];
+            const int hmask = q2.w;
+            if (hmask == 0) continue;
             const int m1 = w0 + r;
-            const int4 q1 = rec[1], q2 = rec[2];
-            const int row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
+            const int4 q0 = rec[0], q1 = rec[1];
+            const int cmask = q0.x, a = q0.x & 0x3F, row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
             const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
-            const int slkA = q2.x, cmask = q2.y, hmask = q2.w;
+            const int slkA = q2.x, keyb0 = q2.y;
             const uint32_t tb1 = (uint32_t)q2.z;
-            const int rowM1 = 2 * m1 * NLp, keyb0 = (1 << 30) + r * KS;   // TDT row m1; (0 + 2^23) << 7 | local index
+            const int rowM1 = 2 * m1 * NLp;   // TDT row m1
+            const uint32_t ya_base = (uint32_t)madd(mlane, 2, row_ya1);   // TD_ca[endc1][m2 of sub-chunk 0]
 #pragma unroll
             for (int k = 0; k < KS; k++) {
                 if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
                 const int bf = q_bf[k];
                 const uint32_t b = (uint32_t)bf & 0xFFFFu;
-                const int ya1 = lds_t<uint16_t>((uint32_t)madd(row_ya1, one, q_m2[k]));     // d_a(p1, m2)
+                static_assert(KS == 2, "immediate offsets below assume two sub-chunks");
+                const int ya1 = k ? lds_u16_off<64>(ya_base) : lds_u16_off<0>(ya_base);     // d_a(p1, m2)
                 const int Ta2 = lds_t<uint16_t>((uint32_t)madd(row_ta2, one, q_d2[k]));     // T_ca[del2][pick(s1)]
                 const int yb1 = lds_t<uint16_t>((uint32_t)madd(q_e2[k], one, rowM1));       // d_b(p2, m1)
                 const int Tb2 = lds_t<uint16_t>((uint32_t)madd(q_p2[k], one, rowD));        // T_cb[del1][pick(s2)]
@@ -298,12 +311,11 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const int l2 = wsv1 - q_w2[k] - Ta2;                                        // w2 + d(m2,s1) <= w(s1)
                 const int l3 = w1 - q_dep2[k] - yb1;                                        // dep(p2) + yb1 <= w1
                 const int l4 = q_ws2[k] - w1 - Tb2;                                         // w1 + d(m1,s2) <= w(s2)
-                const int trim = lane_lo + 32 * k - m1;                                     // m2 - m1 - 1 >= 0
+                const int trim = mlane + (32 * k - 1) - m1;                                 // m2 - m1 - 1 >= 0
                 const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
-                const int e2 = madd(delta, one, nasp);
-                uint32_t nadm;
-                if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)e2 & 0x80000000u;
-                else nadm = ~(uint32_t)e2 & 0x80000000u;
+                uint32_t nadm;                                                              // delta holds delta - asp
+                if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)delta & 0x80000000u;
+                else nadm = ~(uint32_t)delta & 0x80000000u;
                 const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
             }
