@@ -292,50 +292,25 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
 // every class (DevInst::svcpos).  Then the two no-op relocate targets (t = m,
 // t = succ m) and the adjacent swap pairs fail a link check by construction
 // (their margins are -svc < 0), so no per-move validity test is
-// needed; feasibility, compatibility and the triangle m1 < m2 are folded into
-// one integer margin whose sign bit poisons the key, and admissibility is a
-// sign-bit expression -- the scoring loops are issue-bound, so every
-// compare/select removed counts.
-template <bool TABU, bool HELI, bool TR, class TT, class ET>
-__device__ __forceinline__ void reloc_row_fast(const TT *Ts, const TT *Tt, const ET *Erow, const int (&c_t1)[KR],
-                                               const int (&c_t2)[KR], const int (&c_dw)[KR], const int (&c_k)[KR],
-                                               const int (&c_wsv)[KR], const int (&c_slk)[KR],
-                                               const int (&c_b)[KR], const int (&c_cb)[KR], int a, int rem,
-                                               int inter_bias, int intra_lim, int w_m, int rowP, int rowD,
-                                               int svm0, int dsvm, int it, int asp, uint32_t base, int one,
-                                               int neg, uint32_t &bk32, uint32_t &bidx) {
-    const int wm_neg = madd(w_m, neg, 0);
-#pragma unroll
-    for (int k = 0; k < KR; k++) {
-        // T_cb[endc t][pick m], T_cb[del m][pick t]; shared table: byte addresses (score_reloc_fast)
-        const int T1 = TR ? (int)Tt[madd(c_t1[k], one, rowP)] : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
-        const int T2 = TR ? (int)Ts[madd(c_t2[k], one, rowD)] : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
-        const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));                 // d(c, m)
-        const int ins = madd(x1, one, madd(T2, one, c_k[k]));
-        const int delta = madd(rem, one, ins);
-        // inter-route limit P - F_b (bit 30 of c_slk = vehicle may not fly a heli-only mission)
-        const int slk = HELI ? ((int)((uint32_t)c_slk[k] << 1) >> 1) : (c_slk[k] & 0x3FFFFFFF);
-        const int lim = c_b[k] == a ? intra_lim : madd(slk, one, inter_bias);
-        const int mg = min(min(madd(x1, neg, madd(w_m, one, c_dw[k])), madd(T2, neg, madd(c_wsv[k], one, wm_neg))),
-                           madd(ins, neg, lim));
-        uint32_t nadm;
-        if (TABU) {
-            const int e1 = madd(it, neg, (int)Erow[c_b[k]]);   // E[m][b] - it  (>= 0: tabu)
-            const int e2 = madd(asp, neg, delta);              // delta - asp   (>= 0: no aspiration)
-            nadm = ~(uint32_t)(e1 | e2) & 0x80000000u;
-        } else {
-            nadm = ~(uint32_t)delta & 0x80000000u;             // NS: admissible iff delta < 0
-        }
-        const uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | nadm | (uint32_t)(mg >> 31);
-        const bool better = k32 < bk32;
-        bk32 = better ? k32 : bk32;
-        bidx = better ? base + 32 * k : bidx;
-    }
-}
+// needed; and every intra-route move fails one of its new-link checks (a
+// feasible route is strictly deadline-sorted, reading #42), so the flight
+// limit is checked in its inter-route form for every move and a relocate row
+// whose removal leaves route a over the limit is skipped.  Feasibility,
+// compatibility and the triangle m1 < m2 are OR-combined into one margin whose
+// sign bit poisons the key, admissibility is a sign-bit expression, and sums are
+// split between 3-input adds (ALU pipe) and mad.lo (FMA pipe) -- the scoring
+// loops are issue-bound, so every instruction removed counts.
+//
+// Keys: with a uint16 table (|delta| < 2^20) a lane keeps the 32-bit key
+// nadm << 31 | (delta + 2^23) << 7 | local index over blocks of 32 rows (one
+// unsigned min per move, the index recovered at the block's end, window.cuh);
+// with an int32 table it keeps (class << 31 | delta + 2^30) and the index.
+constexpr int FB_ROWS = 32;   // rows per key block (uint16 tables)
 
 template <bool TABU, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
                                                      int asp, int lane) {
+    constexpr bool K16 = sizeof(TT) == 2;
     const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
@@ -350,7 +325,7 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
-        int t1 = tsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = -1, cb = 0;
+        int t1 = tsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0, cb = 0;
         if (t < S) {
             const int4 rs = RS4[t];
             const int bb = (int16_t)((uint32_t)rs.w >> 16);
@@ -365,47 +340,84 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
                 dw = -rs.x;                                  // -dep(pred t)
                 kk = rs.z - rs.y;                            // svco(t) - inc(t)
                 wsv = cs.x - rs.z;                           // w(t) - svco(t)
-                slk = (P - F[bb]) | (((vc >> 8) & 1) ? 0 : (1 << 30));
+                slk = (P - F[bb]) - (((vc >> 8) & 1) ? 0 : (1 << 30));   // heli offset (masked off for non-heli rows)
             }
         }
         c_t1[k] = t1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
         c_cb[k] = cb;
     }
+    uint64_t best = KEY_NONE;
     uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
-    for (int m = m_lo; m < m_hi; m++) {
-        const int4 rm = RS4[m];
-        const int a = (int16_t)((uint32_t)rm.w >> 16);
-        if (a < 0) continue;
-        const int s = LK[m] & 0xFFFF;
-        const int4 rsx = RS4[s];
-        const int4 csx = CS4[s];
-        const int ca = VC[a] & 0xFF;
-        const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
-        if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
-        const int rem = Dps - rm.y - rsx.y;
-        const int4 cm = CS4[m];
-        const int Fa = F[a];
-        const int inter_bias = (Fa + rem <= P) ? 0 : NEG;
-        const int intra_lim = P - Fa - rem;
-        const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : tsz * (cm.y & 0xFFFF),
-                  rowD = tsz * (int)((uint32_t)cm.y >> 16) * NLp;
-        const ET *Erow = TABU ? E + m * V : nullptr;
-        const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;
-        if (MH[m])
-            reloc_row_fast<TABU, true, TR>(Ts, Tt, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
-                                       intra_lim, w_m, rowP, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
-                                       bidx);
-        else
-            reloc_row_fast<TABU, false, TR>(Ts, Tt, Erow, c_t1, c_t2, c_dw, c_k, c_wsv, c_slk, c_b, c_cb, a, rem, inter_bias,
-                                        intra_lim, w_m, rowP, rowD, cm.z, cm.w - cm.z, it, asp, base, one, neg, bk32,
-                                        bidx);
+    for (int m0 = m_lo; m0 < m_hi; m0 += FB_ROWS) {
+        const int m_end = min(m_hi, m0 + FB_ROWS);
+        if (K16) bk32 = 0xFFFFFFFFu;
+        for (int m = m0; m < m_end; m++) {
+            const int4 rm = RS4[m];
+            const int a = (int16_t)((uint32_t)rm.w >> 16);
+            if (a < 0) continue;
+            const int s = LK[m] & 0xFFFF;
+            const int4 rsx = RS4[s];
+            const int4 csx = CS4[s];
+            const int ca = VC[a] & 0xFF;
+            const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+            if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
+            const int rem = Dps - rm.y - rsx.y;
+            if (F[a] + rem > P) continue;         // no feasible relocate of m (reading #42)
+            const int4 cm = CS4[m];
+            const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : tsz * (cm.y & 0xFFFF),
+                      rowD = tsz * (int)((uint32_t)cm.y >> 16) * NLp;
+            const int svm0 = cm.z, dsvm = cm.w - cm.z, wm_neg = -cm.x;
+            const int hmask = MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
+            const int remasp = TABU ? rem - asp : rem;
+            const ET *Erow = TABU ? E + m * V : nullptr;
+            const int remk = (rem + (1 << 23)) * 128 + (m - m0) * KR;            // K16 key base
+            const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;        // int32-table index
+#pragma unroll
+            for (int k = 0; k < KR; k++) {
+                // T_cb[endc t][pick m], T_cb[del m][pick t]; shared table: byte addresses
+                const int T1 = TR ? (int)Tt[madd(c_t1[k], one, rowP)] : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
+                const int T2 = TR ? (int)Ts[madd(c_t2[k], one, rowD)] : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
+                const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));              // d(c, m)
+                const int ins = x1 + T2 + c_k[k];
+                const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));               // dep(c) + d(c,m) <= w_m
+                const int mB = c_wsv[k] + wm_neg - T2;                                // w_m + d(m,t) <= w(t)
+                const int mC = madd(ins, neg, c_slk[k] & hmask);                      // F_b + ins <= P (+ heli)
+                const int mg = mA | mB | mC;
+                const int e2 = madd(ins, one, remasp);                                // delta - asp (TS) / delta (NS)
+                uint32_t nadm;
+                if (TABU) {
+                    const int e1 = madd(it, neg, (int)Erow[c_b[k]]);                  // E[m][b] - it (>= 0: tabu)
+                    nadm = ~(uint32_t)(e1 | e2) & 0x80000000u;
+                } else {
+                    nadm = ~(uint32_t)e2 & 0x80000000u;
+                }
+                if constexpr (K16) {
+                    const uint32_t k32 = (uint32_t)madd(ins, 128, remk + k) | nadm | (uint32_t)(mg >> 31);
+                    bk32 = min(bk32, k32);
+                } else {
+                    const uint32_t k32 = (uint32_t)madd(rem + ins, one, DELTA_BIAS) | nadm | (uint32_t)(mg >> 31);
+                    const bool better = k32 < bk32;
+                    bk32 = better ? k32 : bk32;
+                    bidx = better ? base + 32 * k : bidx;
+                }
+            }
+        }
+        if (K16 && bk32 != 0xFFFFFFFFu) {
+            const int lid = bk32 & 127;
+            const uint32_t idx = (uint32_t)(m0 + lid / KR) * (uint32_t)S + (uint32_t)(t0 + lane + 32 * (lid % KR));
+            const uint32_t d = ((bk32 >> 7) & 0xFFFFFFu) + (uint32_t)(DELTA_BIAS - (1 << 23));
+            const uint64_t key = ((uint64_t)((bk32 & 0x80000000u) | d) << 32) | idx;
+            best = key < best ? key : best;
+        }
     }
-    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+    if (!K16) best = bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+    return best;
 }
 
 template <bool TABU, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, int hi, int m1_lo, int m1_hi, int it,
                                                     int asp, int lane) {
+    constexpr bool K16 = sizeof(TT) == 2;
     const TT *Ts = C.Ts, *Tt = C.Tt;
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
     const uint8_t *MH = C.MH;
@@ -416,7 +428,8 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
     const uint32_t Rb = C.Rb;
     const int one = C.one, neg = C.neg;
     const int lo = hi - 32 * KS;
-    // m2-side cache; q_f: bit 20 = m2 heli-only, bit 21 = vehicle of m2 cannot fly heli-only
+    const int sa = TABU ? asp : 0;   // aspiration folded into route a's terms: "dl" below is delta - asp
+    // m2-side cache; q_bf = b | heli_only(m2) << 31; q_slk carries the heli offset
     int q_p2m[KS], q_sv0[KS], q_dsv[KS], q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS],
         q_slk[KS], q_bf[KS];
     int q_cb[KS];
@@ -425,8 +438,8 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
-        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = tsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = NEG,
-            bf = -1, cb = 0;
+        int p2m = 0, sv0 = 0, dsv = 0, d2 = 0, e2 = tsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0,
+            bf = 0, cb = 0;
         if (m2 >= 0) {
             const int4 r2 = RS4[m2];
             const int b = (int16_t)((uint32_t)r2.w >> 16);
@@ -449,81 +462,100 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 dep2 = r2.x;
                 kb = rs2.z - r2.y - rs2.y;                        // svco(s2) - inc2 - inc(s2)
                 ws2 = cs2.x - rs2.z;                              // w(s2) - svco(s2)
-                slk = P - F[b];
-                bf = b | ((int)MH[m2] << 20) | ((((vc >> 8) & 1) ? 0 : 1) << 21);
+                slk = (P - F[b]) - (((vc >> 8) & 1) ? 0 : (1 << 30));
+                bf = b | (MH[m2] ? (int)0x80000000 : 0);
             }
         }
         q_p2m[k] = p2m; q_sv0[k] = sv0; q_dsv[k] = dsv; q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2;
         q_dep2[k] = dep2; q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_cb[k] = cb;
     }
+    const int mlane = lo + lane;
+    uint64_t best = KEY_NONE;
     uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
-    for (int m1 = m1_lo; m1 < m1_hi; m1++) {
-        const int4 r1 = RS4[m1];
-        const int a = (int16_t)((uint32_t)r1.w >> 16);
-        if (a < 0) continue;
-        const int s1 = LK[m1] & 0xFFFF;
-        const int4 c1 = CS4[m1];
-        const int4 rs1 = RS4[s1];
-        const int4 cs1 = CS4[s1];
-        const uint32_t vca = VC[a];
-        const int ca = vca & 0xFF;
-        const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * NLp);  // T_ca[endc1][.]
-        const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp            // Tt_ca[pick(s1)][.]
-                               : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF)); // T_ca[.][pick(s1)]
-        const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : tsz * (c1.y & 0xFFFF);
-        const int row_tb2 = tsz * (int)((uint32_t)c1.y >> 16) * NLp;
-        const int ndepc1 = -r1.x, w1 = c1.x, nw1 = -c1.x;
-        const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
-        const int ka = rs1.z - r1.y - rs1.y;            // svco(s1) - inc1 - inc(s1)
-        const int slkA = P - F[a];
-        const int sv10 = c1.z, dsv1 = c1.w - c1.z;
-        // compatibility mask over q_bf: m1 heli-only needs bit 21 clear; m2 heli-only (bit 20) needs route a heli-ok
-        const int cmask = (MH[m1] ? (1 << 21) : 0) | (((vca >> 8) & 1) ? 0 : (1 << 20));
-        const ET *Erow = TABU ? E + m1 * V : nullptr;
-        // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
-        const ET *ecol = TABU ? ((TR && C.Et) ? C.Et + (size_t)a * C.n : E + a) : nullptr;
-        const int estr = (TR && C.Et) ? 1 : V;
-        const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;
-        const int tri = -m1 - 1;
+    for (int w0 = m1_lo; w0 < m1_hi; w0 += FB_ROWS) {
+        const int w_end = min(m1_hi, w0 + FB_ROWS);
+        if (K16) bk32 = 0xFFFFFFFFu;
+        for (int m1 = w0; m1 < w_end; m1++) {
+            const int4 r1 = RS4[m1];
+            const int a = (int16_t)((uint32_t)r1.w >> 16);
+            if (a < 0) continue;
+            const int s1 = LK[m1] & 0xFFFF;
+            const int4 c1 = CS4[m1];
+            const int4 rs1 = RS4[s1];
+            const int4 cs1 = CS4[s1];
+            const uint32_t vca = VC[a];
+            const int ca = vca & 0xFF;
+            const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * NLp);  // T_ca[endc1][.]
+            const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp            // Tt_ca[pick(s1)][.]
+                                   : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF)); // T_ca[.][pick(s1)]
+            const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : tsz * (c1.y & 0xFFFF);
+            const int row_tb2 = tsz * (int)((uint32_t)c1.y >> 16) * NLp;
+            const int ndepc1 = -r1.x, w1 = c1.x;
+            const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
+            const int ka = rs1.z - r1.y - rs1.y - sa;       // svco(s1) - inc1 - inc(s1) - asp
+            const int slkA = P - F[a] - sa;
+            const int sv10 = c1.z, dsv1 = c1.w - c1.z;
+            const int cmask = ((vca >> 8) & 1) ? 0 : (int)0x80000000;   // route a cannot fly heli-only missions
+            const int hmask = MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
+            const ET *Erow = TABU ? E + m1 * V : nullptr;
+            // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
+            const ET *ecol = TABU ? ((TR && C.Et) ? C.Et + (size_t)a * C.n : E + a) : nullptr;
+            const int estr = (TR && C.Et) ? 1 : V;
+            const int keyb = (1 << 30) + sa * 128 + (m1 - w0) * KS;               // K16: (2^23 + asp) << 7 | lid
+            const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;   // int32 tables
 #pragma unroll
-        for (int k = 0; k < KS; k++) {
-            if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
-            const int m2 = lo + lane + 32 * k;
-            const int bf = q_bf[k];
-            const int b = (int)(int16_t)(bf & 0xFFFF);
-            const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
-            const int a_yb1 = madd(q_e2[k], one, rowp1), a_tb2 = madd(q_p2[k], one, row_tb2);
-            const int Tya1 = TR ? (int)Ts[a_ya1] : lds_t<TT>((uint32_t)a_ya1);
-            const int Ta2 = TR ? (int)Tt[a_ta2] : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
-            const int Tyb1 = TR ? (int)Tt[a_yb1] : lds_t<TT>((uint32_t)a_yb1);
-            const int Tb2 = TR ? (int)Ts[a_tb2] : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
-            const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));                    // p1 -> m2
-            const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                       // p2 -> m1
-            const int da = madd(ya1, one, madd(Ta2, one, ka));
-            const int db = madd(yb1, one, madd(Tb2, one, q_kb[k]));
-            const int delta = madd(da, one, db);
-            const int mf = a == b ? madd(delta, neg, slkA) : min(madd(da, neg, slkA), madd(db, neg, q_slk[k]));
-            // link margins; the triangle m2 > m1 and compatibility are folded into the first one
-            const int l1 = madd(bf & cmask, -512, madd(ya1, neg, madd(q_w2[k], one, ndepc1)));
-            const int mg = min(min(min(l1, madd(Ta2, neg, madd(q_w2[k], neg, wsv1))),
-                                   min(madd(yb1, neg, madd(q_dep2[k], neg, w1)), madd(Tb2, neg, madd(q_ws2[k], one, nw1)))),
-                               min(mf, madd(m2, one, tri)));
-            uint32_t nadm;
-            if (TABU) {
-                const int t1 = madd(it, neg, (int)Erow[b]);                      // E[m1][b] - it
-                const int t2 = madd(it, neg, (int)ecol[max(m2, 0) * estr]);      // E[m2][a] - it
-                const int e2 = madd(asp, neg, delta);
-                nadm = ~(uint32_t)((t1 & t2) | e2) & 0x80000000u;
-            } else {
-                nadm = ~(uint32_t)delta & 0x80000000u;
+            for (int k = 0; k < KS; k++) {
+                if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+                const int bf = q_bf[k];
+                const int b = bf & 0xFFFF;
+                const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
+                const int a_yb1 = madd(q_e2[k], one, rowp1), a_tb2 = madd(q_p2[k], one, row_tb2);
+                const int Tya1 = TR ? (int)Ts[a_ya1] : lds_t<TT>((uint32_t)a_ya1);
+                const int Ta2 = TR ? (int)Tt[a_ta2] : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
+                const int Tyb1 = TR ? (int)Tt[a_yb1] : lds_t<TT>((uint32_t)a_yb1);
+                const int Tb2 = TR ? (int)Ts[a_tb2] : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
+                const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));                    // p1 -> m2
+                const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                       // p2 -> m1
+                const int da = ya1 + Ta2 + ka;                                                    // (- asp)
+                const int db = yb1 + Tb2 + q_kb[k];
+                const int dl = madd(da, one, db);                                                 // delta - asp
+                const int mfA = madd(da, neg, slkA);                                              // F_a + da <= P
+                const int mfB = madd(db, neg, q_slk[k] & hmask);                                  // F_b + db <= P
+                const int l1 = madd(ya1, neg, madd(q_w2[k], one, ndepc1));                        // dep(p1) + ya1 <= w2
+                const int l2 = wsv1 - q_w2[k] - Ta2;                                              // w2 + d(m2,s1) <= w(s1)
+                const int l3 = w1 - q_dep2[k] - yb1;                                              // dep(p2) + yb1 <= w1
+                const int l4 = q_ws2[k] - w1 - Tb2;                                               // w1 + d(m1,s2) <= w(s2)
+                const int trim = mlane + (32 * k - 1) - m1;                                       // m2 - m1 - 1 >= 0
+                const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
+                uint32_t nadm;
+                if (TABU) {
+                    const int t1 = madd(it, neg, (int)Erow[b]);                                  // E[m1][b] - it
+                    const int t2 = madd(it, neg, (int)ecol[max(mlane + 32 * k, 0) * estr]);      // E[m2][a] - it
+                    nadm = ~(uint32_t)((t1 & t2) | dl) & 0x80000000u;
+                } else {
+                    nadm = ~(uint32_t)dl & 0x80000000u;
+                }
+                if constexpr (K16) {
+                    const uint32_t k32 = (uint32_t)madd(dl, 128, keyb + k) | nadm | (uint32_t)(mg >> 31);
+                    bk32 = min(bk32, k32);
+                } else {
+                    const uint32_t k32 = (uint32_t)madd(dl, one, DELTA_BIAS + sa) | nadm | (uint32_t)(mg >> 31);
+                    const bool better = k32 < bk32;
+                    bk32 = better ? k32 : bk32;
+                    bidx = better ? base + 32 * k : bidx;
+                }
             }
-            const uint32_t k32 = (uint32_t)madd(delta, one, DELTA_BIAS) | nadm | (uint32_t)(mg >> 31);
-            const bool better = k32 < bk32;
-            bk32 = better ? k32 : bk32;
-            bidx = better ? base + 32 * k : bidx;
+        }
+        if (K16 && bk32 != 0xFFFFFFFFu) {
+            const int lid = bk32 & 127;
+            const uint32_t idx = Rb + (uint32_t)(w0 + lid / KS) * (uint32_t)n + (uint32_t)(lo + lane + 32 * (lid % KS));
+            const uint32_t d = ((bk32 >> 7) & 0xFFFFFFu) + (uint32_t)(DELTA_BIAS - (1 << 23));
+            const uint64_t key = ((uint64_t)((bk32 & 0x80000000u) | d) << 32) | idx;
+            best = key < best ? key : best;
         }
     }
-    return bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+    if (!K16) best = bk32 == 0xFFFFFFFFu ? KEY_NONE : (((uint64_t)bk32 << 32) | bidx);
+    return best;
 }
 
 // ---------------------------------------------------------------------------
