@@ -109,3 +109,38 @@ def test_window_equals_fast_kernel(A, ctx, mode, tenure, monkeypatch):
     (r1, t1, p1, m1), (r0, t0, p0, m0) = out
     assert (r1 == r0).all() and (t1 == t0).all() and (p1 == p0).all() and (m1 == m0).all()
     assert len(set(r1["best_obj"].tolist())) > 1   # the runs differ (seeded kicks)
+
+
+def _far_location(inst, t_far=60000):
+    """The instance plus one location no base or mission uses, 60000 s from everything: the
+    node costs d_c(x, m) = T_c[x][pick_m] + T_c[pick_m][del_m] then exceed uint16 (the window
+    scorers' staged table) while T itself still fits uint16."""
+    T = inst.travel_s
+    nc, nl, _ = T.shape
+    T2 = np.full((nc, nl + 1, nl + 1), t_far, np.int32)
+    T2[:, :nl, :nl] = T
+    for c in range(nc):
+        T2[c, nl, nl] = 0
+    inst.travel_s = T2
+    return inst
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_window_fallback_large_node_costs(A, ctx, oracle_mod, mode):
+    """Node costs above 65535 s: the batched kernel falls back to the FAST scorers
+    (shared-memory tabu matrix, 64-bit keys); sampled runs still equal the oracle."""
+    inst = _far_location(instgen.generate("batched"))
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    R, iters = 64, 200
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    tr = np.zeros((R, iters), A.TRACE_DTYPE)
+    prm = A.params(mode=mode, tenure=10, max_iters=iters, kick=8, trace_level=1)
+    A.as_batch_run(ctx, h, R, p, m, prm, seeds, shared_start=True, results=res, trace_out=tr)
+    for r in (0, 31, R - 1):
+        o = O.search(p, m, mode=mode, tenure=10, max_iters=iters, seed=int(seeds[r]), kick=8)
+        k = o["iters_done"]
+        assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == k
+        assert (tr[r]["idx"][:k] == o["trace"]["idx"]).all()
