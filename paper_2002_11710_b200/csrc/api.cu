@@ -690,7 +690,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
     // window scorers (window.cuh) for the batched kernel: every move kind, positive service legs, uint16 table,
     // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
-    bool win = (P->move_mask & 15u) == 15u && D->svcpos && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
+    bool win = (P->move_mask & 15u) == 15u && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
                (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
     size_t sh_b = 0, run_b = 0;
     batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure, I->tsym != 0);
@@ -966,7 +966,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     for (int j = 0; j < n_jobs && win; j++) {
         const DevInst *D;
         if ((st = get_dev_inst(ctx, jobs[j].inst, &D)) != AS_OK) return st;
-        if (D->svcpos && (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535)) win = false;
+        if (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535) win = false;
     }
     int64_t run0 = 0, bp0 = 0, bm0 = 0, e0 = 0;
     for (int j = 0; j < n_jobs; j++) {
@@ -975,7 +975,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
         BatchJob &b = J[j];
         b.inst = *D;
-        const bool wj = win && D->svcpos;
+        const bool wj = win;
         b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu, wj, P->tenure, I->tsym != 0);
         b.e_off = e0;
         if (wj && tabu) e0 += (int64_t)jobs[j].n_runs * I->n * I->V;
@@ -1069,7 +1069,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         CUDA_TRY(cudaEventRecord(ctx->evj, ctx->stream));
         CUDA_TRY(cudaStreamWaitEvent(ctx->cap, ctx->evj, 0));
         CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta + n_fast, n_gen, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->cap));
+                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->cap, win));
         ctx->launches++;
     }
     if (n_fast > 0) {
@@ -1078,7 +1078,7 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         ctx->launches++;
     } else {
         CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_gen, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->stream));
+                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->stream, win));
         ctx->launches++;
     }
     if (n_gen > 0 && n_fast > 0) {   // join

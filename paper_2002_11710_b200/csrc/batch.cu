@@ -76,7 +76,8 @@ void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
 // that run number).
 template <bool TABU, class TT, class ET, bool FULL, bool WIN>
 __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const BatchLayout &L, int NLp, int cta_run0) {
-    static_assert(!WIN || (FULL && sizeof(TT) == 2 && sizeof(ET) == 4), "window scorers: FAST, uint16 table, int32 E");
+    // WIN: the window scorers (every move kind); FULL then selects their positive-leg (svcpos) form
+    static_assert(!WIN || (sizeof(TT) == 2 && sizeof(ET) == 4), "window scorers: uint16 table, int32 E");
     extern __shared__ __align__(16) unsigned char smem[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC, NL = I.NL;
@@ -376,7 +377,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         // ============================ relocate block ============================
         for (int t0 = 0; t0 < S; t0 += 32 * KR) {
             uint64_t kb;
-            if constexpr (WIN) kb = score_reloc_win<TABU>(SC, W, t0, 0, n, it, asp, lane);
+            if constexpr (WIN) kb = score_reloc_win<TABU, FULL>(SC, W, t0, 0, n, it, asp, lane);
             else kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
                            : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
@@ -387,7 +388,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         // by the generic three-link formula below.
         for (int hi = n; hi > 1; hi -= 32 * KS) {
             uint64_t kb;
-            if constexpr (WIN) kb = score_swap_win<TABU>(SC, W, hi, 0, hi - 1, it, asp, lane);
+            if constexpr (WIN) kb = score_swap_win<TABU, FULL>(SC, W, hi, 0, hi - 1, it, asp, lane);
             else kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
                            : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
             kmin = kb < kmin ? kb : kmin;
@@ -549,9 +550,13 @@ static cudaError_t launch_jobs_t(const SearchArgs &A, const BatchJob *jobs, cons
 
 cudaError_t launch_batch_jobs(const SearchArgs &A, const BatchJob *jobs, const int4 *cta, int n_cta, int threads,
                               size_t smem, int mode, int tbytes, int ebytes, bool full, cudaStream_t st, bool win) {
-    if (win)   // window scorers: FULL, uint16 table, tabu matrix in global memory (int32)
-        return mode == 1 ? launch_jobs_t<true, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st)
-                         : launch_jobs_t<false, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st);
+    if (win) {   // window scorers: uint16 table, tabu matrix in global memory (int32); full = positive legs
+        if (full)
+            return mode == 1 ? launch_jobs_t<true, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st)
+                             : launch_jobs_t<false, uint16_t, int32_t, true, true>(A, jobs, cta, n_cta, threads, smem, st);
+        return mode == 1 ? launch_jobs_t<true, uint16_t, int32_t, false, true>(A, jobs, cta, n_cta, threads, smem, st)
+                         : launch_jobs_t<false, uint16_t, int32_t, false, true>(A, jobs, cta, n_cta, threads, smem, st);
+    }
     if (mode == 1) {
         if (tbytes == 2 && ebytes == 2)
             return full ? launch_jobs_t<true, uint16_t, int16_t, true>(A, jobs, cta, n_cta, threads, smem, st)
@@ -574,9 +579,13 @@ BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebyt
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,
                          cudaStream_t st, bool win) {
     const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
-    if (win)   // window scorers: FULL, uint16 table, tabu matrix in global memory (int32)
-        return mode == 1 ? launch_one<true, uint16_t, int32_t, true, true>(A, RPC, smem, st)
-                         : launch_one<false, uint16_t, int32_t, true, true>(A, RPC, smem, st);
+    if (win) {   // window scorers: uint16 table, tabu matrix in global memory (int32); positive legs or general
+        if (A.inst.svcpos)
+            return mode == 1 ? launch_one<true, uint16_t, int32_t, true, true>(A, RPC, smem, st)
+                             : launch_one<false, uint16_t, int32_t, true, true>(A, RPC, smem, st);
+        return mode == 1 ? launch_one<true, uint16_t, int32_t, false, true>(A, RPC, smem, st)
+                         : launch_one<false, uint16_t, int32_t, false, true>(A, RPC, smem, st);
+    }
     if (mode == 1) {
         if (tbytes == 2 && ebytes == 2)
             return full ? launch_one<true, uint16_t, int16_t, true>(A, RPC, smem, st)

@@ -92,10 +92,10 @@ __device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
 //        hmask = 0: row has no feasible move (skip); else 0x3FFFFFFF (m not heli-only) or ~0
 //        (heli-only); rowD = byte offset of table row del_m
 //   q1 = {TB[m], rem - asp (TS) or rem (NS), byte offset of TDT row m, 0}
-template <bool TABU>
+template <bool TABU, bool SV>
 __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m, int r,
                                                  int asp) {
-    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0);
+    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
     const int4 rm = C.RS4[m];
     const int a = (int16_t)((uint32_t)rm.w >> 16);
     if (a >= 0) {
@@ -105,19 +105,24 @@ __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_
         const int ca = C.VC[a] & 0xFF;
         const int Dps = (int)C.Ts[(ca * C.NL + (rm.w & 0xFFFF)) * C.NLp + (csx.y & 0xFFFF)] + rsx.z;
         const int rem = Dps - rm.y - rsx.y;   // removal delta d(p,s) - d(p,m) - d(m,s)
-        // link p->s (con7/con8) and route a's flight total after the removal (con6, reading #42)
-        if (rm.x + Dps <= csx.x && C.F[a] + rem <= C.P) {
+        // link p->s (con7/con8); with positive legs (SV) also route a's flight total after the removal
+        // (con6, reading #42: no intra-route move is feasible, so no move of the row is)
+        if (rm.x + Dps <= csx.x && (!SV || C.F[a] + rem <= C.P)) {
             const int4 cm = C.CS4[m];
             q0 = make_int4((rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR, C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF,
                            cm.x, 2 * (int)((uint32_t)cm.y >> 16) * C.NLp);
-            q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m * C.NLp, 0);
+            q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m * C.NLp, s);
+            // general legs: the same-route limit P - F_a - rem, and the inter-route bias (NEG when the
+            // removal alone leaves route a over the limit)
+            q2 = make_int4(C.P - C.F[a] - rem, C.F[a] + rem <= C.P ? 0 : NEG, a, 0);
         }
     }
     int4 *rec = W.WB + r * WIN_REC_INT4;
     rec[0] = q0; rec[1] = q1;
+    if (!SV) rec[2] = q2;
 }
 
-template <bool TABU>
+template <bool TABU, bool SV>
 __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int t0,
                                                     int m_lo, int m_hi, int it, int asp, int lane) {
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
@@ -152,7 +157,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
     uint64_t best = KEY_NONE;
     for (int w0 = m_lo; w0 < m_hi; w0 += WIN_ROWS) {
         __syncwarp();
-        if (w0 + lane < m_hi) win_reloc_record<TABU>(C, W, w0 + lane, lane, asp);
+        if (w0 + lane < m_hi) win_reloc_record<TABU, SV>(C, W, w0 + lane, lane, asp);
         __syncwarp();
         const int nr = min(WIN_ROWS, m_hi - w0);
         uint32_t bk = WIN_NONE;
@@ -164,7 +169,13 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
             const int4 q1 = rec[1];
             const int remk = q0.x, w_m = q0.z, rowD = q0.w;
             const uint32_t tb = (uint32_t)q1.x;
-            const int remasp = q1.y, rowM = q1.z;
+            const int remasp = q1.y, rowM = q1.z, sm = q1.w;
+            int intra_lim = 0, inter_bias = 0, am = 0;
+            if (!SV) {
+                const int4 q2 = rec[2];
+                intra_lim = q2.x; inter_bias = q2.y; am = q2.z;
+            }
+            const int m = w0 + r;
 #pragma unroll
             for (int k = 0; k < KR; k++) {
                 const int x1 = lds_t<uint16_t>((uint32_t)madd(c_x1[k], one, rowM));    // d_cb(c, m)
@@ -172,8 +183,16 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
                 const int ins = x1 + T2 + c_k[k];                                       // insertion delta
                 const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));                 // dep(c) + d(c,m) <= w_m
                 const int mB = c_wsv[k] - w_m - T2;                                     // w_m + d(m,t) <= w(t)
-                const int mC = madd(ins, neg, c_slk[k] & hmask);                        // F_b + ins <= P (+ heli)
-                const int mg = mA | mB | mC;
+                int mg;
+                if (SV) {
+                    const int mC = madd(ins, neg, c_slk[k] & hmask);                    // F_b + ins <= P (+ heli)
+                    mg = mA | mB | mC;
+                } else {   // general legs: same-route flight limit, explicit no-op targets (t = m, t = succ m)
+                    const int t = t0 + lane + 32 * k;
+                    const int lim = c_b[k] == am ? intra_lim : (c_slk[k] & hmask) + inter_bias;
+                    const int noop = (t == m) | (t == sm) ? -1 : 0;
+                    mg = mA | mB | (lim - ins) | noop;
+                }
                 const int e2 = madd(ins, one, remasp);                                  // delta - asp (TS) / delta (NS)
                 uint32_t nadm;
                 if (TABU) nadm = shl_clamp(tb, (uint32_t)c_b[k]) & ~(uint32_t)e2 & 0x80000000u;
@@ -197,11 +216,11 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 // m1 < m2; m2 over the lanes in a top-aligned chunk of 32 * KS (as score_swap_fast).
 // Record of row m1 (3 int4); TS folds the aspiration threshold asp into ka, slkA and keyb, so the
 // scorer's "delta" is delta - asp (its sign is the aspiration test) and the key still encodes delta:
-//   q0 = {cmask | a, TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses / offsets);
-//        cmask = bit 31 when route a cannot fly heli-only missions
+//   q0 = {cmask | s1 << 8 | a, TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses /
+//        offsets); cmask = bit 31 when route a cannot fly heli-only missions
 //   q1 = {-depc1, w1, w(s1) - svco(s1), svco(s1) - inc1 - inc(s1) - asp}
 //   q2 = {P - F_a - asp, keyb = (2^23 + asp) << 7 | r * KS, TB[m1], hmask (0: skip the row)}
-template <bool TABU>
+template <bool TABU, bool SV>
 __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m1, int r,
                                                 int tsm, int asp) {
     int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
@@ -215,7 +234,7 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
         const uint32_t vca = C.VC[a];
         const int ca = vca & 0xFF;
         const int sa = TABU ? asp : 0;
-        q0 = make_int4((((vca >> 8) & 1) ? 0 : (int)0x80000000) | a,
+        q0 = make_int4((((vca >> 8) & 1) ? 0 : (int)0x80000000) | a | (s1 << 8),
                        W.tdsm + 2 * ((ca * C.NL + (r1.w & 0xFFFF)) * W.NTDp),       // TD_ca[endc1][.]
                        W.ttsm + 2 * ((ca * C.NL + (cs1.y & 0xFFFF)) * C.NLp),       // Tt_ca[pick(s1)][.]
                        2 * (int)((uint32_t)c1.y >> 16) * C.NLp);                    // T_.[del1][.]
@@ -227,7 +246,7 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
     rec[0] = q0; rec[1] = q1; rec[2] = q2;
 }
 
-template <bool TABU>
+template <bool TABU, bool SV>
 __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int hi,
                                                    int m1_lo, int m1_hi, int it, int asp, int lane) {
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
@@ -240,13 +259,16 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
     const int tsm = (int)__cvta_generic_to_shared(C.Ts);
     // m2 side, per lane; q_bf = b | heli_only(m2) << 31, q_slk carries the heli offset
     int q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS], q_slk[KS], q_bf[KS];
+    int q_s2[KS];   // general legs only: succ(m2), for the adjacent pairs
     uint32_t q_tb[KS];
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
         int d2 = 0, e2 = W.tdtsm, p2 = tsm, w2 = 0, dep2 = 0, kb = 0, ws2 = NEG, slk = 0, bf = 0xFFFF;
         uint32_t tb = 0;
+        q_s2[k] = -1;
         if (m2 >= 0) {
+            if (!SV) q_s2[k] = LK[m2] & 0xFFFF;
             const int4 r2 = RS4[m2];
             const int b = (int16_t)((uint32_t)r2.w >> 16);
             if (b >= 0) {
@@ -275,7 +297,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
     uint64_t best = KEY_NONE;
     for (int w0 = m1_lo; w0 < m1_hi; w0 += WIN_ROWS) {
         __syncwarp();
-        if (w0 + lane < m1_hi) win_swap_record<TABU>(C, W, w0 + lane, lane, tsm, asp);
+        if (w0 + lane < m1_hi) win_swap_record<TABU, SV>(C, W, w0 + lane, lane, tsm, asp);
         __syncwarp();
         const int nr = min(WIN_ROWS, m1_hi - w0);
         uint32_t bk = WIN_NONE;
@@ -287,6 +309,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const int m1 = w0 + r;
             const int4 q0 = rec[0], q1 = rec[1];
             const int cmask = q0.x, a = q0.x & 0x3F, row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
+            const int s1 = (q0.x >> 8) & 0x7FFF;
             const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
             const int slkA = q2.x, keyb0 = q2.y;
             const uint32_t tb1 = (uint32_t)q2.z;
@@ -312,7 +335,15 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const int l3 = w1 - q_dep2[k] - yb1;                                        // dep(p2) + yb1 <= w1
                 const int l4 = q_ws2[k] - w1 - Tb2;                                         // w1 + d(m1,s2) <= w(s2)
                 const int trim = mlane + (32 * k - 1) - m1;                                 // m2 - m1 - 1 >= 0
-                const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
+                int mg;
+                if (SV) {
+                    mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
+                } else {   // general legs: same-route flight limit, explicit adjacent pairs
+                    const int m2 = mlane + 32 * k;
+                    const int mf = (int)b == a ? madd(delta, neg, slkA) : (mfA | mfB);   // F_a + delta <= P
+                    const int adj = (s1 == m2) | (q_s2[k] == m1) ? -1 : 0;
+                    mg = (l1 | l2 | l3) | (l4 | mf | adj) | (trim | (bf & cmask));
+                }
                 uint32_t nadm;                                                              // delta holds delta - asp
                 if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)delta & 0x80000000u;
                 else nadm = ~(uint32_t)delta & 0x80000000u;
