@@ -144,3 +144,49 @@ def test_window_fallback_large_node_costs(A, ctx, oracle_mod, mode):
         k = o["iters_done"]
         assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == k
         assert (tr[r]["idx"][:k] == o["trace"]["idx"]).all()
+
+
+def _zero_legs(cfg, k=6):
+    """The config's instance with k missions whose delivery is their pickup (a zero-length
+    service leg): the positive-leg shortcuts (readings #38, #42) do not apply, so the window
+    scorers take their general form (explicit no-op, adjacent-pair and same-route checks)."""
+    inst = instgen.generate(cfg)
+    inst.delivery_loc = inst.delivery_loc.copy()
+    inst.delivery_loc[:k] = inst.pickup_loc[:k]
+    return inst
+
+
+@pytest.mark.parametrize("cfg", ["ontario", "batched"])
+def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch):
+    inst = _zero_legs(cfg)
+    O = oracle_mod.Oracle(inst)
+    st, (p, m), _, _ = O.greedy(insert_mode=1)
+    if st != 0:
+        pytest.skip("no Alg. 1 start for the modified instance")
+    h = A.Instance(inst)
+    R, iters = 64, 300
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    for mode, tenure in ((1, 10), (0, 0)):
+        out = []
+        for win in ("1", "0"):
+            monkeypatch.setenv("AIRSCHED_WIN", win)
+            res = np.zeros(R, A.RESULT_DTYPE)
+            tr = np.zeros((R, iters), A.TRACE_DTYPE)
+            prm = A.params(mode=mode, tenure=tenure, max_iters=iters, kick=6, trace_level=1)
+            A.as_batch_run(ctx, h, R, p, m, prm, seeds, shared_start=True, results=res, trace_out=tr)
+            out.append((res, tr))
+        assert (out[0][0] == out[1][0]).all() and (out[0][1] == out[1][1]).all()
+        res, tr = out[0]
+        for r in (0, R - 1):
+            o = O.search(p, m, mode=mode, tenure=tenure, max_iters=iters, seed=int(seeds[r]), kick=6)
+            kk = o["iters_done"]
+            assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == kk
+            assert (tr[r]["idx"][:kk] == o["trace"]["idx"]).all()
+    # a single run on the batched kernel: full trace and final tabu matrix
+    monkeypatch.setenv("AIRSCHED_WIN", "1")
+    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+    prm = A.params(mode=1, tenure=7, max_iters=iters, trace_level=1, seed=3, kick=4)
+    g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)
+    o = O.search(p, m, mode=1, tenure=7, max_iters=iters, seed=3, kick=4)
+    assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and (g["tabu"] == o["E"]).all()
+    assert g["best_obj"] == o["best_obj"]
