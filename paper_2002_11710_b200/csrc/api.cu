@@ -742,7 +742,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             const bool e_global = env_int("AIRSCHED_GRID_E_GLOBAL", 0) == 1;
             for (auto o : gopts) {
                 if ((t_global && o.t) || (e_global && o.e)) continue;
-                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, 4, o.t, o.e && tabu, tabu);
+                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu, tabu);
                 if (b <= ctx->max_smem) {
                     GA.T_smem = o.t;
                     GA.E_smem = o.e && tabu;
@@ -752,6 +752,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 }
             }
             if (use_grid) {
+                GA.ebytes = ebytes;
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;

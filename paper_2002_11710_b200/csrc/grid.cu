@@ -346,12 +346,16 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
                         cudaStream_t st) {
     const DevInst &I = A.inst;
     GA.NLp = padded_stride(I.NL, tbytes);
-    GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, 4, GA.T_smem, GA.E_smem, mode == 1);
+    const int eb = mode == 1 && tbytes == 2 && GA.ebytes == 2 ? 2 : 4;   // int16 expiries: half the tabu traffic
+    GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, eb, GA.T_smem, GA.E_smem, mode == 1);
     const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     cudaError_t err;
     if (mode == 1) {
-        if (tbytes == 2) err = full ? launch_g<true, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)
-                                    : launch_g<true, uint16_t, int32_t, false>(A, GA, blocks, threads, smem, st);
+        if (tbytes == 2 && eb == 2)
+            err = full ? launch_g<true, uint16_t, int16_t, true>(A, GA, blocks, threads, smem, st)
+                       : launch_g<true, uint16_t, int16_t, false>(A, GA, blocks, threads, smem, st);
+        else if (tbytes == 2) err = full ? launch_g<true, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)
+                                         : launch_g<true, uint16_t, int32_t, false>(A, GA, blocks, threads, smem, st);
         else err = launch_g<true, int32_t, int32_t, false>(A, GA, blocks, threads, smem, st);
     } else {
         if (tbytes == 2) err = full ? launch_g<false, uint16_t, int32_t, true>(A, GA, blocks, threads, smem, st)

@@ -71,6 +71,7 @@ struct GridArgs {
     int NLp;                       // padded row stride of the travel-time table
     GridLayout L;
     int T_smem, E_smem;            // table / tabu matrix staged in shared memory?
+    int ebytes;                    // tabu expiry width: 2 when max_iters + tenure < 32767, else 4
     const void *Tglobal;           // padded table in global memory (uint16 or int32)
     int32_t *Eglobal;              // [n][V] tabu matrix when !E_smem
     int32_t *Etglobal;             // [V][n] its transpose (identical values), when !E_smem
