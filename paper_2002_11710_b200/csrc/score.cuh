@@ -301,6 +301,8 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
 // split between 3-input adds (ALU pipe) and mad.lo (FMA pipe) -- the scoring
 // loops are issue-bound, so every instruction removed counts.
 //
+// Global tables (TR) are read through the read-only data path (__ldg: the table never changes
+// during a run).
 // Keys: with a uint16 table (|delta| < 2^20) a lane keeps the 32-bit key
 // nadm << 31 | (delta + 2^23) << 7 | local index over blocks of 32 rows (one
 // unsigned min per move, the index recovered at the block's end, window.cuh);
@@ -375,8 +377,8 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
 #pragma unroll
             for (int k = 0; k < KR; k++) {
                 // T_cb[endc t][pick m], T_cb[del m][pick t]; shared table: byte addresses
-                const int T1 = TR ? (int)Tt[madd(c_t1[k], one, rowP)] : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
-                const int T2 = TR ? (int)Ts[madd(c_t2[k], one, rowD)] : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
+                const int T1 = TR ? (int)__ldg(&Tt[madd(c_t1[k], one, rowP)]) : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
+                const int T2 = TR ? (int)__ldg(&Ts[madd(c_t2[k], one, rowD)]) : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
                 const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));              // d(c, m)
                 const int ins = x1 + T2 + c_k[k];
                 const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));               // dep(c) + d(c,m) <= w_m
@@ -510,10 +512,10 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 const int b = bf & 0xFFFF;
                 const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
                 const int a_yb1 = madd(q_e2[k], one, rowp1), a_tb2 = madd(q_p2[k], one, row_tb2);
-                const int Tya1 = TR ? (int)Ts[a_ya1] : lds_t<TT>((uint32_t)a_ya1);
-                const int Ta2 = TR ? (int)Tt[a_ta2] : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
-                const int Tyb1 = TR ? (int)Tt[a_yb1] : lds_t<TT>((uint32_t)a_yb1);
-                const int Tb2 = TR ? (int)Ts[a_tb2] : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
+                const int Tya1 = TR ? (int)__ldg(&Ts[a_ya1]) : lds_t<TT>((uint32_t)a_ya1);
+                const int Ta2 = TR ? (int)__ldg(&Tt[a_ta2]) : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
+                const int Tyb1 = TR ? (int)__ldg(&Tt[a_yb1]) : lds_t<TT>((uint32_t)a_yb1);
+                const int Tb2 = TR ? (int)__ldg(&Ts[a_tb2]) : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
                 const int ya1 = madd(q_dsv[k], ca, madd(Tya1, one, q_sv0[k]));                    // p1 -> m2
                 const int yb1 = madd(q_cb[k], dsv1, madd(Tyb1, one, sv10));                       // p2 -> m1
                 const int da = ya1 + Ta2 + ka;                                                    // (- asp)
