@@ -190,3 +190,34 @@ def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch):
     o = O.search(p, m, mode=1, tenure=7, max_iters=iters, seed=3, kick=4)
     assert (g["trace"]["idx"] == o["trace"]["idx"]).all() and (g["tabu"] == o["E"]).all()
     assert g["best_obj"] == o["best_obj"]
+
+
+def test_determinism_repeated_runs(A, ctx, monkeypatch):
+    """the same call repeated gives byte-identical results, traces and best
+    schedules -- the batched kernel (window path), the whole-GPU kernel (C4 prefix) and the
+    multi-instance launch; no atomics touch anything but the packed keys."""
+    inst = instgen.generate("batched")
+    h = A.Instance(inst)
+    gp, gm, _ = A.as_init_greedy(ctx, h)
+    R, iters = 300, 200
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    outs = []
+    for _ in range(3):
+        res = np.zeros(R, A.RESULT_DTYPE)
+        tr = np.zeros((R, iters), A.TRACE_DTYPE)
+        bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
+        bm = np.zeros((R, inst.n_missions), np.int32)
+        prm = A.params(mode=1, tenure=10, max_iters=iters, kick=8, trace_level=1)
+        A.as_batch_run(ctx, h, R, gp, gm, prm, seeds, shared_start=True, results=res, best_ptr_out=bp,
+                       best_missions_out=bm, trace_out=tr)
+        outs.append((res.tobytes(), tr.tobytes(), bp.tobytes(), bm.tobytes()))
+    assert outs[0] == outs[1] == outs[2]
+    large = instgen.generate("large")
+    hl = A.Instance(large)
+    lp, lm, _ = A.as_init_greedy(ctx, hl)
+    runs = []
+    for _ in range(2):
+        g = A.as_tabu_run(ctx, hl, lp, lm, A.params(mode=1, tenure=10, max_iters=60, trace_level=1),
+                          want_trace=True, want_tabu=True)
+        runs.append((g["trace"].tobytes(), g["tabu"].tobytes(), g["best"][0].tobytes(), g["best"][1].tobytes()))
+    assert runs[0] == runs[1]
