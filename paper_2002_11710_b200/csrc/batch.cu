@@ -46,7 +46,7 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.VC = o; o = al16(o + V * 4);
     L.CH = o; o = al16(o + NC);
     L.TT = o; o = al16(o + (win && !tsym ? NC * NL * NLp * tbytes : 0));   // transposed table (window scorers)
-    L.TD = o; o = al16(o + (win ? NC * NL * padded_stride(n, 2) * 2 : 0));  // node costs d_c(x, m) (window scorers)
+    L.TD = o; o = al16(o + (win ? NC * td_layer(n + V, NL) * 2 : 0));         // node costs d_c(x, t) (window scorers)
     L.TDT = o; o = al16(o + (win ? NC * n * padded_stride(NL, 2) * 2 : 0)); // the same, [c][m][x]
     L.shared_bytes = o;
     int r = 0;
@@ -117,13 +117,15 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     }
     for (int i = tid; i < NC; i += blockDim.x) CH[i] = I.cls_heli[i];
     if (WIN) {   // node costs d_c(x, m) = T_c[x][pick_m] + T_c[pick_m][del_m] (O2), uint16 (tdmax checked on the host)
-        const int NTDp = padded_stride(n, 2);
+        // TD over every slot t (END_v: T_c[x][base_v], no service leg), class layers td_layer apart
+        const int NTDp = padded_stride(S, 2), LTD = td_layer(S, NL);
         uint16_t *TD = reinterpret_cast<uint16_t *>(smem + L.TD);
-        for (int i = tid; i < NC * NL * n; i += blockDim.x) {
-            const int c = i / (NL * n), x = (i / n) % NL, m = i % n;
-            const uint16_t d = (uint16_t)(I.T[(c * NL + x) * NL + I.pick[m]] + I.svc[c * n + m]);
-            TD[(c * NL + x) * NTDp + m] = d;
-            reinterpret_cast<uint16_t *>(smem + L.TDT)[(c * n + m) * padded_stride(NL, 2) + x] = d;
+        for (int i = tid; i < NC * NL * S; i += blockDim.x) {
+            const int c = i / (NL * S), x = (i / S) % NL, t = i % S;
+            const int pt = t < n ? I.pick[t] : I.vloc[t - n];
+            const uint16_t d = (uint16_t)(I.T[(c * NL + x) * NL + pt] + (t < n ? I.svc[c * n + t] : 0));
+            TD[c * LTD + x * NTDp + t] = d;
+            if (t < n) reinterpret_cast<uint16_t *>(smem + L.TDT)[(c * n + t) * padded_stride(NL, 2) + x] = d;
         }
     }
     __syncthreads();
@@ -260,7 +262,8 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     W.ttsm = (int)__cvta_generic_to_shared(WIN && !I.tsym ? (const void *)(smem + L.TT) : (const void *)Ts);
     W.tdsm = (int)__cvta_generic_to_shared(smem + L.TD);
     W.tdtsm = (int)__cvta_generic_to_shared(smem + L.TDT);
-    W.NTDp = padded_stride(n, 2);
+    W.NTDp = padded_stride(S, 2);
+    W.LTD = td_layer(S, NL);
     const int ring = A.tenure + 1;
     int it = 0, stop = 0;
     if (A.sweep) {

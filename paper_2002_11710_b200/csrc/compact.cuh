@@ -21,6 +21,15 @@ __host__ __device__ inline int padded_stride(int NL, int tbytes) {
     return (NL & 1) ? NL : NL + 1; // odd number of words
 }
 
+// Class-layer stride (halfwords) of the window scorers' node-cost table TD[c][x][t] (rows of
+// padded_stride(S, 2)): an odd multiple of 16 words, so that the two class layers of one row x
+// start 16 banks apart and 32 lanes reading consecutive slots t of either class hit 32 banks.
+__host__ __device__ inline int td_layer(int S, int NL) {
+    const int words = NL * padded_stride(S, 2) / 2;
+    const int w = (words + 31) / 32 * 32 + 16;   // >= words, == 16 (mod 32)
+    return 2 * (w - 32 >= words ? w - 32 : w);
+}
+
 // Mission view over the AoS records (same interface as MissionViewT).
 template <class TT>
 struct CompactMV {

@@ -60,9 +60,9 @@ struct WinCtx {
     int4 *WB;               // [WIN_ROWS][WIN_REC_INT4] this warp's window buffer (shared)
     const uint32_t *TB;     // [n] tabu bits: bit (31 - v) of TB[m] <=> E[m][v] >= it (TABU only)
     int ttsm;               // shared-window byte address of the transposed table (== the table's when symmetric)
-    int tdsm;               // shared-window byte address of TD[NC][NL][NTDp] (uint16 node costs)
+    int tdsm;               // shared-window byte address of TD[NC][LTD] (uint16 node costs d_c(x, t), rows NTDp)
     int tdtsm;              // ... of TDT[NC][n][NLp] (the same, transposed per class)
-    int NTDp;               // TD row stride (halfwords)
+    int NTDp, LTD;          // TD row stride and class-layer stride (halfwords, compact.cuh td_layer)
 };
 
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {   // x << s, 0 when s >= 32 (PTX shl)
@@ -110,7 +110,7 @@ __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_
         if (rm.x + Dps <= csx.x && (!SV || C.F[a] + rem <= C.P)) {
             const int4 cm = C.CS4[m];
             q0 = make_int4((rem + WIN_BIAS) * (1 << WIN_KEY_SHIFT) + r * KR, C.MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF,
-                           cm.x, 2 * (int)((uint32_t)cm.y >> 16) * C.NLp);
+                           cm.x, 2 * (int)((uint32_t)cm.y >> 16) * W.NTDp);
             q1 = make_int4(TABU ? (int)W.TB[m] : 0, TABU ? rem - asp : rem, 2 * m * C.NLp, s);
             // general legs: the same-route limit P - F_a - rem, and the inter-route bias (NEG when the
             // removal alone leaves route a over the limit)
@@ -135,7 +135,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
-        int x1 = W.tdtsm, t2 = tsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF;
+        int x1 = W.tdtsm, t2 = W.tdsm, dw = 0, kk = 0, wsv = NEG, slk = 0, b = 0xFFFF;
         if (t < S) {
             const int4 rs = RS4[t];
             const int bb = (int16_t)((uint32_t)rs.w >> 16);
@@ -145,10 +145,10 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
                 const int cb = vc & 0xFF;
                 b = bb;
                 x1 = W.tdtsm + 2 * (cb * C.n * NLp + (rs.w & 0xFFFF));      // TDT_cb column endc(t) (row m)
-                t2 = tsm + 2 * (cb * NL * NLp + (cs.y & 0xFFFF));            // column pick(t) of T_cb (row del_m)
+                t2 = W.tdsm + 2 * (cb * W.LTD + t);                          // TD_cb column t (row del_m)
                 dw = -rs.x;                                                 // -dep(pred t)
-                kk = rs.z - rs.y;                                           // svco(t) - inc(t)
-                wsv = cs.x - rs.z;                                          // w(t) - svco(t)
+                kk = -rs.y;                                                 // -inc(t)
+                wsv = cs.x;                                                 // w(t)
                 slk = (P - C.F[bb]) - (((vc >> 8) & 1) ? 0 : WIN_HELI_OFF);
             }
         }
@@ -179,7 +179,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 #pragma unroll
             for (int k = 0; k < KR; k++) {
                 const int x1 = lds_t<uint16_t>((uint32_t)madd(c_x1[k], one, rowM));    // d_cb(c, m)
-                const int T2 = lds_t<uint16_t>((uint32_t)madd(c_t2[k], one, rowD));    // T_cb[del m][pick t]
+                const int T2 = lds_t<uint16_t>((uint32_t)madd(c_t2[k], one, rowD));    // d_cb(m, t)
                 const int ins = x1 + T2 + c_k[k];                                       // insertion delta
                 const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));                 // dep(c) + d(c,m) <= w_m
                 const int mB = c_wsv[k] - w_m - T2;                                     // w_m + d(m,t) <= w(t)
@@ -235,7 +235,7 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
         const int ca = vca & 0xFF;
         const int sa = TABU ? asp : 0;
         q0 = make_int4((((vca >> 8) & 1) ? 0 : (int)0x80000000) | a | (s1 << 8),
-                       W.tdsm + 2 * ((ca * C.NL + (r1.w & 0xFFFF)) * W.NTDp),       // TD_ca[endc1][.]
+                       W.tdsm + 2 * (ca * W.LTD + (r1.w & 0xFFFF) * W.NTDp),       // TD_ca[endc1][.]
                        W.ttsm + 2 * ((ca * C.NL + (cs1.y & 0xFFFF)) * C.NLp),       // Tt_ca[pick(s1)][.]
                        2 * (int)((uint32_t)c1.y >> 16) * C.NLp);                    // T_.[del1][.]
         q1 = make_int4(-r1.x, c1.x, cs1.x - rs1.z, rs1.z - r1.y - rs1.y - sa);
