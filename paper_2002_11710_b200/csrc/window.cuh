@@ -44,6 +44,7 @@
 //    skipped.  Results are identical; the parity suite checks traces bit-exact.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "score.cuh"
 
@@ -301,11 +302,14 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
         __syncwarp();
         const int nr = min(WIN_ROWS, m1_hi - w0);
         uint32_t bk = WIN_NONE;
-        for (int r = 0; r < nr; r++) {
+        // One row m1 = w0 + r.  TRIM0 / TRIM1: sub-chunk k may hold m2 <= m1 (the triangle test is
+        // needed); SKIP0: sub-chunk 0 lies entirely on or below the diagonal.  Rows below lo need no
+        // triangle test at all, so the row loop is split into three ranges with their own bodies.
+        auto row = [&](int r, auto TRIM0, auto TRIM1, auto SKIP0) {
             const int4 *rec = W.WB + r * WIN_REC_INT4;
             const int4 q2 = rec[2];
             const int hmask = q2.w;
-            if (hmask == 0) continue;
+            if (hmask == 0) return;
             const int m1 = w0 + r;
             const int4 q0 = rec[0], q1 = rec[1];
             const int cmask = q0.x, a = q0.x & 0x3F, row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
@@ -317,7 +321,8 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const uint32_t ya_base = (uint32_t)madd(mlane, 2, row_ya1);   // TD_ca[endc1][m2 of sub-chunk 0]
 #pragma unroll
             for (int k = 0; k < KS; k++) {
-                if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+                if (k == 0 && decltype(SKIP0)::value) continue;
+                const bool trim_k = k ? decltype(TRIM1)::value : decltype(TRIM0)::value;
                 const int bf = q_bf[k];
                 const uint32_t b = (uint32_t)bf & 0xFFFFu;
                 static_assert(KS == 2, "immediate offsets below assume two sub-chunks");
@@ -334,15 +339,16 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const int l2 = wsv1 - q_w2[k] - Ta2;                                        // w2 + d(m2,s1) <= w(s1)
                 const int l3 = w1 - q_dep2[k] - yb1;                                        // dep(p2) + yb1 <= w1
                 const int l4 = q_ws2[k] - w1 - Tb2;                                         // w1 + d(m1,s2) <= w(s2)
-                const int trim = mlane + (32 * k - 1) - m1;                                 // m2 - m1 - 1 >= 0
+                const int tc = trim_k ? (mlane + (32 * k - 1) - m1) | (bf & cmask)          // m2 - m1 - 1 >= 0
+                                      : (bf & cmask);
                 int mg;
                 if (SV) {
-                    mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
+                    mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | tc;
                 } else {   // general legs: same-route flight limit, explicit adjacent pairs
                     const int m2 = mlane + 32 * k;
                     const int mf = (int)b == a ? madd(delta, neg, slkA) : (mfA | mfB);   // F_a + delta <= P
                     const int adj = (s1 == m2) | (q_s2[k] == m1) ? -1 : 0;
-                    mg = (l1 | l2 | l3) | (l4 | mf | adj) | (trim | (bf & cmask));
+                    mg = (l1 | l2 | l3) | (l4 | mf | adj) | tc;
                 }
                 uint32_t nadm;                                                              // delta holds delta - asp
                 if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)delta & 0x80000000u;
@@ -350,7 +356,13 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
             }
-        }
+        };
+        using F_ = std::integral_constant<bool, false>;
+        using T_ = std::integral_constant<bool, true>;
+        const int e1 = max(0, min(nr, lo - w0)), e2 = max(e1, min(nr, lo + 31 - w0));
+        for (int r = 0; r < e1; r++) row(r, F_{}, F_{}, F_{});    // m1 < lo: every lane above the diagonal
+        for (int r = e1; r < e2; r++) row(r, T_{}, F_{}, F_{});   // diagonal band of sub-chunk 0
+        for (int r = e2; r < nr; r++) row(r, F_{}, T_{}, T_{});   // sub-chunk 0 done; band of sub-chunk 1
         if (bk != WIN_NONE) {
             const int lid = bk & ((1 << WIN_KEY_SHIFT) - 1);
             const uint32_t idx = Rb + (uint32_t)(w0 + lid / KS) * (uint32_t)n + (uint32_t)(lo + lane + 32 * (lid % KS));
