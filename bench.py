@@ -283,6 +283,8 @@ def run_gpu(args):
         roof["ncu_alu_fma_pipe"] = [prof.get("alu_pipe"), prof.get("fma_pipe")]
     if "shared_wavefronts_pct_of_peak" in prof:   # the memory level that binds (HBM/L2 are ~0 by design)
         roof["ncu_shared_mem_pct_of_peak"] = prof["shared_wavefronts_pct_of_peak"]
+        if "duration_ms" in prof and "shared_wavefronts" in prof:   # 128 B per shared-memory wavefront
+            roof["ncu_shared_mem_GBps"] = prof["shared_wavefronts"] * 128 / (prof["duration_ms"] / 1e3) / 1e9
 
     if rank != 0:
         if world > 1:
