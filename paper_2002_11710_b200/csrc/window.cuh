@@ -90,13 +90,16 @@ __device__ __forceinline__ uint64_t win_key64(uint32_t bk, uint32_t idx) {
 // Relocate block: move m (route a, p -> m -> s) to just before slot t (route b, c -> t).
 // Record of row m (2 int4):
 //   q0 = {remk, hmask, w_m, rowD}   remk = (rem + 2^23) << 7 | r * KR (key base; item k adds k);
-//        hmask = 0: row has no feasible move (skip); else 0x3FFFFFFF (m not heli-only) or ~0
-//        (heli-only); rowD = byte offset of table row del_m
+//        hmask = 0x3FFFFFFF (m not heli-only) or ~0 (heli-only); w_m = NEG for a row without a feasible
+//        move; rowD = byte offset of TD row del_m
 //   q1 = {TB[m], rem - asp (TS) or rem (NS), byte offset of TDT row m, 0}
 template <bool TABU, bool SV>
 __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m, int r,
                                                  int asp) {
-    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
+    // a row without a feasible move keeps w_m = NEG: its first link margin is negative for every target,
+    // so the row loop needs no skip test (such rows are rare: by the triangle inequality the removal
+    // link p -> s and route a's total after the removal are normally feasible)
+    int4 q0 = make_int4(0, 0x3FFFFFFF, NEG, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
     const int4 rm = C.RS4[m];
     const int a = (int16_t)((uint32_t)rm.w >> 16);
     if (a >= 0) {
@@ -166,7 +169,6 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
             const int4 *rec = W.WB + r * WIN_REC_INT4;
             const int4 q0 = rec[0];
             const int hmask = q0.y;
-            if (hmask == 0) continue;
             const int4 q1 = rec[1];
             const int remk = q0.x, w_m = q0.z, rowD = q0.w;
             const uint32_t tb = (uint32_t)q1.x;
