@@ -222,11 +222,13 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
 //   q0 = {cmask | s1 << 8 | a, TD_ca row endc1, Tt_ca row pick(s1), T row del1}   (byte addresses /
 //        offsets); cmask = bit 31 when route a cannot fly heli-only missions
 //   q1 = {-depc1, w1, w(s1) - svco(s1), svco(s1) - inc1 - inc(s1) - asp}
-//   q2 = {P - F_a - asp, keyb = (2^23 + asp) << 7 | r * KS, TB[m1], hmask (0: skip the row)}
+//   q2 = {P - F_a - asp, keyb = (2^23 + asp) << 7 | r * KS, TB[m1], hmask}
 template <bool TABU, bool SV>
 __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int m1, int r,
                                                 int tsm, int asp) {
-    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
+    // an unassigned m1 (partial schedules) keeps -depc1 = NEG: every move of the row fails its first
+    // link margin, so the row loop needs no skip test; the table offsets stay valid addresses
+    int4 q0 = make_int4(0, W.tdsm, W.ttsm, 0), q1 = make_int4(NEG, 0, 0, 0), q2 = make_int4(0, 0, 0, 0x3FFFFFFF);
     const int4 r1 = C.RS4[m1];
     const int a = (int16_t)((uint32_t)r1.w >> 16);
     if (a >= 0) {
@@ -311,7 +313,6 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const int4 *rec = W.WB + r * WIN_REC_INT4;
             const int4 q2 = rec[2];
             const int hmask = q2.w;
-            if (hmask == 0) return;
             const int m1 = w0 + r;
             const int4 q0 = rec[0], q1 = rec[1];
             const int cmask = q0.x, a = q0.x & 0x3F, row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
