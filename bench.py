@@ -139,6 +139,15 @@ def valid_moves(inst):
     return n * (n + V - 2) + n * (n - 1) // 2
 
 
+def batched_config(cfg, inst, R, iters, world):
+    """`config` of the batched workload; the reference arm reports the same object."""
+    return {"workload": f"C3 batched: {R} tabu runs/GPU of a {inst.n_vehicles}-vehicle/"
+                        f"{inst.n_missions}-mission instance, {iters} iters, tenure {cfg.tenure}, kick {cfg.kick}",
+            "runs_per_gpu": R, "iters_per_run": iters, "valid_moves_per_iter": valid_moves(inst),
+            "instance_seed": inst.seed, "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"runs sharded over {world} GPU(s)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -159,11 +168,15 @@ def run_reference(args):
         tot_it += it
         tot_t += dt
     value = tot_it * valid_moves(inst) / tot_t
+    if cfg.n_runs > 1:   # the GPU arm's config; each step times a bounded sample of it (cpu_baseline.sample)
+        config = batched_config(cfg, inst, args.runs or cfg.n_runs, args.iters or cfg.max_iters, 1)
+    else:
+        config = {"workload": f"{args.workload}: n={inst.n_missions}, V={inst.n_vehicles}, TS",
+                  "valid_moves_per_iter": valid_moves(inst)}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"C3 batched ({args.workload})", "runs_per_step": runs, "iters_per_run": iters,
-                       "n_missions": inst.n_missions, "n_vehicles": inst.n_vehicles},
+            "config": config,
             "tabu_iters_per_s": tot_it / tot_t,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{runs} runs x {iters} TS iterations of the C3 instance per step"},
@@ -301,11 +314,7 @@ def run_gpu(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"C3 batched: {R} tabu runs/GPU of a {inst.n_vehicles}-vehicle/"
-                                   f"{inst.n_missions}-mission instance, {iters} iters, tenure {cfg.tenure}, kick {cfg.kick}",
-                       "runs_per_gpu": R, "iters_per_run": iters, "valid_moves_per_iter": VM,
-                       "instance_seed": inst.seed, "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"runs sharded over {world} GPU(s)"},
+            "config": batched_config(cfg, inst, R, iters, world),
             "tabu_iters_per_s": iters_all / (t_ms / 1e3),
             "best_objective_s": gb["best_obj"], "best_run": gb["best_run"],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
