@@ -4,12 +4,18 @@ seeded random instances outside the generator's shapes: 1-3 matrix layers
 scorers instead of the FAST ones), asymmetric tables, tight and loose deadlines,
 helicopter-only missions, small flight limits, 0..40 missions, 1..8 vehicles,
 and the no-wait variant."""
+import os
+
 import numpy as np
 import pytest
 
 from paper_2002_11710_b200 import instgen
 
 pytestmark = pytest.mark.gpu
+
+# longer sweeps on demand: AIRSCHED_FUZZ_SCALE multiplies the trial counts, AIRSCHED_FUZZ_SEED shifts the seeds
+SCALE = max(1, int(os.environ.get("AIRSCHED_FUZZ_SCALE", "1")))
+SEED = int(os.environ.get("AIRSCHED_FUZZ_SEED", "0"))
 
 
 @pytest.fixture(scope="module")
@@ -100,9 +106,9 @@ PATHS = {
 def test_fuzz_runs(A, ctx, oracle_mod, path, monkeypatch):
     for k, v in PATHS[path].items():
         monkeypatch.setenv(k, v)
-    rng = np.random.default_rng(20021171 + list(PATHS).index(path))
+    rng = np.random.default_rng(20021171 + list(PATHS).index(path) + SEED)
     done = 0
-    for trial in range(120):
+    for trial in range(120 * SCALE):
         inst = random_instance(rng)
         O = oracle_mod.Oracle(inst)
         start = feasible_start(O)
@@ -121,15 +127,15 @@ def test_fuzz_runs(A, ctx, oracle_mod, path, monkeypatch):
                     digest=(path == "k_search"))
         compare_run(A, ctx, O, h, p, m, 0, 0, 80)
         done += 1
-        if done >= 40:
+        if done >= 40 * SCALE:
             break
-    assert done >= 20
+    assert done >= 20 * SCALE
 
 
 def test_fuzz_eval_and_batch(A, ctx, oracle_mod):
-    rng = np.random.default_rng(7117)
+    rng = np.random.default_rng(7117 + SEED)
     done = 0
-    for trial in range(80):
+    for trial in range(80 * SCALE):
         inst = random_instance(rng)
         O = oracle_mod.Oracle(inst)
         start = feasible_start(O)
@@ -159,15 +165,15 @@ def test_fuzz_eval_and_batch(A, ctx, oracle_mod):
             assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == o["iters_done"]
             assert res[r]["best_iter"] == o["best_iter"] and res[r]["kicks_applied"] == o["kicks_applied"]
         done += 1
-        if done >= 25:
+        if done >= 25 * SCALE:
             break
-    assert done >= 12
+    assert done >= 12 * SCALE
 
 
 def test_fuzz_nowait_and_greedy(A, ctx, oracle_mod):
-    rng = np.random.default_rng(99173)
+    rng = np.random.default_rng(99173 + SEED)
     done = 0
-    for trial in range(80):
+    for trial in range(80 * SCALE):
         inst = random_instance(rng, no_wait=1)
         O = oracle_mod.Oracle(inst)
         h = A.Instance(inst)
@@ -188,6 +194,6 @@ def test_fuzz_nowait_and_greedy(A, ctx, oracle_mod):
         od, of, ok = O.eval_moves(p, m, mode=0)
         assert (d == od).all() and (f == of).all()
         done += 1
-        if done >= 20:
+        if done >= 20 * SCALE:
             break
-    assert done >= 10
+    assert done >= 10 * SCALE
