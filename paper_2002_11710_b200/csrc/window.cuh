@@ -299,6 +299,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
         q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_tb[k] = tb;
     }
     const int mlane = lo + lane;   // m2 of sub-chunk 0 (sub-chunk k: + 32 k)
+    const int NLp2 = 2 * NLp;
     uint64_t best = KEY_NONE;
     for (int w0 = m1_lo; w0 < m1_hi; w0 += WIN_ROWS) {
         __syncwarp();
@@ -309,18 +310,20 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
         // One row m1 = w0 + r.  TRIM0 / TRIM1: sub-chunk k may hold m2 <= m1 (the triangle test is
         // needed); SKIP0: sub-chunk 0 lies entirely on or below the diagonal.  Rows below lo need no
         // triangle test at all, so the row loop is split into three ranges with their own bodies.
+        // row terms that depend on m1 = w0 + r, formed from r by one add / IMAD each
+        const int rowM1_w0 = w0 * NLp2;          // TDT row offset of m1 = w0
+        const int trim_w0 = mlane - 1 - w0;      // m2 - m1 - 1 of sub-chunk 0 at m1 = w0
         auto row = [&](int r, auto TRIM0, auto TRIM1, auto SKIP0) {
             const int4 *rec = W.WB + r * WIN_REC_INT4;
             const int4 q2 = rec[2];
             const int hmask = q2.w;
-            const int m1 = w0 + r;
             const int4 q0 = rec[0], q1 = rec[1];
             const int cmask = q0.x, a = q0.x & 0x3F, row_ya1 = q0.y, row_ta2 = q0.z, rowD = q0.w;
             const int s1 = (q0.x >> 8) & 0x7FFF;
             const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
             const int slkA = q2.x, keyb0 = q2.y;
             const uint32_t tb1 = (uint32_t)q2.z;
-            const int rowM1 = 2 * m1 * NLp;   // TDT row m1
+            const int rowM1 = madd(r, NLp2, rowM1_w0);   // TDT row m1 (2 m1 NLp)
             const uint32_t ya_base = (uint32_t)madd(mlane, 2, row_ya1);   // TD_ca[endc1][m2 of sub-chunk 0]
 #pragma unroll
             for (int k = 0; k < KS; k++) {
@@ -342,13 +345,13 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                 const int l2 = wsv1 - q_w2[k] - Ta2;                                        // w2 + d(m2,s1) <= w(s1)
                 const int l3 = w1 - q_dep2[k] - yb1;                                        // dep(p2) + yb1 <= w1
                 const int l4 = q_ws2[k] - w1 - Tb2;                                         // w1 + d(m1,s2) <= w(s2)
-                const int tc = trim_k ? (mlane + (32 * k - 1) - m1) | (bf & cmask)          // m2 - m1 - 1 >= 0
+                const int tc = trim_k ? (trim_w0 + 32 * k - r) | (bf & cmask)               // m2 - m1 - 1 >= 0
                                       : (bf & cmask);
                 int mg;
                 if (SV) {
                     mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | tc;
                 } else {   // general legs: same-route flight limit, explicit adjacent pairs
-                    const int m2 = mlane + 32 * k;
+                    const int m1 = w0 + r, m2 = mlane + 32 * k;
                     const int mf = (int)b == a ? madd(delta, neg, slkA) : (mfA | mfB);   // F_a + delta <= P
                     const int adj = (s1 == m2) | (q_s2[k] == m1) ? -1 : 0;
                     mg = (l1 | l2 | l3) | (l4 | mf | adj) | tc;
