@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (building the checker is not using it)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _LIB, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-pthread", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -189,6 +189,35 @@ class Oracle:
         tp = (lambda k: _p(tr[k])) if trace else (lambda k: None)
         lib().or_search(self.ref, _p(length), _p(r), C.byref(prm), _p(bl), _p(br), _p(fl), _p(fr), C.byref(res),
                         tp("idx"), tp("delta"), tp("cur"), tp("best"), tp("cls"), tp("digest"), _p(E))
+        k = res.iters_done
+        out = dict(best_obj=res.best_obj, final_obj=res.final_obj, start_obj=res.start_obj,
+                   best_iter=res.best_iter, iters_done=k, stop_reason=res.stop_reason,
+                   kicks_applied=res.kicks_applied, best=self.to_csr(bl, br), final=self.to_csr(fl, fr),
+                   E=E[:n])
+        if trace:
+            out["trace"] = {key: val[:k].copy() for key, val in tr.items()}
+        return out
+
+    def search_par(self, ptr, ms, mode=MODE_TABU, tenure=10, max_iters=100, seed=0, kick=0, mask=0xF,
+                   strict_tabu_stop=False, threads=None, memo=True, trace=True):
+        """or_search driven over `threads` index chunks (+ memo of unchanged moves):
+        the full-length parity driver for the large configs.  Same results as search()."""
+        length, r = self.to_lists(ptr, ms)
+        V, n = self.V, self.n
+        threads = int(threads or os.cpu_count() or 1)
+        bl, br = np.zeros_like(length), np.zeros_like(r)
+        fl, fr = np.zeros_like(length), np.zeros_like(r)
+        K = max(int(max_iters), 1)
+        tr = dict(idx=np.zeros(K, np.int64), delta=np.zeros(K, np.int32), cur=np.zeros(K, np.int64),
+                  best=np.zeros(K, np.int64), cls=np.zeros(K, np.int32))
+        E = np.zeros((max(n, 1), V), np.int32)
+        prm = _Params(int(mode), int(tenure), int(max_iters), int(kick), int(bool(strict_tabu_stop)), 0, int(mask),
+                      int(seed))
+        res = _Result()
+        tp = (lambda k: _p(tr[k])) if trace else (lambda k: None)
+        lib().or_search_par(self.ref, _p(length), _p(r), C.byref(prm), C.c_int32(threads), C.c_int32(int(bool(memo))),
+                            _p(bl), _p(br), _p(fl), _p(fr), C.byref(res), tp("idx"), tp("delta"), tp("cur"),
+                            tp("best"), tp("cls"), _p(E))
         k = res.iters_done
         out = dict(best_obj=res.best_obj, final_obj=res.final_obj, start_obj=res.start_obj,
                    best_iter=res.best_iter, iters_done=k, stop_reason=res.stop_reason,

@@ -8,6 +8,7 @@
  * /root/reference/PAPER.md ("P:n"); readings #k refer to DESIGN.md's
  * ambiguity ledger (= SURVEY.md §8(c).2).
  */
+#define _POSIX_C_SOURCE 200809L  /* pthread barriers (the parallel driver) */
 #include "oracle.h"
 
 #include <stdlib.h>
@@ -744,5 +745,230 @@ int32_t or_sweep(const or_inst *I, const int32_t *len0, const int32_t *r0, const
     res->best_obj = best;
     res->final_obj = cur;
     free(len); free(r); free(E); free(perm); free(snap);
+    return 0;
+}
+
+/* ------------------------------------------- parallel driver of O10/O11 -- */
+/* A faster DRIVER of the same search for the full-length parity checks on the
+ * large configs (C4: 20,000 iterations over 393,750 valid moves; C5: 1,000
+ * over 24.4 M).  It changes no arithmetic: every per-move value still comes
+ * from eval_one / is_tabu above, and the selection rule is select_move's
+ * (admissible before by-default, smallest delta, lowest index).  Two things
+ * differ, both pinned against or_search (tests/test_oracle_driver.py):
+ *   (1) the canonical index range is cut into `threads` contiguous chunks
+ *       scanned concurrently; each chunk keeps its lowest-index minimum with
+ *       select_move's strict '<', and the chunk results are merged in chunk
+ *       order with the same strict '<' -- the global lowest-index minimum;
+ *   (2) with memo != 0, a move's (VALID, FEASIBLE, delta) is kept from the
+ *       previous iteration unless the move touches a route the last applied
+ *       move changed.  eval_one reads only the routes of the move's m (m1)
+ *       and t (m2) (route-local mode), and a mission changes route only if it
+ *       lies in a changed route before and after, so a move whose routes are
+ *       both unchanged has the same values; TABU and ADMISSIBLE depend on E,
+ *       it, cur and best and are recomputed for every move every iteration. */
+#include <pthread.h>
+
+typedef struct {
+    const or_inst *I;
+    const int32_t *len, *r;
+    const or_params *prm;
+    const int32_t *E;
+    int32_t it;
+    int64_t best_obj, lo, hi;
+    int32_t memo, first;
+    const uint8_t *changed;    /* [V] routes changed by the last move */
+    int32_t *m_delta;          /* memo [N] */
+    uint8_t *m_flags;          /* memo [N]: VALID | FEASIBLE */
+    /* chunk result */
+    int64_t adm_idx, adm_delta, def_idx, def_delta;
+    /* persistent worker: waits at `start`, scans, meets the driver at `done` */
+    pthread_barrier_t *start, *done;
+    volatile int32_t *quit;
+} par_chunk;
+
+static void *par_select_chunk(void *arg) {
+    par_chunk *C = (par_chunk *)arg;
+    const or_inst *I = C->I;
+    const int64_t n = I->n, V = I->V, Rb = n * (n + V);
+    evalctx X;
+    evalctx_init(&X, I, C->len, C->r);
+    C->adm_idx = C->def_idx = -1;
+    C->adm_delta = C->def_delta = 0;
+    /* (u, w) = (m, t) in the relocate block, (m1, m2) in the swap block, stepped
+     * along with idx (no division per index) */
+    int64_t u, w;
+    if (C->lo < Rb) { u = C->lo / (n + V); w = C->lo % (n + V); }
+    else { u = (C->lo - Rb) / (n > 0 ? n : 1); w = (C->lo - Rb) % (n > 0 ? n : 1); }
+    for (int64_t idx = C->lo; idx < C->hi; idx++) {
+        if (idx == Rb) { u = 0; w = 0; }
+        else if (idx > C->lo) {
+            if (++w == (idx < Rb ? n + V : n)) { w = 0; u++; }
+        }
+        move_t mv;
+        int64_t delta = 0;
+        int32_t feas = 0, valid;
+        int32_t fresh = 1;
+        if (C->memo && !C->first) {
+            /* routes the move reads: those of m and t (relocate) or m1 and m2 (swap) */
+            int32_t ra = X.veh[u], rb;
+            if (idx < Rb) rb = w < n ? X.veh[w] : (int32_t)(w - n);
+            else rb = X.veh[w];
+            fresh = (ra >= 0 && C->changed[ra]) || (rb >= 0 && C->changed[rb]);
+        }
+        if (fresh) {
+            valid = eval_one(&X, C->len, C->r, idx, C->prm->mask, 0, &mv, &delta, &feas);
+            if (C->memo) {
+                C->m_delta[idx] = (int32_t)delta;
+                C->m_flags[idx] = (uint8_t)((valid ? OR_FLAG_VALID : 0) | (valid && feas ? OR_FLAG_FEASIBLE : 0));
+            }
+        } else {
+            valid = (C->m_flags[idx] & OR_FLAG_VALID) != 0;
+            feas = (C->m_flags[idx] & OR_FLAG_FEASIBLE) != 0;
+            delta = C->m_delta[idx];
+            if (!valid || !feas) continue;
+            /* skip the tabu test of a move that cannot be selected whatever its class
+             * (strict '<', ascending scan): no smaller than both running minima, or no
+             * smaller than an admissible one (an admissible move anywhere beats every
+             * by-default move, so this chunk's by-default minimum is then never used) */
+            if (C->adm_idx >= 0 && delta >= C->adm_delta) continue;
+            if (C->prm->mode == OR_MODE_TABU)
+                build_move(I, C->len, C->r, X.veh, X.pos, idx, C->prm->mask, &mv, X.ra, X.rb);  /* its pairs */
+        }
+        if (!valid || !feas) continue;
+        int32_t admissible;
+        if (C->prm->mode == OR_MODE_TABU)
+            admissible = !is_tabu(I, &mv, C->E, C->it) || X.cur + delta < C->best_obj;
+        else
+            admissible = delta < 0;
+        if (admissible) {
+            if (C->adm_idx < 0 || delta < C->adm_delta) { C->adm_idx = idx; C->adm_delta = delta; }
+        } else {
+            if (C->def_idx < 0 || delta < C->def_delta) { C->def_idx = idx; C->def_delta = delta; }
+        }
+    }
+    evalctx_free(&X);
+    return NULL;
+}
+
+static void *par_worker(void *arg) {
+    par_chunk *C = (par_chunk *)arg;
+    for (;;) {
+        pthread_barrier_wait(C->start);
+        if (*C->quit) break;
+        par_select_chunk(C);
+        pthread_barrier_wait(C->done);
+    }
+    return NULL;
+}
+
+int32_t or_search_par(const or_inst *I, const int32_t *len0, const int32_t *r0, const or_params *prm,
+                      int32_t threads, int32_t memo, int32_t *best_len, int32_t *best_r, int32_t *final_len,
+                      int32_t *final_r, or_result *res, int64_t *tr_idx, int32_t *tr_delta, int64_t *tr_cur,
+                      int64_t *tr_best, int32_t *tr_cls, int32_t *E_out) {
+    int32_t n = I->n, V = I->V;
+    if (threads < 1) threads = 1;
+    size_t rs = sizeof(int32_t) * (size_t)V * (size_t)(n > 0 ? n : 1);
+    int64_t N = or_move_space_size(I);
+    int32_t *len = (int32_t *)malloc(sizeof(int32_t) * (size_t)V);
+    int32_t *r = (int32_t *)malloc(rs);
+    int32_t *E = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1) * (size_t)V);
+    uint8_t *changed = (uint8_t *)calloc((size_t)V, 1);
+    int32_t *m_delta = memo ? (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1)) : NULL;
+    uint8_t *m_flags = memo ? (uint8_t *)malloc((size_t)(N > 0 ? N : 1)) : NULL;
+    par_chunk *C = (par_chunk *)calloc((size_t)threads, sizeof(par_chunk));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    pthread_barrier_t bstart, bdone;
+    volatile int32_t quit = 0;
+    if (threads > 1) {
+        pthread_barrier_init(&bstart, NULL, (unsigned)threads + 1);
+        pthread_barrier_init(&bdone, NULL, (unsigned)threads + 1);
+        for (int32_t q = 0; q < threads; q++) {
+            C[q].start = &bstart; C[q].done = &bdone; C[q].quit = &quit;
+            pthread_create(&th[q], NULL, par_worker, &C[q]);
+        }
+    }
+    memcpy(len, len0, sizeof(int32_t) * (size_t)V);
+    memcpy(r, r0, rs);
+    for (int64_t k = 0; k < (int64_t)n * V; k++) E[k] = -1;
+
+    memset(res, 0, sizeof(*res));
+    res->kicks_applied = or_kick(I, len, r, prm->seed, prm->kick);
+    int64_t cur = or_objective(I, len, r);
+    int64_t best = cur;
+    res->start_obj = cur;
+    res->best_iter = -1;
+    memcpy(best_len, len, sizeof(int32_t) * (size_t)V);
+    memcpy(best_r, r, rs);
+    int32_t it;
+    for (it = 0; it < prm->max_iters; it++) {
+        for (int32_t q = 0; q < threads; q++) {
+            par_chunk *c = &C[q];
+            c->I = I; c->len = len; c->r = r; c->prm = prm;
+            c->E = prm->mode == OR_MODE_TABU ? E : NULL;
+            c->it = it; c->best_obj = best;
+            c->lo = N * q / threads; c->hi = N * (q + 1) / threads;
+            c->memo = memo; c->first = it == 0; c->changed = changed;
+            c->m_delta = m_delta; c->m_flags = m_flags;
+            if (threads == 1) par_select_chunk(c);
+        }
+        if (threads > 1) {
+            pthread_barrier_wait(&bstart);   /* workers scan their chunks */
+            pthread_barrier_wait(&bdone);
+        }
+        /* merge in chunk order with select_move's strict '<' */
+        int64_t adm_idx = -1, adm_delta = 0, def_idx = -1, def_delta = 0;
+        for (int32_t q = 0; q < threads; q++) {
+            if (C[q].adm_idx >= 0 && (adm_idx < 0 || C[q].adm_delta < adm_delta)) { adm_idx = C[q].adm_idx; adm_delta = C[q].adm_delta; }
+            if (C[q].def_idx >= 0 && (def_idx < 0 || C[q].def_delta < def_delta)) { def_idx = C[q].def_idx; def_delta = C[q].def_delta; }
+        }
+        int32_t cls;
+        int64_t delta, idx;
+        if (adm_idx >= 0) { cls = 0; delta = adm_delta; idx = adm_idx; }
+        else if (def_idx >= 0) { cls = 1; delta = def_delta; idx = def_idx; }
+        else { cls = -1; delta = 0; idx = -1; }
+        if (cls < 0) { res->stop_reason = 2; break; }
+        if (cls == 1 && prm->mode == OR_MODE_NS) { res->stop_reason = 1; break; }
+        if (cls == 1 && prm->strict_tabu_stop) { res->stop_reason = 2; break; }
+        evalctx X;
+        evalctx_init(&X, I, len, r);
+        move_t mv;
+        int64_t d2;
+        int32_t f2;
+        eval_one(&X, len, r, idx, prm->mask, 0, &mv, &d2, &f2);
+        write_back(I, len, r, &mv, X.ra, X.rb);
+        evalctx_free(&X);
+        memset(changed, 0, (size_t)V);
+        changed[mv.a] = 1;
+        changed[mv.b] = 1;
+        cur += delta;
+        if (prm->mode == OR_MODE_TABU)
+            for (int32_t k = 0; k < mv.n_pairs; k++)
+                E[(int64_t)mv.from_m[k] * V + mv.from_v[k]] = it + prm->tenure;
+        if (cur < best) {
+            best = cur;
+            res->best_iter = it;
+            memcpy(best_len, len, sizeof(int32_t) * (size_t)V);
+            memcpy(best_r, r, rs);
+        }
+        if (tr_idx) tr_idx[it] = idx;
+        if (tr_delta) tr_delta[it] = (int32_t)delta;
+        if (tr_cur) tr_cur[it] = cur;
+        if (tr_best) tr_best[it] = best;
+        if (tr_cls) tr_cls[it] = cls;
+    }
+    res->iters_done = it;
+    res->best_obj = best;
+    res->final_obj = cur;
+    if (final_len) memcpy(final_len, len, sizeof(int32_t) * (size_t)V);
+    if (final_r) memcpy(final_r, r, rs);
+    if (E_out) memcpy(E_out, E, sizeof(int32_t) * (size_t)n * (size_t)V);
+    if (threads > 1) {
+        quit = 1;
+        pthread_barrier_wait(&bstart);
+        for (int32_t q = 0; q < threads; q++) pthread_join(th[q], NULL);
+        pthread_barrier_destroy(&bstart);
+        pthread_barrier_destroy(&bdone);
+    }
+    free(len); free(r); free(E); free(changed); free(m_delta); free(m_flags); free(C); free(th);
     return 0;
 }

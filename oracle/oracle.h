@@ -91,6 +91,14 @@ int32_t or_search(const or_inst *I, const int32_t *len0, const int32_t *r0, cons
                   or_result *res, int64_t *tr_idx, int32_t *tr_delta, int64_t *tr_cur,
                   int64_t *tr_best, int32_t *tr_cls, uint64_t *tr_digest, int32_t *E_out);
 
+/* The same search (NS / TS + kick) driven over `threads` contiguous index chunks,
+ * optionally keeping unchanged moves' values between iterations (memo); no
+ * digests.  Identical results to or_search (see oracle.c). */
+int32_t or_search_par(const or_inst *I, const int32_t *len0, const int32_t *r0, const or_params *prm,
+                      int32_t threads, int32_t memo, int32_t *best_len, int32_t *best_r, int32_t *final_len,
+                      int32_t *final_r, or_result *res, int64_t *tr_idx, int32_t *tr_delta, int64_t *tr_cur,
+                      int64_t *tr_best, int32_t *tr_cls, int32_t *E_out);
+
 /* f1: the paper-literal (i, j) sweep of Alg. 2 / Alg. 3 (see oracle.c).  One
  * trace entry per (i, j) step, idx -1 when CurrentMin stayed empty. */
 int32_t or_sweep(const or_inst *I, const int32_t *len0, const int32_t *r0, const or_params *prm,

@@ -12,6 +12,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the CUDA C-ABI library)")
     config.addinivalue_line("markers", "slow: long CPU test")
+    config.addinivalue_line("markers", "fulllength: full-length large-config trace parity (minutes of oracle time)")
 
 
 @pytest.fixture(scope="session")
