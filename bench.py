@@ -134,6 +134,30 @@ def cpu_oracle_leg(inst, cfg, start, runs, iters, threads):
     return sum(done), dt
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def gather_clocks(clocks, world):
+    """Clock records of every rank -> one record (median of the ranks' medians, union of reasons)."""
+    if world == 1:
+        return clocks
+    import torch.distributed as dist
+    allc = [None] * world
+    dist.all_gather_object(allc, clocks)
+    sm = [c["sm_mhz"] for c in allc if c.get("sm_mhz")]
+    mx = [c["sm_max_mhz"] for c in allc if c.get("sm_max_mhz")]
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted({r for c in allc for r in c.get("reasons", [])}),
+            "samples": int(sum(c.get("samples", 0) for c in allc)), "per_rank_sm_mhz": [c.get("sm_mhz") for c in allc]}
+
+
 def valid_moves(inst):
     n, V = inst.n_missions, inst.n_vehicles
     return n * (n + V - 2) + n * (n - 1) // 2
@@ -173,13 +197,15 @@ def run_reference(args):
     else:
         config = {"workload": f"{args.workload}: n={inst.n_missions}, V={inst.n_vehicles}, TS",
                   "valid_moves_per_iter": valid_moves(inst)}
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": config,
             "tabu_iters_per_s": tot_it / tot_t,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{runs} runs x {iters} TS iterations of the C3 instance per step"},
+            "measured": {"runs_per_step": runs, "iters_per_run": iters, "launched_gpus": args.gpus,
+                         "note": "the plain oracle on the host cores (rank 0 only); n_gpus 0: no GPU work"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -242,7 +268,7 @@ def run_gpu(args):
         step()
         ev[k][1].record(stream)
     torch.cuda.synchronize()
-    clocks = sampler.stop()
+    clocks = gather_clocks(sampler.stop(), world)
     if world > 1:
         dist.barrier()
     launches = ctx.kernel_launches - launches0
@@ -276,7 +302,14 @@ def run_gpu(args):
         A.as_batch_run(ctx, h, R, hp, hm, prm, hs, shared_start=True, results=hres)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_iters = int(hres.numpy().view(A.RESULT_DTYPE)["iters_done"].sum())
-    e2e_value = e2e_iters * VM / (float(np.mean(e2e_ms)) / 1e3) * world
+    e2e_t = float(np.mean(e2e_ms))
+    if world > 1:   # whole job: iterations summed over ranks / the slowest rank's wall time
+        tt = torch.tensor([e2e_t, float(e2e_iters)], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        e2e_t, e2e_iters = float(mx[0].item()), int(tt[1].item())
+    e2e_value = e2e_iters * VM / (e2e_t / 1e3)
     h2d = p.nbytes + m.nbytes + seeds_np.nbytes
     d2h = R * 40
 
@@ -299,6 +332,7 @@ def run_gpu(args):
         if "duration_ms" in prof and "shared_wavefronts" in prof:   # 128 B per shared-memory wavefront
             roof["ncu_shared_mem_GBps"] = prof["shared_wavefronts"] * 128 / (prof["duration_ms"] / 1e3) / 1e9
 
+    sharded = None if args.no_sharded else sharded_c5(args, A, ctx, comm, world, rank, dev)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -309,8 +343,11 @@ def run_gpu(args):
         cores = os.cpu_count() or 1
         runs_cpu, iters_cpu = cores * 4, 100
         it_cpu, dt_cpu = cpu_oracle_leg(inst, cfg, start, runs_cpu, iters_cpu, cores)
-        cpu = {"value": it_cpu * VM / dt_cpu, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{runs_cpu} runs x {iters_cpu} TS iterations (seeds 1..{runs_cpu}, kick {cfg.kick}) of the same instance"}
+        it1, dt1 = cpu_oracle_leg(inst, cfg, start, 2, iters_cpu, 1)
+        cpu = {"value": it_cpu * VM / dt_cpu, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+               "single_thread_value": it1 * VM / dt1,
+               "sample": f"{runs_cpu} runs x {iters_cpu} TS iterations (seeds 1..{runs_cpu}, kick {cfg.kick}) of the "
+                         f"same instance on {cores} threads; single thread: 2 runs x {iters_cpu}"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
@@ -320,11 +357,93 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
+            "sharded_c5": sharded,
             "step_ms": step_ms}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def sharded_c5(args, A, ctx, comm, world, rank, dev):
+    """Extra object: C5 (BASELINE configs[4], disaster surge, n=4000, V=100) as ONE instance
+    whose move space is sharded over the N ranks (strong scaling; N=1: the whole-GPU kernel).
+    Per rank one persistent k_grid scores its tile slice and exchanges the 8-byte winner with
+    its peers through NVLink stores into an NCCL symmetric window (bounded wait); if that
+    path fails on any rank, every rank falls back to the NCCL-graph path and the object says so.
+    value = iterations x valid moves / device time (max over ranks); e2e = as_tabu_run with
+    host buffers (start in, result + best schedule out), wall clock, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    cfg, inst = workload("surge")
+    h = A.Instance(inst)
+    ctx.upload(h)
+    p, m, _ = A.as_init_greedy(ctx, h)
+    iters = args.shard_iters
+    prm = A.params(mode=A.AS_MODE_TABU, tenure=cfg.tenure, max_iters=iters)
+    VM = valid_moves(inst)
+    path = "k_grid on 1 GPU" if world == 1 else "fused: k_grid per rank, NVLink key exchange (symmetric window)"
+    err = None
+    ctx.set_option("XR_TIMEOUT_MS", 10000)
+
+    def run(want_best=False):
+        return A.as_tabu_run(ctx, h, p, m, prm, want_best=want_best, comm=comm)
+
+    def agree(ok):
+        if world == 1:
+            return ok
+        t = torch.tensor([0.0 if ok else 1.0], device=dev)
+        dist.all_reduce(t)
+        return t.item() == 0.0
+
+    try:
+        run()
+        ok = True
+    except A.AirschedError as e:   # noqa: PERF203
+        ok, err = False, str(e)
+    if not agree(ok):
+        if world == 1:
+            return {"error": err}
+        ctx.set_option("SHARD_FUSED", 0)
+        path = f"NCCL graphs (ncclAllReduce MIN per iteration); fused path failed: {err}"
+        run()
+    run()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(int(dev.index or 0))
+    sampler.start()
+    sampler.mark()
+    ms, its = [], 0
+    for _ in range(3):
+        r = run()
+        ms.append(ctx.last_kernel_ms)
+        its += r["iters_done"]
+    clocks = gather_clocks(sampler.stop(), world)
+    t = sum(ms) / 1e3
+    t0 = time.perf_counter()
+    r = run(want_best=True)
+    te = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([t, te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t, te = float(tt[0].item()), float(tt[1].item())
+    ctx.set_option("SHARD_FUSED", None)
+    ctx.set_option("XR_TIMEOUT_MS", None)
+    ops = (inst.n_missions * (inst.n_missions + inst.n_vehicles - 2) * OPS_RELOCATE +
+           inst.n_missions * (inst.n_missions - 1) // 2 * OPS_SWAP)
+    f_mhz = clocks.get("sm_mhz") or 1965.0
+    peak = 148 * 128 * f_mhz * 1e6 / 1e9 * world
+    ach = its * ops / t / 1e9
+    return {"workload": f"C5 surge: n={inst.n_missions}, V={inst.n_vehicles}, TS {iters} iters per step, "
+                        f"one instance sharded over {world} GPU(s)", "scaling": "strong", "path": path,
+            "value": its * VM / t, "unit": UNIT, "tabu_iters_per_s": its / t, "ms_per_step": 1e3 * t / 3,
+            "steps": 3, "n_gpus": world, "valid_moves_per_iter": VM, "best_obj": r["best_obj"], "clocks": clocks,
+            "e2e": {"value": r["iters_done"] * VM / te, "unit": UNIT, "h2d_bytes_per_step": int(p.nbytes + m.nbytes),
+                    "d2h_bytes_per_step": int(40 + (inst.n_vehicles + 1 + inst.n_missions) * 4)},
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gop/s", "frac": ach / peak,
+                         "traffic": None,
+                         "peak_basis": f"{world} x 148 SM x 128 INT32 lanes x {f_mhz:.0f} MHz; {OPS_RELOCATE}/{OPS_SWAP} "
+                                       "algorithmic ops per relocate/swap move"}}
 
 
 def run_jobs(args):
@@ -491,11 +610,16 @@ def run_single(args):
         dist.barrier()
     sampler.mark()
     ms, its = [], 0
-    for _ in range(args.steps):
+    t_wall = time.perf_counter()
+    steps = 0
+    # at least `steps` steps; with --min-seconds, more until the timed region lasts that long, so the
+    # clock sampler (200 ms period) sees the kernels of sub-millisecond configs
+    while steps < args.steps or time.perf_counter() - t_wall < args.min_seconds:
         r = fn()
         ms.append(ctx.last_kernel_ms)
         its += r["iters_done"]
-    clocks = sampler.stop()
+        steps += 1
+    clocks = gather_clocks(sampler.stop(), world)
     t = sum(ms) / 1e3
     if world > 1:
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
@@ -505,18 +629,62 @@ def run_single(args):
         dist.destroy_process_group()
         return 0
     VM = valid_moves(inst)
-    line = {"metric": METRIC, "value": its * VM / t, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+    line = {"metric": METRIC, "value": its * VM / t, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": f"{args.workload}: n={inst.n_missions}, V={inst.n_vehicles}, "
                                    f"{'NS' if args.ns else 'TS'} {iters} iters", "valid_moves_per_iter": VM,
                        "parallelism": f"move space sharded over {world} GPUs" if world > 1 else "1 GPU"},
-            "tabu_iters_per_s": its / t, "iters_done_per_step": its / args.steps, "best_obj": r["best_obj"],
+            "tabu_iters_per_s": its / t, "iters_done_per_step": its / steps, "best_obj": r["best_obj"],
             "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(args):
+    """`--gpus N` without a torchrun environment: start N ranks (one per GPU) under
+    torch.distributed.run on this node and return its exit code.  Refuses (exit 2)
+    when fewer than N GPUs are visible (the dry mode needs none)."""
+    if not args.dry and args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} GPU(s) visible", "n_gpus": args.gpus}),
+                  flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Launch-path check without GPUs: every rank joins a gloo group, all-reduces its
+    rank, and rank 0 prints the world it saw (tests/test_bench_contract.py)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([1.0, float(rank)])
+        dist.all_reduce(t)
+        ranks, rank_sum = int(t[0].item()), int(t[1].item())
+        dist.destroy_process_group()
+    else:
+        ranks, rank_sum = 1, 0
+    if rank == 0:
+        print(json.dumps({"dry": True, "n_gpus": args.gpus, "world": world, "ranks_seen": ranks,
+                          "rank_sum": rank_sum}), flush=True)
     return 0
 
 
@@ -533,9 +701,25 @@ def main():
     ap.add_argument("--ref-runs-per-core", type=int, default=2)
     ap.add_argument("--ref-iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the extra sharded-C5 object")
+    ap.add_argument("--shard-iters", type=int, default=200, help="TS iterations per step of the sharded C5 object")
     ap.add_argument("--traffic", type=float, default=None, help="dram bytes/launch from an ncu --set full capture")
     ap.add_argument("--ns", action="store_true", help="single-instance workloads: neighbourhood search")
+    ap.add_argument("--min-seconds", type=float, default=0.0,
+                    help="single-instance workloads: repeat steps until the timed region lasts this long")
+    ap.add_argument("--dry", action="store_true", help="launch-path check on CPU (gloo), no GPU work")
     args = ap.parse_args()
+    launched = "WORLD_SIZE" in os.environ
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if not launched and args.gpus > 1:
+        return relaunch(args)
+    _, world, _ = dist_env()
+    if launched and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}", "n_gpus": args.gpus}), flush=True)
+        return 2
+    if args.dry:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "instances":

@@ -107,6 +107,39 @@ as_status as_schedule_check(const as_instance *inst, const int32_t *route_ptr, c
  * stream); NULL = the legacy default stream. */
 as_status as_ctx_create(int32_t device, void *cuda_stream, as_ctx **out);
 as_status as_ctx_set_stream(as_ctx *ctx, void *cuda_stream);
+
+/* Explicit per-context overrides of the kernel choice and launch shape.  The
+ * library picks every kernel and shape itself; these options exist so that the
+ * test suite can force each code path (and its fallbacks) onto small inputs.
+ * Nothing else changes them -- no environment variable is read.  value
+ * INT64_MIN restores the automatic choice; other values must lie in
+ * [-1, 2^40]; an unknown option returns AS_ERR_INVALID_ARG.  Results never
+ * depend on these options (the parity tests run every path). */
+enum {
+    AS_OPT_SMEM_LIMIT = 0,     /* cap on dynamic shared memory per CTA, bytes */
+    AS_OPT_T_SMEM,             /* 0: per-run kernel keeps the table in global memory */
+    AS_OPT_WINDOW,             /* 0: batched kernel without the window scorers */
+    AS_OPT_BATCH_KERNEL,       /* 1: single runs on the batched kernel; 0: never */
+    AS_OPT_GRID,               /* 1: single runs on the whole-GPU kernel; 0: never */
+    AS_OPT_GRID_MIN,           /* move count from which single runs use the whole-GPU kernel */
+    AS_OPT_ONE_CTA,            /* 0: no one-CTA whole-GPU kernel for small single runs */
+    AS_OPT_GRID_T_GLOBAL,      /* 1: whole-GPU kernel reads the table from global memory */
+    AS_OPT_GRID_E_GLOBAL,      /* 1: whole-GPU kernel keeps the tabu matrix in global memory */
+    AS_OPT_GRID_BLOCKS,        /* CTAs of the whole-GPU kernel */
+    AS_OPT_GRID_G,             /* rows per tile of the whole-GPU kernel */
+    AS_OPT_VERBOSE,            /* 1: print the dispatch decision to stderr */
+    AS_OPT_RPC,                /* runs per CTA of the batched kernel */
+    AS_OPT_THREADS,            /* threads per CTA of the per-run kernel */
+    AS_OPT_SHARDED,            /* 1: single runs on the sharded (global-state) kernels without a comm */
+    AS_OPT_GREEDY_GLOBAL,      /* 1: device Alg. 1 keeps its state in global memory */
+    AS_OPT_SHARD_FUSED,        /* 0: sharded runs with a comm use the NCCL-graph path, not the fused kernel */
+    AS_OPT_SHARD_FUSED_1,      /* 1: the fused kernel also with a one-rank comm */
+    AS_OPT_SHARD_EMULATE,      /* sharded kernels without a comm: emulate this many ranks' slices */
+    AS_OPT_SHARD_K,            /* iterations per CUDA graph of the NCCL-graph path */
+    AS_OPT_XR_TIMEOUT_MS,      /* fused sharded exchange: bound on the wait for a peer (default 30000) */
+    AS_OPT_COUNT
+};
+as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t value);
 void as_ctx_destroy(as_ctx *ctx);
 /* Upload (and cache on ctx) the instance's device copy.  Optional: every call
  * below uploads on first use; call this to keep the upload out of a timed
@@ -192,7 +225,9 @@ typedef struct {
     int32_t reserved;
 } as_run_params;
 
-enum { AS_STOP_MAX_ITERS = 0, AS_STOP_LOCAL_OPT = 1, AS_STOP_NO_MOVE = 2, AS_STOP_INFEASIBLE_START = 3 };
+enum { AS_STOP_MAX_ITERS = 0, AS_STOP_LOCAL_OPT = 1, AS_STOP_NO_MOVE = 2, AS_STOP_INFEASIBLE_START = 3,
+       AS_STOP_COMM_ABORT = 4   /* fused sharded run: a peer's key did not arrive within the exchange
+                                   timeout; the call returns AS_ERR_COMM (the result is partial) */ };
 
 typedef struct {
     int64_t best_obj, final_obj, start_obj;
@@ -230,7 +265,9 @@ as_status as_nbhd_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, const
  * [n_runs][n], trace_out [n_runs][max_iters] (trace_level >= 1).
  * best_run_out (host, nullable): run with the smallest (best_obj, run) over
  * all ranks of comm.  A run whose start is infeasible reports stop_reason
- * AS_STOP_INFEASIBLE_START; the call still succeeds. */
+ * AS_STOP_INFEASIBLE_START; the call still succeeds.  The best-run reduction
+ * packs (best_obj << 32 | global run): AS_ERR_UNSUPPORTED when V x
+ * flight_limit_s >= 2^31, AS_ERR_INVALID_ARG when nranks x n_runs >= 2^32. */
 as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *inst, int32_t n_runs,
                        const int32_t *start_ptr, const int32_t *start_missions, int32_t shared_start,
                        const as_run_params *params, const uint64_t *seeds, as_run_result *results,

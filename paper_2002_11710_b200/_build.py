@@ -39,15 +39,28 @@ def nccl_dir() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc every csrc/*.cu to an object (in parallel), then link libairsched.so."""
     if not force and up_to_date():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     nd = nccl_dir()
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
-           "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nd, "include"), "-o", LIB + ".tmp"] + sources() + \
-          ["-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+              "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nd, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        common.insert(1, "-Xptxas=-v")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        subprocess.check_call(common + ["-c", src, "-o", obj])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [nvcc, ARCH, "-shared", "-o", LIB + ".tmp"] + objs + \
+          ["-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     return LIB

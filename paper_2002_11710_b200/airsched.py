@@ -22,14 +22,19 @@ AS_MODE_NS, AS_MODE_TABU = 0, 1
 AS_FLAG_VALID, AS_FLAG_FEASIBLE, AS_FLAG_TABU, AS_FLAG_ADMISSIBLE, AS_FLAG_BYDEFAULT = 1, 2, 4, 8, 16
 AS_MOVE_INTER_RELOCATE, AS_MOVE_INTRA_RELOCATE, AS_MOVE_INTER_SWAP, AS_MOVE_INTRA_SWAP, AS_MOVE_ALL = 1, 2, 4, 8, 15
 AS_KEY_NONE = 0xFFFFFFFFFFFFFFFF
-AS_STOP_MAX_ITERS, AS_STOP_LOCAL_OPT, AS_STOP_NO_MOVE, AS_STOP_INFEASIBLE_START = 0, 1, 2, 3
+AS_STOP_MAX_ITERS, AS_STOP_LOCAL_OPT, AS_STOP_NO_MOVE, AS_STOP_INFEASIBLE_START, AS_STOP_COMM_ABORT = 0, 1, 2, 3, 4
+# as_ctx_set_option names (include/airsched.h AS_OPT_*), in enum order
+OPTIONS = ["SMEM_LIMIT", "T_SMEM", "WINDOW", "BATCH_KERNEL", "GRID", "GRID_MIN", "ONE_CTA", "GRID_T_GLOBAL",
+           "GRID_E_GLOBAL", "GRID_BLOCKS", "GRID_G", "VERBOSE", "RPC", "THREADS", "SHARDED", "GREEDY_GLOBAL",
+           "SHARD_FUSED", "SHARD_FUSED_1", "SHARD_EMULATE", "SHARD_K", "XR_TIMEOUT_MS"]
+OPT_UNSET = -(1 << 63)
 
 SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "as_valid_moves_per_iter",
            "as_schedule_check", "as_ctx_create", "as_ctx_set_stream", "as_ctx_destroy", "as_instance_upload",
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
            "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
-           "as_init_greedy_batch", "as_batch_run_jobs"]
+           "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option"]
 
 
 class AirschedError(RuntimeError):
@@ -85,6 +90,7 @@ def _load():
         "as_schedule_check": (i32, [vp, vp, vp, vp, vp]),
         "as_ctx_create": (i32, [i32, vp, vp]),
         "as_ctx_set_stream": (i32, [vp, vp]),
+        "as_ctx_set_option": (i32, [vp, i32, i64]),
         "as_ctx_destroy": (None, [vp]),
         "as_instance_upload": (i32, [vp, vp]),
         "as_init_greedy": (i32, [vp, vp, i32, i32, vp, vp, vp]),
@@ -196,6 +202,25 @@ class Ctx:
 
     def set_stream(self, stream):
         _check(lib.as_ctx_set_stream(self.handle, C.c_void_p(stream)))
+
+    def set_option(self, name: str, value):
+        """as_ctx_set_option(AS_OPT_<name>, value); None = back to the automatic choice."""
+        _check(lib.as_ctx_set_option(self.handle, OPTIONS.index(name), OPT_UNSET if value is None else int(value)))
+
+    def options(self, **kw):
+        """Context manager: set options, restore the automatic choice on exit."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def cm():
+            for k, v in kw.items():
+                self.set_option(k, v)
+            try:
+                yield self
+            finally:
+                for k in kw:
+                    self.set_option(k, None)
+        return cm()
 
     def upload(self, inst: Instance):
         _check(lib.as_instance_upload(self.handle, inst.handle))

@@ -251,25 +251,30 @@ struct as_ctx {
     float last_ms = 0.f;
     int32_t batch_runs = -1, batch_n = 0, batch_V = 0;   // last as_batch_run
     int64_t launches = 0;
+    size_t max_smem_hw = 0;                 // the device's opt-in limit (max_smem = min(this, AS_OPT_SMEM_LIMIT))
+    int64_t opt[AS_OPT_COUNT];              // as_ctx_set_option overrides; OPT_UNSET = automatic
+    unsigned long long xr_timeout_ns = 30000000000ull;   // fused sharded exchange: bound on a peer's wait
 };
 
 struct as_comm {
     int nranks = 1, rank = 0, device = 0;
     ncclComm_t nccl = nullptr;
-    // NCCL device API state for the fused sharded kernel (set up on first use, collectively)
-    int dev_state = 0;             // 0 untried, 1 ready, -1 unavailable (LSA team != all ranks, or setup failed)
-    void *xbuf = nullptr;          // symmetric buffer (ncclMemAlloc) holding the [3][nranks] key slots
+    // symmetric window of the fused sharded kernel (set up on first use, collectively)
+    int dev_state = 0;             // 0 untried, 1 ready, -1 unavailable (LSA team != all ranks)
+    void *xbuf = nullptr;          // symmetric buffer (ncclMemAlloc) holding the [3][nranks] {key, tag} slots
     ncclWindow_t win = nullptr;
-    ncclDevComm devc{};
-    ncclDevComm *devc_dev = nullptr;   // device copy
+    unsigned epoch = 0;            // fused runs so far (identical on every rank: the calls are collective)
 };
 
 // Grid-kernel options of a fused sharded run (run_core).
 struct GridXr {
     int nranks, rank;
-    const ncclDevComm *devc;
+    unsigned epoch;
+    unsigned long long timeout_ns;
     ncclWindow_t win;
 };
+
+constexpr int64_t OPT_UNSET = INT64_MIN;
 
 #define NCCL_TRY(expr)                                                                              \
     do {                                                                                            \
@@ -296,13 +301,26 @@ extern "C" as_status as_ctx_create(int32_t device, void *stream, as_ctx **out) {
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10) return fail(AS_ERR_DEVICE, "this build targets sm_100a (B200); device is sm_%d%d", prop.major, prop.minor);
     c->n_sm = prop.multiProcessorCount;
-    c->max_smem = prop.sharedMemPerBlockOptin;
-    if (getenv("AIRSCHED_SMEM_LIMIT")) c->max_smem = std::min<size_t>(c->max_smem, (size_t)atol(getenv("AIRSCHED_SMEM_LIMIT")));   // test knob
+    c->max_smem = c->max_smem_hw = prop.sharedMemPerBlockOptin;
+    for (int k = 0; k < AS_OPT_COUNT; k++) c->opt[k] = OPT_UNSET;
     CUDA_TRY(cudaEventCreate(&c->ev0));
     CUDA_TRY(cudaEventCreate(&c->ev1));
     CUDA_TRY(cudaEventCreateWithFlags(&c->evj, cudaEventDisableTiming));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
     *out = c.release();
+    return AS_OK;
+}
+
+extern "C" as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t value) {
+    if (!ctx) return fail(AS_ERR_INVALID_ARG, "null ctx");
+    if (option < 0 || option >= AS_OPT_COUNT) return fail(AS_ERR_INVALID_ARG, "unknown option %d", option);
+    if (value != OPT_UNSET && (value < -1 || value > (int64_t)1 << 40))
+        return fail(AS_ERR_INVALID_ARG, "option %d: value %lld out of range", option, (long long)value);
+    ctx->opt[option] = value;
+    if (option == AS_OPT_SMEM_LIMIT)
+        ctx->max_smem = value == OPT_UNSET ? ctx->max_smem_hw : std::min<size_t>(ctx->max_smem_hw, (size_t)std::max<int64_t>(0, value));
+    if (option == AS_OPT_XR_TIMEOUT_MS)
+        ctx->xr_timeout_ns = value == OPT_UNSET ? 30000000000ull : (unsigned long long)std::max<int64_t>(1, value) * 1000000ull;
     return AS_OK;
 }
 
@@ -606,10 +624,16 @@ static as_status pick_layout(as_ctx *ctx, const as_instance *I, bool tabu, int *
     return fail(AS_ERR_UNSUPPORTED, "instance too large for the per-CTA persistent kernel (n=%d, V=%d)", n, V);
 }
 
-static int env_int(const char *name, int dflt) {
-    const char *s = getenv(name);
-    return s ? atoi(s) : dflt;
+// An as_ctx_set_option override, or the automatic choice dflt.
+static int opt_int(const as_ctx *ctx, int option, int dflt) {
+    const int64_t v = ctx->opt[option];
+    return v == OPT_UNSET ? dflt : (int)v;
 }
+
+// The window scorers' general-leg form blocks a row whose removal leaves route a over the
+// flight limit by adding NEG (-2^29) to P - F_b (window.cuh win_reloc_record): exact only while
+// P < 2^28 (validation allows up to 2^30 - 1), so larger limits take the FAST scorers.
+#define WIN_P_OK (I->P < (1 << 28))
 
 static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, const int32_t *start_ptr,
                           const int32_t *start_ms, int32_t shared_start, const as_run_params *P,
@@ -630,7 +654,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     size_t smem;
     const bool kfit = pick_layout(ctx, I, tabu, &T_smem, &E_smem, &smem) == AS_OK;
     if (!kfit) { T_smem = 0; E_smem = 0; smem = 0; }
-    const int force_T = env_int("AIRSCHED_T_SMEM", -1);
+    const int force_T = opt_int(ctx, AS_OPT_T_SMEM, -1);
     if (force_T == 0 && T_smem) {
         T_smem = 0;
         smem = search_smem_bytes(n, V, I->NL, I->NC, false, E_smem, I->no_wait != 0);
@@ -691,7 +715,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     // window scorers (window.cuh) for the batched kernel: every move kind, positive service legs, uint16 table,
     // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
     bool win = (P->move_mask & 15u) == 15u && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
-               (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
+               (!tabu || P->tenure <= WIN_MAX_TENURE) && opt_int(ctx, AS_OPT_WINDOW, 1) == 1 &&
+               WIN_P_OK;
     size_t sh_b = 0, run_b = 0;
     batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure, I->tsym != 0);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
@@ -711,7 +736,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     // the no-wait variant (f3) runs on k_search
     const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !I->no_wait;
     if (P->sweep && I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sweep mode (f1) is not built for the no-wait variant");
-    const int want_batch = env_int("AIRSCHED_BATCH_KERNEL", -1);
+    const int want_batch = opt_int(ctx, AS_OPT_BATCH_KERNEL, -1);
     bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single) || P->sweep);
     if (P->sweep && !use_batch)
         return fail(AS_ERR_UNSUPPORTED, "the sweep mode runs on the batched kernel (compact layout required)");
@@ -724,22 +749,22 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     if (xr && !(single && compact_ok && !P->sweep))
         return fail(AS_ERR_UNSUPPORTED, "fused sharded run needs the compact layout");
     if (single && compact_ok && !P->sweep) {
-        const int want_grid = xr ? 1 : env_int("AIRSCHED_GRID", -1);
+        const int want_grid = xr ? 1 : opt_int(ctx, AS_OPT_GRID, -1);
         const bool kfits = kfit;
         // CTAs: one per single-row tile up to the SM count (an iteration's floor is one tile's
         // latency + the grid barrier + the apply; an SM scoring many tiles at once is issue-bound,
         // DESIGN.md §7); ONE CTA (no grid barrier) when one CTA's warps take every tile
         const int64_t tiles1 = (int64_t)((S + 127) / 128 + (n > 1 ? (n - 1 + 63) / 64 : 0)) * n + (n + 31) / 32;
         const int need_blocks = (int)std::min<int64_t>(ctx->n_sm, tiles1);   // tiles spread one per CTA first
-        const bool big = N >= env_int("AIRSCHED_GRID_MIN", 100000) || tiles1 > GRID_WARPS;
+        const bool big = N >= opt_int(ctx, AS_OPT_GRID_MIN, 100000) || tiles1 > GRID_WARPS;
         // small single runs: the same kernel on ONE CTA (no grid barrier)
-        const bool one_cta = !big && kfits && want_grid != 1 && env_int("AIRSCHED_ONE_CTA", 1) == 1;
+        const bool one_cta = !big && kfits && want_grid != 1 && opt_int(ctx, AS_OPT_ONE_CTA, 1) == 1;
         if (want_grid == 1 || one_cta || (want_grid == -1 && (big || !kfits))) {
             auto &D = ctx->insts[I];
             const int tb = D.tpad_bytes;
             struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
-            const bool t_global = env_int("AIRSCHED_GRID_T_GLOBAL", 0) == 1;   // test knobs
-            const bool e_global = env_int("AIRSCHED_GRID_E_GLOBAL", 0) == 1;
+            const bool t_global = opt_int(ctx, AS_OPT_GRID_T_GLOBAL, 0) == 1;   // test options
+            const bool e_global = opt_int(ctx, AS_OPT_GRID_E_GLOBAL, 0) == 1;
             for (auto o : gopts) {
                 if ((t_global && o.t) || (e_global && o.e)) continue;
                 size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu, tabu);
@@ -756,14 +781,14 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 int coop = 0;
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
                 use_grid = coop != 0;
-                grid_blocks = one_cta ? 1 : std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS",
+                grid_blocks = one_cta ? 1 : std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS,
                                                                                       want_grid == 1 ? ctx->n_sm : need_blocks)));
-                if (xr) grid_blocks = std::max(1, std::min(ctx->n_sm, env_int("AIRSCHED_GRID_BLOCKS", ctx->n_sm)));
+                if (xr) grid_blocks = std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS, ctx->n_sm)));
                 GA.Tglobal = D.Tpad;
                 void *p;
-                if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
-                GA.gkey = (unsigned long long *)p;
-                CUDA_TRY(cudaMemsetAsync(p, 0xFF, 3 * 8, ctx->stream));
+                if ((st = scratch(ctx, "g_ll", (size_t)(2 * 2 * grid_blocks + 4) * 8, &p)) != AS_OK) return st;
+                GA.ll = (unsigned long long *)p;          // zeroed by the kernel (own slots) at launch
+                GA.llb = GA.ll + 2 * 2 * grid_blocks;
                 if ((st = scratch(ctx, "g_bs", (size_t)S * 4, &p)) != AS_OK) return st;
                 GA.BS = (int32_t *)p;
                 if (tabu && !GA.E_smem) {
@@ -787,7 +812,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     const double cost = (double)rounds * g + 0.3 * (double)rounds;
                     if (cost <= best_cost) { best_cost = cost; GA.G = g; }
                 }
-                GA.G = std::max(1, env_int("AIRSCHED_GRID_G", GA.G));
+                GA.G = std::max(1, opt_int(ctx, AS_OPT_GRID_G, GA.G));
                 GA.tlo = 0;
                 GA.thi = grid_tile_count(n, V, GA.G);
                 if (xr) {   // this rank's slice of the tile list (same weighted plan as the sharded kernels)
@@ -795,16 +820,15 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     GA.xr = 1;
                     GA.xr_nranks = xr->nranks;
                     GA.xr_rank = xr->rank;
-                    GA.xr_comm = xr->devc;
+                    GA.xr_epoch = xr->epoch;
+                    GA.xr_timeout_ns = xr->timeout_ns;
                     GA.xr_win = xr->win;
-                    if ((st = scratch(ctx, "g_key2", 3 * 8, &p)) != AS_OK) return st;
-                    GA.gkey2 = (unsigned long long *)p;
                 }
             }
         }
     }
     if (xr && !use_grid) return fail(AS_ERR_UNSUPPORTED, "fused sharded run: the state does not fit the grid kernel");
-    if (env_int("AIRSCHED_VERBOSE", 0))
+    if (opt_int(ctx, AS_OPT_VERBOSE, 0))
         fprintf(stderr, "[airsched] n=%d V=%d runs=%d single=%d -> %s (blocks %d, G %d, T_smem %d, E_smem %d, smem %zu)\n",
                 n, V, n_runs, (int)single, use_grid ? (xr ? "k_grid fused-sharded" : grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
                 use_batch ? (win ? "k_batch/window" : "k_batch") : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
@@ -817,7 +841,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
         ctx->launches--;   // counted once below
     } else if (use_batch) {
         int rpc = (int)std::min<int64_t>(28, std::min<int64_t>(rpc_fit, (n_runs + ctx->n_sm - 1) / ctx->n_sm));
-        rpc = std::max(1, env_int("AIRSCHED_RPC", rpc));
+        rpc = std::max(1, opt_int(ctx, AS_OPT_RPC, rpc));
         rpc = std::min(rpc, std::min(28, rpc_fit));
         size_t smem_b = sh_b + (size_t)rpc * run_b;
         if (win && tabu) {   // the window path keeps each run's tabu matrix in global memory
@@ -836,7 +860,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
         } else {
             threads = 256;
         }
-        threads = env_int("AIRSCHED_THREADS", threads);
+        threads = opt_int(ctx, AS_OPT_THREADS, threads);
         CUDA_TRY(launch_search(A, tabu ? 1 : 0, n_runs, threads, smem, ctx->stream));
     }
     ctx->launches++;
@@ -861,7 +885,7 @@ extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *
     int64_t obj;
     as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
     if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
-    if ((comm || env_int("AIRSCHED_SHARDED", 0) == 1) && !P->sweep) {
+    if ((comm || opt_int(ctx, AS_OPT_SHARDED, 0) == 1) && !P->sweep) {
         if (I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sharded path is not built for the no-wait variant");
         if (digest && P->trace_level >= 2) return fail(AS_ERR_UNSUPPORTED, "tabu digests are not produced by the sharded path");
         return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
@@ -894,6 +918,12 @@ extern "C" as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance 
                                   int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int64_t *best_run_out) {
     if (!ctx || !I || !P) return fail(AS_ERR_INVALID_ARG, "null argument");
     if (!start_ptr) return fail(AS_ERR_INVALID_ARG, "null start");
+    // the best-run key packs (best objective << 32 | global run): objective <= V * P and the
+    // global run index must each fit 32 bits
+    if ((int64_t)I->V * I->P >= (1ll << 31))
+        return fail(AS_ERR_UNSUPPORTED, "V * flight_limit_s >= 2^31: the best-run key cannot hold the objective");
+    if ((int64_t)(comm ? comm->nranks : 1) * n_runs >= (1ll << 32))
+        return fail(AS_ERR_INVALID_ARG, "nranks * n_runs >= 2^32");
     // results are needed on the device for the best-run reduction
     as_run_result *res = results;
     if (!res || !is_device_ptr(res)) {
@@ -948,11 +978,14 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
         if (I->NL > 65535 || I->n + I->V > 65535 || I->V > 32767 || I->NC > 2 || I->no_wait)
             return fail(AS_ERR_UNSUPPORTED, "job %d: the multi-instance batch needs the compact layout (NL, n+V < 65536, <= 2 classes, waiting model)", j);
         if (I->maxT > 65535) tbytes = 4;
+        if ((int64_t)I->V * I->P >= (1ll << 31))   // best-run key: objective << 32 (see as_batch_run)
+            return fail(AS_ERR_UNSUPPORTED, "job %d: V * flight_limit_s >= 2^31", j);
         total += jobs[j].n_runs;
         bp_total += (int64_t)jobs[j].n_runs * (I->V + 1);
         bm_total += (int64_t)jobs[j].n_runs * I->n;
     }
-    if (total >= (1ll << 31)) return fail(AS_ERR_INVALID_ARG, "too many runs");
+    if (total >= (1ll << 31) || (int64_t)(comm ? comm->nranks : 1) * total >= (1ll << 32))
+        return fail(AS_ERR_INVALID_ARG, "too many runs");
     const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
     // per-job device instance, layout, runs per CTA, packed start
     std::vector<BatchJob> J(n_jobs);
@@ -963,11 +996,12 @@ extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_job
     std::vector<std::pair<int64_t, int64_t>> poff(n_jobs, {-1, -1});
     // window scorers (window.cuh) for the FAST launch when every FAST job qualifies (V <= 32)
     bool win = ((P->sweep ? 1u : P->move_mask) & 15u) == 15u && !P->sweep && tbytes == 2 &&
-               (!tabu || P->tenure <= WIN_MAX_TENURE) && env_int("AIRSCHED_WIN", 1) == 1;
+               (!tabu || P->tenure <= WIN_MAX_TENURE) && opt_int(ctx, AS_OPT_WINDOW, 1) == 1 &&
+               true;
     for (int j = 0; j < n_jobs && win; j++) {
         const DevInst *D;
         if ((st = get_dev_inst(ctx, jobs[j].inst, &D)) != AS_OK) return st;
-        if (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535) win = false;
+        if (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535 || jobs[j].inst->P >= (1 << 28)) win = false;
     }
     int64_t run0 = 0, bp0 = 0, bm0 = 0, e0 = 0;
     for (int j = 0; j < n_jobs; j++) {
@@ -1178,7 +1212,7 @@ extern "C" as_status as_init_greedy_batch(as_ctx *ctx, const as_instance *I, int
     const size_t lim = ctx->max_smem;
     int warps = 0;
     bool T_smem = false, state_smem = false;
-    if (env_int("AIRSCHED_GREEDY_GLOBAL", 0) == 1) warps = -1;   // test knob: state in global memory
+    if (opt_int(ctx, AS_OPT_GREEDY_GLOBAL, 0) == 1) warps = -1;   // test option: state in global memory
     for (int w = 8; w >= 1 && !warps; w /= 2)
         if (greedy_smem_bytes(*D, w, true, true) <= lim) { warps = w; T_smem = state_smem = true; }
     for (int w = 8; w >= 1 && !warps; w /= 2)
@@ -1244,11 +1278,7 @@ extern "C" void as_comm_destroy(as_comm *comm) {
     if (!comm) return;
     if (comm->nccl) {
         cudaSetDevice(comm->device);
-        if (comm->dev_state == 1) {
-            ncclDevCommDestroy(comm->nccl, &comm->devc);
-            ncclCommWindowDeregister(comm->nccl, comm->win);
-            cudaFree(comm->devc_dev);
-        }
+        if (comm->dev_state == 1) ncclCommWindowDeregister(comm->nccl, comm->win);
         if (comm->xbuf) ncclMemFree(comm->xbuf);
         ncclCommDestroy(comm->nccl);
     }
@@ -1287,15 +1317,20 @@ static as_status comm_device_setup(as_comm *comm) {
     if (comm->dev_state) return AS_OK;
     comm->dev_state = -1;
     if (ncclTeamLsa(comm->nccl).nRanks != comm->nranks) return AS_OK;   // not every peer load/store reachable
-    NCCL_TRY(ncclMemAlloc(&comm->xbuf, 4096));
-    NCCL_TRY(ncclCommWindowRegister(comm->nccl, comm->xbuf, 4096, &comm->win, NCCL_WIN_COLL_SYMMETRIC));
-    CUDA_TRY(cudaMemset(comm->xbuf, 0, 4096));
-    ncclDevCommRequirements reqs;
-    memset(&reqs, 0, sizeof(reqs));
-    reqs.lsaBarrierCount = 1;
-    NCCL_TRY(ncclDevCommCreate(comm->nccl, &reqs, &comm->devc));
-    CUDA_TRY(cudaMalloc(&comm->devc_dev, sizeof(ncclDevComm)));
-    CUDA_TRY(cudaMemcpy(comm->devc_dev, &comm->devc, sizeof(ncclDevComm), cudaMemcpyHostToDevice));
+    const size_t bytes = std::max<size_t>(4096, (size_t)3 * comm->nranks * 16);
+    NCCL_TRY(ncclMemAlloc(&comm->xbuf, bytes));
+    CUDA_TRY(cudaMemset(comm->xbuf, 0, bytes));   // tags 0: no epoch >= 1 matches them
+    CUDA_TRY(cudaDeviceSynchronize());
+    NCCL_TRY(ncclCommWindowRegister(comm->nccl, comm->xbuf, bytes, &comm->win, NCCL_WIN_COLL_SYMMETRIC));
+    // every rank's window is zeroed before any rank's first fused kernel can store into it:
+    // a one-word all-reduce as a barrier (the memsets above completed before it on each rank)
+    int *bar = nullptr;
+    CUDA_TRY(cudaMalloc(&bar, sizeof(int)));
+    ncclResult_t r = ncclAllReduce(bar, bar, 1, ncclInt32, ncclSum, comm->nccl, 0);
+    cudaError_t e = cudaStreamSynchronize(0);
+    cudaFree(bar);
+    if (r != ncclSuccess) return fail(AS_ERR_COMM, "setup barrier: %s", ncclGetErrorString(r));
+    if (e != cudaSuccess) return fail(AS_ERR_DEVICE, "setup barrier: %s", cudaGetErrorString(e));
     comm->dev_state = 1;
     return AS_OK;
 }
@@ -1305,17 +1340,20 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
                              int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out) {
     as_status st = set_device(ctx);
     if (st != AS_OK) return st;
-    // Fused path (default with a communicator; AIRSCHED_SHARD_FUSED=0 disables it): one persistent
+    // Fused path (default with a communicator; AS_OPT_SHARD_FUSED = 0 disables it): one persistent
     // k_grid per rank scores the rank's tile slice and exchanges the 8-byte winner with its peers
     // through NVLink stores into a symmetric window + an LSA barrier inside the kernel, instead
     // of [eval kernel, ncclAllReduce, apply kernel] per iteration.  Needs every peer in the LSA
     // team and the state in shared memory; otherwise the NCCL path below runs.
-    if (comm && env_int("AIRSCHED_SHARD_FUSED", 1) == 1 && (comm->nranks > 1 || env_int("AIRSCHED_SHARD_FUSED_1", 0) == 1)) {
+    if (comm && opt_int(ctx, AS_OPT_SHARD_FUSED, 1) == 1 && (comm->nranks > 1 || opt_int(ctx, AS_OPT_SHARD_FUSED_1, 0) == 1)) {
         if ((st = comm_device_setup(comm)) != AS_OK) return st;
         if (comm->dev_state == 1) {
-            GridXr xr{comm->nranks, comm->rank, comm->devc_dev, comm->win};
+            GridXr xr{comm->nranks, comm->rank, ++comm->epoch, ctx->xr_timeout_ns, comm->win};
             st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, nullptr,
                           tabu_out, true, &xr);
+            if (st == AS_OK && result->stop_reason == AS_STOP_COMM_ABORT)
+                return fail(AS_ERR_COMM, "fused sharded run: a peer's key did not arrive within %.1f s (rank %d of %d)",
+                            ctx->xr_timeout_ns / 1e9, comm->rank, comm->nranks);
             if (st != AS_ERR_UNSUPPORTED) return st;
         }
     }
@@ -1385,7 +1423,7 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
     shard_plan(n, V, G, nranks, rank, &tlo, &thi, nullptr, nullptr);
     // Test mode (no communicator): emulate R ranks on one GPU by scoring the R
     // slices one after another into the same key before the apply.
-    const int emulate = comm ? 1 : std::max(1, env_int("AIRSCHED_SHARD_EMULATE", 1));
+    const int emulate = comm ? 1 : std::max(1, opt_int(ctx, AS_OPT_SHARD_EMULATE, 1));
     std::vector<std::pair<int, int>> slices;
     if (emulate > 1) {
         for (int r = 0; r < emulate; r++) {
@@ -1403,7 +1441,7 @@ static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, c
     CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evj, 0));
     CUDA_TRY(cudaEventRecord(ctx->ev0, cs));
     if (P->max_iters > 0) {
-        const int K = std::max(1, std::min(P->max_iters, env_int("AIRSCHED_SHARD_K", 64)));
+        const int K = std::max(1, std::min(P->max_iters, opt_int(ctx, AS_OPT_SHARD_K, 64)));
         cudaGraph_t graph;
         cudaGraphExec_t exec;
         CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));

@@ -46,7 +46,10 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.VC = o; o = al16(o + V * 4);
     L.CH = o; o = al16(o + NC);
     L.TT = o; o = al16(o + (win && !tsym ? NC * NL * NLp * tbytes : 0));   // transposed table (window scorers)
-    L.TD = o; o = al16(o + (win ? NC * td_layer(n + V, NL) * 2 : 0));         // node costs d_c(x, t) (window scorers)
+    // node costs d_c(x, t) (window scorers); 128 B of guard before them: the lowest swap chunk's
+    // lanes with m2 < 0 (masked) form addresses up to 126 B before a TD row (window.cuh ya_base)
+    if (win) o = al16(o + 128);
+    L.TD = o; o = al16(o + (win ? NC * td_layer(n + V, NL) * 2 : 0));
     L.TDT = o; o = al16(o + (win ? NC * n * padded_stride(NL, 2) * 2 : 0)); // the same, [c][m][x]
     L.shared_bytes = o;
     int r = 0;

@@ -64,13 +64,14 @@ struct CompactRV {
     ET *E;
 };
 
+// Warp minimum of a 64-bit key with two 32-bit REDUX.MIN (sm_80+): the minimum high word, then
+// the minimum low word among the lanes holding it -- two instructions instead of five 64-bit
+// shuffle rounds (the key reductions sit on the per-iteration critical path of k_grid / k_batch).
 __device__ __forceinline__ uint64_t wmin(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        uint64_t u = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        v = u < v ? u : v;
-    }
-    return v;
+    const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+    const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, hi);
+    const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? lo : 0xFFFFFFFFu);
+    return ((uint64_t)mh << 32) | ml;
 }
 
 template <class T>

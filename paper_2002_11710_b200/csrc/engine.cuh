@@ -24,6 +24,9 @@
 namespace airsched {
 
 constexpr uint64_t KEY_NONE = 0xFFFFFFFFFFFFFFFFull;
+// Never a selection key (its delta field would be 2^30 - 1; |delta| < 2^29, reading #32):
+// the fused sharded exchange returns it when a peer's key did not arrive in time.
+constexpr uint64_t KEY_ABORT = 0x7FFFFFFFFFFFFFFFull;
 constexpr int32_t DELTA_BIAS = 1 << 30;
 
 // Instance, device-resident (uploaded once per ctx).

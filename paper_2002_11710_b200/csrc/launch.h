@@ -76,15 +76,17 @@ struct GridArgs {
     int32_t *Eglobal;              // [n][V] tabu matrix when !E_smem
     int32_t *Etglobal;             // [V][n] its transpose (identical values), when !E_smem
     int32_t *BS;                   // [S] best-schedule successor array
-    unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
+    unsigned long long *ll;        // [2][gridDim][2] LL key slots (grid.cu ll_publish / ll_gather_min)
+    unsigned long long *llb;       // [2][2] LL broadcast slot of the all-ranks winner (fused sharded run)
     int G;                         // rows per tile
     int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
     // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
-    // into every peer's symmetric window slot over NVLink and meets the peers at an LSA barrier
+    // and a tag into every peer's symmetric window slot over NVLink and waits (bounded) for the
+    // peers' tags of this iteration in its own window (grid.cu rank_exchange)
     int xr, xr_nranks, xr_rank;
-    const ncclDevComm *xr_comm;    // device copy of the NCCL device communicator
-    ncclWindow_t xr_win;           // symmetric window: [3][nranks] u64 slots
-    unsigned long long *gkey2;     // [3] the all-ranks winner per slot
+    unsigned xr_epoch;             // per-call run epoch (same on every rank), high half of the tags
+    unsigned long long xr_timeout_ns;   // bound on the wait for the peers' keys
+    ncclWindow_t xr_win;           // symmetric window: [3][nranks] {key, tag} u64 pairs
 };
 
 // Sharded single-instance run (shard.cu): replica state in global memory.

@@ -20,3 +20,18 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture
+def ctxopt(ctx):
+    """Set as_ctx_set_option overrides on the module's context for one test
+    (e.g. ctxopt(GRID=1)); the automatic choice is restored afterwards."""
+    names = []
+
+    def set_(**kw):
+        for k, v in kw.items():
+            ctx.set_option(k, v)
+            names.append(k)
+    yield set_
+    for k in names:
+        ctx.set_option(k, None)

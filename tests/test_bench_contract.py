@@ -38,3 +38,42 @@ def test_reference_arm_config_is_gpu_arms(ref_line):
     _, inst = bench.workload("batched")
     assert ref_line["config"] == bench.batched_config(cfg, inst, cfg.n_runs, cfg.max_iters, 1)
     assert ref_line["config"]["valid_moves_per_iter"] == bench.valid_moves(inst)
+
+
+def _run(args, env=None, timeout=300):
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    return subprocess.run([sys.executable, "bench.py"] + args, cwd=ROOT, capture_output=True, text=True,
+                          timeout=timeout, env=e)
+
+
+def test_gpus_flag_spawns_ranks():
+    """`--gpus 2` outside torchrun re-launches bench.py as 2 ranks (torch.distributed.run,
+    127.0.0.1); the dry mode joins a gloo group and rank 0 reports what it saw."""
+    r = _run(["--gpus", "2", "--dry"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    L = lines[0]
+    assert L["dry"] and L["n_gpus"] == 2 and L["world"] == 2 and L["ranks_seen"] == 2 and L["rank_sum"] == 1
+
+
+def test_gpus_flag_refuses_missing_gpus():
+    """More GPUs asked for than visible: one error line, exit code 2, no silent 1-GPU run."""
+    import torch
+    if torch.cuda.device_count() >= 3:
+        pytest.skip("this host has the GPUs")
+    r = _run(["--gpus", "3", "--steps", "1", "--warmup", "1"])
+    assert r.returncode == 2
+    assert "error" in json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_world_size_must_match_gpus():
+    r = _run(["--gpus", "2", "--dry"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "error" in json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_reference_arm_reports_no_gpus(ref_line):
+    assert ref_line["n_gpus"] == 0 and ref_line["cpu_baseline"]["cpu_model"]

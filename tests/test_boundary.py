@@ -119,3 +119,20 @@ def test_ctx_without_gpu_fails_loudly(A):
     with pytest.raises(A.AirschedError) as e:
         A.Ctx(0, 0)
     assert e.value.status == A.AS_ERR_DEVICE
+
+
+def test_option_enum_matches_binding(A):
+    """as_ctx_set_option: the binding's option names are the header's AS_OPT_* enum in order."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "airsched.h")).read()
+    block = hdr[hdr.index("AS_OPT_SMEM_LIMIT = 0"):hdr.index("AS_OPT_COUNT")]
+    names = re.findall(r"AS_OPT_([A-Z_0-9]+)", block)
+    assert names == A.OPTIONS
+
+
+def test_library_reads_no_environment():
+    """Dispatch is explicit (as_ctx_set_option): the library's own sources read no
+    environment variable (the statically linked CUDA runtime has its own)."""
+    import glob
+    for f in glob.glob(os.path.join(ROOT, "paper_2002_11710_b200", "csrc", "*")):
+        assert "getenv" not in open(f).read(), f

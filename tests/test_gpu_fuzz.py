@@ -92,20 +92,19 @@ def compare_run(A, ctx, O, h, p, m, mode, tenure, iters, seed=0, kick=0, digest=
 # the batched kernel for a single run, the sharded kernels with 2 emulated ranks
 PATHS = {
     "default": {},
-    "k_search": {"AIRSCHED_GRID": "0", "AIRSCHED_ONE_CTA": "0"},
-    "k_grid_1cta": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_BLOCKS": "1"},
-    "k_grid_all": {"AIRSCHED_GRID": "1"},
-    "k_grid_tglobal": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_T_GLOBAL": "1", "AIRSCHED_GRID_G": "2"},
-    "k_grid_teglobal": {"AIRSCHED_GRID": "1", "AIRSCHED_GRID_T_GLOBAL": "1", "AIRSCHED_GRID_E_GLOBAL": "1"},
-    "k_batch": {"AIRSCHED_BATCH_KERNEL": "1"},
-    "sharded2": {"AIRSCHED_SHARDED": "1", "AIRSCHED_SHARD_EMULATE": "2", "AIRSCHED_SHARD_K": "3"},
+    "k_search": {"GRID": 0, "ONE_CTA": 0},
+    "k_grid_1cta": {"GRID": 1, "GRID_BLOCKS": 1},
+    "k_grid_all": {"GRID": 1},
+    "k_grid_tglobal": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_G": 2},
+    "k_grid_teglobal": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1},
+    "k_batch": {"BATCH_KERNEL": 1},
+    "sharded2": {"SHARDED": 1, "SHARD_EMULATE": 2, "SHARD_K": 3},
 }
 
 
 @pytest.mark.parametrize("path", list(PATHS))
-def test_fuzz_runs(A, ctx, oracle_mod, path, monkeypatch):
-    for k, v in PATHS[path].items():
-        monkeypatch.setenv(k, v)
+def test_fuzz_runs(A, ctx, oracle_mod, path, ctxopt):
+    ctxopt(**PATHS[path])
     rng = np.random.default_rng(20021171 + list(PATHS).index(path) + SEED)
     done = 0
     for trial in range(120 * SCALE):

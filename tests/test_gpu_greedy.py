@@ -90,8 +90,8 @@ def test_greedy_large(A, ctx, oracle_mod, cfg):
     assert st == 0 and routes_of(gp, gm) == routes_of(p, m) and gn == nr
 
 
-def test_greedy_state_in_global(A, ctx, oracle_mod, monkeypatch):
-    monkeypatch.setenv("AIRSCHED_GREEDY_GLOBAL", "1")
+def test_greedy_state_in_global(A, ctx, oracle_mod, monkeypatch, ctxopt):
+    ctxopt(GREEDY_GLOBAL=1)
     for cfg in ("ontario", "batched"):
         inst = instgen.generate(cfg)
         O = oracle_mod.Oracle(inst)

@@ -189,7 +189,7 @@ def test_nowait_greedy_parity(A, ctx, oracle_mod):
     assert n_ok >= 6 and n_fail >= 1
 
 
-def test_nowait_unsupported_paths(A, ctx, oracle_mod, monkeypatch):
+def test_nowait_unsupported_paths(A, ctx, oracle_mod, monkeypatch, ctxopt):
     inst = nowait("tiny")
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -197,7 +197,7 @@ def test_nowait_unsupported_paths(A, ctx, oracle_mod, monkeypatch):
     with pytest.raises(A.AirschedError) as e:
         A.as_tabu_run(ctx, h, p, m, A.params(mode=1, tenure=3, max_iters=10, sweep=1))
     assert e.value.status == A.AS_ERR_UNSUPPORTED
-    monkeypatch.setenv("AIRSCHED_SHARDED", "1")
+    ctxopt(SHARDED=1)
     with pytest.raises(A.AirschedError) as e:
         A.as_tabu_run(ctx, h, p, m, A.params(mode=1, tenure=3, max_iters=10))
     assert e.value.status == A.AS_ERR_UNSUPPORTED

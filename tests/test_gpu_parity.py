@@ -367,10 +367,10 @@ def test_batch_per_run_starts(A, ctx, oracle_mod):
 
 
 @pytest.mark.parametrize("cfg,iters", [("tiny", 200), ("ontario", 400), ("batched", 300)])
-def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch):
+def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch, ctxopt):
     """The cooperative whole-GPU kernel (k_grid) forced onto small instances:
     many tiles per row group, most warps idle -- the trace must not change."""
-    monkeypatch.setenv("AIRSCHED_GRID", "1")
+    ctxopt(GRID=1)
     inst = instgen.generate(cfg)
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -378,11 +378,11 @@ def test_grid_kernel_forced_small(A, ctx, oracle_mod, cfg, iters, monkeypatch):
     c = instgen.CONFIGS[cfg]
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=3, kick=5)
     _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
-    monkeypatch.setenv("AIRSCHED_GRID_G", "3")
+    ctxopt(GRID_G=3)
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
-    monkeypatch.setenv("AIRSCHED_GRID_T_GLOBAL", "1")   # table in global memory: row-local reads
+    ctxopt(GRID_T_GLOBAL=1)   # table in global memory: row-local reads
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
-    monkeypatch.setenv("AIRSCHED_GRID_E_GLOBAL", "1")   # tabu matrix (and its transpose) in global memory
+    ctxopt(GRID_E_GLOBAL=1)   # tabu matrix (and its transpose) in global memory
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=5, kick=4)
 
 
@@ -400,14 +400,14 @@ def test_surge_run_parity_prefix(A, ctx, oracle_mod):
 # ------------------------------------------------- sharded single instance (C5) --
 @pytest.mark.parametrize("cfg,iters,emulate", [("tiny", 200, 1), ("ontario", 400, 3), ("large", 30, 8),
                                                ("surge", 2, 8)])
-def test_sharded_path_parity(A, ctx, oracle_mod, cfg, iters, emulate, monkeypatch):
+def test_sharded_path_parity(A, ctx, oracle_mod, cfg, iters, emulate, monkeypatch, ctxopt):
     """The sharded path's kernels (replica in global memory, per-iteration
     eval -> MIN -> apply in a CUDA graph).  With `emulate` > 1 the slices of
     that many ranks are scored one after another on this GPU (no kernel waits
     on another) -- the move sequence must equal the oracle's."""
-    monkeypatch.setenv("AIRSCHED_SHARDED", "1")
-    monkeypatch.setenv("AIRSCHED_SHARD_EMULATE", str(emulate))
-    monkeypatch.setenv("AIRSCHED_SHARD_K", "7")
+    ctxopt(SHARDED=1)
+    ctxopt(SHARD_EMULATE=int(emulate))
+    ctxopt(SHARD_K=7)
     inst = instgen.generate(cfg)
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -457,11 +457,11 @@ def test_batch_gather_best(A, ctx, oracle_mod):
         assert O.objective(*g["best"]) == g["best_obj"] and O.feasible(*g["best"])
 
 
-def test_per_cta_kernel_still_exact(A, ctx, oracle_mod, monkeypatch):
+def test_per_cta_kernel_still_exact(A, ctx, oracle_mod, monkeypatch, ctxopt):
     """k_search (one run per CTA, int32 layout) -- the path for tabu digests and
     for instances outside the compact layout -- forced for a plain run."""
-    monkeypatch.setenv("AIRSCHED_ONE_CTA", "0")
-    monkeypatch.setenv("AIRSCHED_GRID", "0")
+    ctxopt(ONE_CTA=0)
+    ctxopt(GRID=0)
     inst = instgen.generate("ontario")
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -556,15 +556,12 @@ def test_asymmetric_table_parity(A, ctx, oracle_mod, cfg, iters, monkeypatch):
     c = instgen.CONFIGS[cfg]
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters, seed=4, kick=4)
     _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
-    with monkeypatch.context() as mp:
-        mp.setenv("AIRSCHED_GRID", "1")
+    with ctx.options(GRID=1):
         _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
-        mp.setenv("AIRSCHED_GRID_T_GLOBAL", "1")   # row-local reads of the global table (TR)
-        _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
-        _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
-    with monkeypatch.context() as mp:
-        mp.setenv("AIRSCHED_SHARDED", "1")
-        mp.setenv("AIRSCHED_SHARD_EMULATE", "3")
+        with ctx.options(GRID_T_GLOBAL=1):   # row-local reads of the global table (TR)
+            _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+            _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    with ctx.options(SHARDED=1, SHARD_EMULATE=3):
         _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
     R = 40
     seeds = np.arange(1, R + 1, dtype=np.uint64)
@@ -648,12 +645,12 @@ def test_batch_run_jobs(A, ctx, oracle_mod):
     assert e.value.status == A.AS_ERR_UNSUPPORTED
 
 
-def test_state_too_large_for_shared_memory(A, oracle_mod, monkeypatch):
+def test_state_too_large_for_shared_memory(A, oracle_mod):
     """When no on-chip kernel can hold an instance's state, as_tabu_run runs the sharded
     kernels on one rank (state in global memory).  Forced here by capping the usable shared
     memory of a fresh context; the trace must still equal the oracle's."""
-    monkeypatch.setenv("AIRSCHED_SMEM_LIMIT", "12000")
     small = A.Ctx(0)
+    small.set_option("SMEM_LIMIT", 12000)
     inst = instgen.generate("ontario")
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -687,11 +684,11 @@ def test_largest_single_instance(A, ctx, oracle_mod):
 
 
 @pytest.mark.parametrize("cfg,iters", [("ontario", 400), ("large", 30), ("surge", 2)])
-def test_sharded_fused_one_rank(A, ctx, oracle_mod, cfg, iters, monkeypatch):
+def test_sharded_fused_one_rank(A, ctx, oracle_mod, cfg, iters, monkeypatch, ctxopt):
     """The fused sharded kernel (k_grid per rank; the 8-byte winner exchanged through NVLink
     stores into an NCCL symmetric window + an LSA barrier inside the kernel), run with a
     one-rank communicator on this GPU: its tile slice, exchange and apply against the oracle."""
-    monkeypatch.setenv("AIRSCHED_SHARD_FUSED_1", "1")
+    ctxopt(SHARD_FUSED_1=1)
     comm = A.Comm(ctx, 1, 0, A.as_comm_unique_id())
     inst = instgen.generate(cfg)
     O = oracle_mod.Oracle(inst)

@@ -8,7 +8,7 @@ reading (DESIGN.md #42).  Checked here, bit-exact against the CPU oracle:
 full traces, final tabu matrices and best schedules over tenures that stress
 the ring (0, 1, 2, the default 10, the limit 64, and 65 which falls back to the
 shared-memory tabu matrix), strict tabu stop, NS; and the window kernel against
-the FAST kernel (AIRSCHED_WIN=0) on whole batches.
+the FAST kernel (option WINDOW=0) on whole batches.
 """
 import numpy as np
 import pytest
@@ -45,10 +45,10 @@ def start_of(O, inst):
 
 @pytest.mark.parametrize("cfg,iters", [("tiny", 200), ("ontario", 600), ("batched", 400)])
 @pytest.mark.parametrize("tenure", [0, 1, 2, 10, 64, 65])
-def test_window_single_run_trace(A, ctx, oracle_mod, cfg, iters, tenure, monkeypatch):
+def test_window_single_run_trace(A, ctx, oracle_mod, cfg, iters, tenure, monkeypatch, ctxopt):
     """One run on the batched kernel: every chosen move, the objective trace, the
     final tabu matrix and the best schedule equal the oracle's."""
-    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+    ctxopt(BATCH_KERNEL=1)
     inst = instgen.generate(cfg)
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -66,8 +66,8 @@ def test_window_single_run_trace(A, ctx, oracle_mod, cfg, iters, tenure, monkeyp
 
 
 @pytest.mark.parametrize("cfg", ["tiny", "ontario"])
-def test_window_strict_stop_and_ns(A, ctx, oracle_mod, cfg, monkeypatch):
-    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+def test_window_strict_stop_and_ns(A, ctx, oracle_mod, cfg, monkeypatch, ctxopt):
+    ctxopt(BATCH_KERNEL=1)
     inst = instgen.generate(cfg)
     O = oracle_mod.Oracle(inst)
     h = A.Instance(inst)
@@ -87,8 +87,8 @@ def test_window_strict_stop_and_ns(A, ctx, oracle_mod, cfg, monkeypatch):
 
 
 @pytest.mark.parametrize("mode,tenure", [(1, 10), (1, 0), (1, 64), (0, 0)])
-def test_window_equals_fast_kernel(A, ctx, mode, tenure, monkeypatch):
-    """Whole batches: the window kernel and the FAST kernel (AIRSCHED_WIN=0) give the
+def test_window_equals_fast_kernel(A, ctx, mode, tenure, monkeypatch, ctxopt):
+    """Whole batches: the window kernel and the FAST kernel (option WINDOW=0) give the
     same results, traces and best schedules for every run."""
     inst = instgen.generate("batched")
     h = A.Instance(inst)
@@ -97,7 +97,7 @@ def test_window_equals_fast_kernel(A, ctx, mode, tenure, monkeypatch):
     seeds = np.arange(1, R + 1, dtype=np.uint64)
     out = []
     for win in ("1", "0"):
-        monkeypatch.setenv("AIRSCHED_WIN", win)
+        ctxopt(WINDOW=int(win))
         res = np.zeros(R, A.RESULT_DTYPE)
         tr = np.zeros((R, iters), A.TRACE_DTYPE)
         bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
@@ -157,7 +157,7 @@ def _zero_legs(cfg, k=6):
 
 
 @pytest.mark.parametrize("cfg", ["ontario", "batched"])
-def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch):
+def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch, ctxopt):
     inst = _zero_legs(cfg)
     O = oracle_mod.Oracle(inst)
     st, (p, m), _, _ = O.greedy(insert_mode=1)
@@ -169,7 +169,7 @@ def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch):
     for mode, tenure in ((1, 10), (0, 0)):
         out = []
         for win in ("1", "0"):
-            monkeypatch.setenv("AIRSCHED_WIN", win)
+            ctxopt(WINDOW=int(win))
             res = np.zeros(R, A.RESULT_DTYPE)
             tr = np.zeros((R, iters), A.TRACE_DTYPE)
             prm = A.params(mode=mode, tenure=tenure, max_iters=iters, kick=6, trace_level=1)
@@ -183,8 +183,8 @@ def test_window_general_legs(A, ctx, oracle_mod, cfg, monkeypatch):
             assert res[r]["best_obj"] == o["best_obj"] and res[r]["iters_done"] == kk
             assert (tr[r]["idx"][:kk] == o["trace"]["idx"]).all()
     # a single run on the batched kernel: full trace and final tabu matrix
-    monkeypatch.setenv("AIRSCHED_WIN", "1")
-    monkeypatch.setenv("AIRSCHED_BATCH_KERNEL", "1")
+    ctxopt(WINDOW=1)
+    ctxopt(BATCH_KERNEL=1)
     prm = A.params(mode=1, tenure=7, max_iters=iters, trace_level=1, seed=3, kick=4)
     g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)
     o = O.search(p, m, mode=1, tenure=7, max_iters=iters, seed=3, kick=4)

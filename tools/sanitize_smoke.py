@@ -21,10 +21,9 @@ def main():
         A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_digest=True, want_tabu=True)      # k_search
         prm = A.params(mode=1, tenure=5, max_iters=30, trace_level=1, seed=3, kick=3)
         A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)                         # k_grid, 1 CTA
-        os.environ["AIRSCHED_GRID"] = "1"
-        A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)                         # k_grid, all SMs
-        A.as_nbhd_run(ctx, h, p, m, A.params(mode=0, max_iters=30), want_trace=True)
-        del os.environ["AIRSCHED_GRID"]
+        with ctx.options(GRID=1):
+            A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)                     # k_grid, all SMs
+            A.as_nbhd_run(ctx, h, p, m, A.params(mode=0, max_iters=30), want_trace=True)
         R = 40
         res = np.zeros(R, A.RESULT_DTYPE)
         bp = np.zeros((R, inst.n_vehicles + 1), np.int32)
@@ -32,10 +31,8 @@ def main():
         A.as_batch_run(ctx, h, R, p, m, prm, np.arange(1, R + 1, dtype=np.uint64), results=res, best_ptr_out=bp,
                        best_missions_out=bm)                                                       # k_batch
         A.as_batch_gather_best(ctx, h, R, bp, bm)
-        os.environ["AIRSCHED_SHARDED"] = "1"
-        os.environ["AIRSCHED_SHARD_EMULATE"] = "3"
-        A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)                         # sharded kernels
-        del os.environ["AIRSCHED_SHARDED"], os.environ["AIRSCHED_SHARD_EMULATE"]
+        with ctx.options(SHARDED=1, SHARD_EMULATE=3):
+            A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=True)                     # sharded kernels
     print("sanitize smoke ok")
 
 
