@@ -644,6 +644,62 @@ def run_single(args):
     return 0
 
 
+# (config, single-thread iterations, all-core iterations)
+ORACLE_PLAN = [("tiny", 200, 200), ("ontario", 200, 400), ("batched", 100, 100), ("large", 5, 40), ("surge", 1, 3)]
+
+
+
+def oracle_baselines(out):
+    """cpu_baseline leg for every config: the oracle as it stands on this host,
+    single thread (or_search) and all cores (independent runs for C3; or_search_par with memo
+    off -- the same per-move arithmetic over one index chunk per core -- for the single-instance
+    configs), bounded samples (a few iterations of C4/C5).  JSON lines to `out`."""
+    import oracle  # noqa: F401  (cpu_baseline leg only)
+    from concurrent.futures import ThreadPoolExecutor
+    cores = os.cpu_count() or 1
+    rows = []
+    for name, it1, itn in ORACLE_PLAN:
+        cfg = instgen.CONFIGS[name]
+        inst = instgen.generate(name)
+        O = oracle.Oracle(inst)
+        st, (p, m), _, _ = O.greedy()
+        n, V = inst.n_missions, inst.n_vehicles
+        VM = n * (n + V - 2) + n * (n - 1) // 2
+        t0 = time.perf_counter()
+        r = O.search(p, m, mode=1, tenure=cfg.tenure, max_iters=it1, trace=False)
+        t1 = time.perf_counter() - t0
+        single = r["iters_done"] * VM / t1
+        if cfg.n_runs > 1:
+            runs = cores * 4
+
+            def one(seed):
+                return O.search(p, m, mode=1, tenure=cfg.tenure, max_iters=itn, seed=seed, kick=cfg.kick,
+                                trace=False)["iters_done"]
+            t0 = time.perf_counter()
+            with ThreadPoolExecutor(max_workers=cores) as ex:
+                its = sum(ex.map(one, range(1, runs + 1)))
+            tn = time.perf_counter() - t0
+            alln = its * VM / tn
+            how = f"{runs} independent runs x {itn} TS iterations on {cores} threads"
+        else:
+            t0 = time.perf_counter()
+            r = O.search_par(p, m, mode=1, tenure=cfg.tenure, max_iters=itn, threads=cores, memo=False, trace=False)
+            tn = time.perf_counter() - t0
+            alln = r["iters_done"] * VM / tn
+            how = f"{itn} TS iterations, index range in {cores} chunks (or_search_par, memo off)"
+        row = {"config": name, "n": n, "V": V, "valid_moves_per_iter": VM, "unit": "move evals/s",
+               "single_thread": single, "single_thread_sample": f"{it1} TS iterations (or_search)",
+               "all_cores": alln, "all_cores_sample": how, "cores": cores, "cpu_model": cpu_model(),
+               "kind": "oracle (plain recompute per move, untuned)"}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as f:
+        for r in rows:
+            f.write(json.dumps(r) + "\n")
+
+
+
 def free_port():
     import socket
     with socket.socket() as so:
@@ -708,6 +764,8 @@ def main():
     ap.add_argument("--min-seconds", type=float, default=0.0,
                     help="single-instance workloads: repeat steps until the timed region lasts this long")
     ap.add_argument("--dry", action="store_true", help="launch-path check on CPU (gloo), no GPU work")
+    ap.add_argument("--oracle-baselines", default=None, metavar="PATH",
+                    help="only the cpu_baseline leg, for every config: write JSON lines to PATH")
     args = ap.parse_args()
     launched = "WORLD_SIZE" in os.environ
     if args.gpus < 1:
@@ -720,6 +778,9 @@ def main():
         return 2
     if args.dry:
         return run_dry(args)
+    if args.oracle_baselines:
+        oracle_baselines(args.oracle_baselines)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "instances":

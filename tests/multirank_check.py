@@ -1,4 +1,4 @@
-"""Multi-rank parity check of the sharded single-instance paths (run under torchrun, one
+"""(Test helper.) Multi-rank parity check of the sharded single-instance paths (run under torchrun, one
 rank per GPU; tests/test_gpu_multirank.py launches it with 2/4/8 ranks when the box has
 the GPUs).  Every rank runs as_tabu_run / as_nbhd_run with an NCCL communicator on C2
 (full 5,000 iterations) and a C5 prefix, on the fused path (k_grid per rank, NVLink key

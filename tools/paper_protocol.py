@@ -6,11 +6,15 @@ For n = 12, 15, ..., 33 missions and the paper's fleet (12 vehicles: 8
 helicopters + 4 planes, one per base): an Ontario-like instance with
 deadlines inside 24 h, the Alg. 1 start, 10 runs each of NS and TS (runs differ
 by their seeded kick, the analogue of the paper's random permutation vectors,
-P:269), U / L / A objective in hours, the exact optimum from the arc ILP (scipy
-HiGHS, the test-only stand-in for Gurobi, with a time limit; status reported),
-and the A-gap.  Runtimes are GPU device times per run.  Writes a markdown table.
+P:269), U / L / A objective in hours, the exact optimum of the arc model
+(tools/exact.py: scipy HiGHS, the stand-in for Gurobi, with a time limit; status
+reported; --mps-dir also writes each instance's model as MPS for an external
+solver), and the A-gap.  Runtimes are GPU device times per run.
+Writes a markdown table and (--json) the rows with every run's raw result, the
+start schedule and the parameters, from which tests/test_gpu_protocol.py re-runs
+run 1 of each size on the CPU oracle (this tool itself never touches oracle/).
 
-    python tools/paper_protocol.py --out profiles/r01/paper_protocol.md
+    python tools/paper_protocol.py --out profiles/r02/paper_protocol.md
 """
 from __future__ import annotations
 
@@ -23,8 +27,9 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tools")]
 
+import exact  # noqa: E402
 from paper_2002_11710_b200 import airsched as A  # noqa: E402
 from paper_2002_11710_b200 import instgen  # noqa: E402
 
@@ -35,21 +40,20 @@ def paper_instance(n, seed):
 
 
 def ilp(inst, time_limit):
-    from scipy.optimize import milp  # noqa: F401  (availability check)
-    import pins
     t0 = time.perf_counter()
-    opt = pins.ilp_optimum(inst, time_limit=time_limit)
+    opt = exact.solve(inst, time_limit=time_limit)
     return opt, time.perf_counter() - t0
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "paper_protocol.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "paper_protocol.md"))
+    ap.add_argument("--json", default=None, help="also write the rows as JSON lines")
+    ap.add_argument("--mps-dir", default=None, help="write each instance's model (MPS) here")
     ap.add_argument("--runs", type=int, default=10)
     ap.add_argument("--iters", type=int, default=1000)
     ap.add_argument("--ilp-time", type=float, default=120.0)
     ap.add_argument("--sizes", default="12,15,18,21,24,27,30,33")
-    ap.add_argument("--oracle-check", action="store_true", help="compare run 1 of each size with the CPU oracle")
     args = ap.parse_args()
     ctx = A.Ctx(0)
     rows = []
@@ -69,13 +73,14 @@ def main():
             objs = res["best_obj"] / 3600.0
             out[name] = dict(U=float(objs.max()), L=float(objs.min()), A=float(objs.mean()), ms=ms,
                              iters=int(res["iters_done"].mean()), raw=res["best_obj"].tolist())
-            if args.oracle_check:
-                import oracle
-                O = oracle.Oracle(inst)
-                o = O.search(p, m, mode=mode, tenure=10, max_iters=args.iters, seed=1, kick=4, trace=False)
-                assert o["best_obj"] == res[0]["best_obj"], (n, name, o["best_obj"], res[0]["best_obj"])
+
+        if args.mps_dir:
+            os.makedirs(args.mps_dir, exist_ok=True)
+            exact.export_mps(inst, os.path.join(args.mps_dir, f"paper_n{n}.mps"))
         opt, t_ilp = ilp(inst, args.ilp_time)
-        rows.append(dict(n=n, start_h=start / 3600.0, opt_h=None if opt is None else opt / 3600.0, t_ilp=t_ilp, **out))
+        rows.append(dict(n=n, seed=2002117100 + 100 + n, start_h=start / 3600.0,
+                         opt_h=None if opt is None else opt / 3600.0, t_ilp=t_ilp,
+                         start_ptr=p.tolist(), start_ms=m.tolist(), iters=args.iters, tenure=10, kick=4, **out))
         print(json.dumps({k: (v if not isinstance(v, dict) else {kk: vv for kk, vv in v.items() if kk != "raw"})
                           for k, v in rows[-1].items()}), flush=True)
     lines = ["# Paper protocol (§5) on synthetic instances — SURVEY §8(f) f4", "",
@@ -98,6 +103,10 @@ def main():
               "2.0-7.1 %, Gurobi stuck beyond 27 missions, CUDA variants 0.5-0.7 s per run.", ""]
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write("\n".join(lines))
+    if args.json:
+        with open(args.json, "w") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
     print("\n".join(lines))
 
 
