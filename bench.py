@@ -37,6 +37,73 @@ UNIT = "move evals/s"
 # per swap pair, with the per-row removal part amortised.
 OPS_RELOCATE = 23
 OPS_SWAP = 37
+# SURVEY §8(d) algorithmic on-chip work per move (what the method must touch, the m side
+# amortised): relocate 2 T + target record + vehicle record + E = 36-40 B, ~40 instructions;
+# swap 4 T + 2 records + 2 vehicles + 2 E = 72 B, ~80 instructions.
+BYTES_RELOCATE, BYTES_SWAP = 38, 72
+INSTR_RELOCATE, INSTR_SWAP = 40, 80
+PROFILE_DIR = os.path.join(ROOT, "profiles", "r02")
+
+
+def onchip_peaks():
+    """Measured on-chip ceilings of this B200 (tools/onchip_peaks.cu, committed JSON)."""
+    try:
+        with open(os.path.join(PROFILE_DIR, "onchip_peaks.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def move_mix(inst):
+    n, V = inst.n_missions, inst.n_vehicles
+    return n * (n + V - 2), n * (n - 1) // 2
+
+
+def onchip_roofline(relocs, swaps, t_s, f_mhz, n_gpus=1, workload=None):
+    """Roofline of the move-evaluation kernel at the memory level that serves it (SURVEY §8(d):
+    shared memory / L1 for the resident configs; HBM ~0 by design) and at instruction issue.
+    achieved = algorithmic bytes (instructions) of the moves scored / device time; peak = the
+    MEASURED shared-memory bandwidth (conflict-free LDS wavefronts, tools/onchip_peaks.cu) and
+    the issue ceiling (4 SMSP x 32 lanes per SM cycle; measured INT mixes alongside), both at the
+    SM clock sampled under load.  `bound` = the ceiling closer to saturation."""
+    pk = onchip_peaks()
+    f = f_mhz * 1e6
+    smem_bpc = (pk.get("lds_seq") or {}).get("bytes_per_sm_cycle") or 128.0
+    smem_peak = 148 * smem_bpc * f * n_gpus
+    issue_peak = 148 * 128 * f * n_gpus
+    b = relocs * BYTES_RELOCATE + swaps * BYTES_SWAP
+    ins = relocs * INSTR_RELOCATE + swaps * INSTR_SWAP
+    a_smem, a_issue = b / t_s, ins / t_s
+    ops = relocs * OPS_RELOCATE + swaps * OPS_SWAP
+    smem = {"achieved": a_smem / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s", "frac": a_smem / smem_peak,
+            "peak_basis": f"measured {smem_bpc:.1f} B per SM cycle (conflict-free LDS, profiles/r02/onchip_peaks.json)"
+                          f" x 148 SMs x {f_mhz:.0f} MHz" + (f" x {n_gpus} GPUs" if n_gpus > 1 else "")}
+    issue = {"achieved": a_issue / 1e9, "peak": issue_peak / 1e9, "unit": "Ginstr/s", "frac": a_issue / issue_peak,
+             "peak_basis": f"148 SMs x 4 SMSP x 32 lanes x {f_mhz:.0f} MHz" + (f" x {n_gpus} GPUs" if n_gpus > 1 else ""),
+             "measured_int_lanes_per_sm_cycle": {"alu_only": (pk.get("int_alu") or {}).get("lanes_per_sm_cycle"),
+                                                 "alu_fma_mix": (pk.get("int_mix") or {}).get("lanes_per_sm_cycle")}}
+    bound, main = ("smem", smem) if smem["frac"] >= issue["frac"] else ("issue", issue)
+    roof = {"bound": bound, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
+            "frac": main["frac"], "traffic": measured_traffic(workload) if workload else None,
+            "peak_basis": main["peak_basis"],
+            "model": f"SURVEY 8(d) per move: relocate {BYTES_RELOCATE} B / {INSTR_RELOCATE} instr, swap {BYTES_SWAP} B / "
+                     f"{INSTR_SWAP} instr; {relocs:.4g} relocates + {swaps:.4g} swaps scored",
+            "smem": smem, "issue": issue,
+            "op_count": {"achieved": ops / t_s / 1e9, "peak": issue_peak / 1e9, "unit": "Gop/s",
+                         "frac": ops / t_s / issue_peak,
+                         "basis": f"{OPS_RELOCATE}/{OPS_SWAP} algorithmic integer ops per relocate/swap move"}}
+    prof = measured_profile(workload) if workload else {}
+    if prof:   # hardware counters of the committed ncu capture of this workload's dominant kernel
+        hw = {"source": prof.get("source"), "issue_slots_busy": prof.get("issue_slots_busy"),
+              "alu_fma_pipe": [prof.get("alu_pipe"), prof.get("fma_pipe")]}
+        if "shared_wavefronts" in prof and "duration_ms" in prof:
+            gbps = prof["shared_wavefronts"] * 128 / (prof["duration_ms"] / 1e3) / 1e9
+            hw["shared_wavefront_GBps"] = gbps
+            hw["shared_wavefront_frac_of_measured_peak"] = gbps / (148 * smem_bpc * 1965e6 / 1e9)
+            if "shared_bank_conflict_wavefronts" in prof:
+                hw["bank_conflict_share"] = prof["shared_bank_conflict_wavefronts"] / prof["shared_wavefronts"]
+        roof["ncu"] = hw
+    return roof
 
 
 def log(*a):
@@ -313,24 +380,12 @@ def run_gpu(args):
     h2d = p.nbytes + m.nbytes + seeds_np.nbytes
     d2h = R * 40
 
-    # ---- roofline of the dominant kernel (k_batch: the step is k_batch + the tiny k_batch_best)
-    ops = (inst.n_missions * (inst.n_missions + inst.n_vehicles - 2) * OPS_RELOCATE +
-           inst.n_missions * (inst.n_missions - 1) // 2 * OPS_SWAP)
+    # ---- roofline of the dominant kernel (k_batch: the step is k_batch + the tiny k_batch_best;
+    # its share of the step is in the committed ncu launch list)
     f_mhz = clocks.get("sm_mhz") or 1965.0
-    peak_gops = 148 * 128 * f_mhz * 1e6 / 1e9
-    achieved_gops = (iters_total * ops) / (t_ms / 1e3) / 1e9 if world == 1 else (iters_all * ops) / (t_ms / 1e3) / world / 1e9
-    roof = {"bound": "alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
-            "frac": achieved_gops / peak_gops, "traffic": args.traffic if args.traffic is not None else
-            measured_traffic(args.workload),
-            "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"}
-    prof = measured_profile(args.workload)
-    if "issue_slots_busy" in prof:   # the issue-slot view of the same kernel (ncu): it is issue-bound
-        roof["ncu_issue_slots_busy"] = prof["issue_slots_busy"]
-        roof["ncu_alu_fma_pipe"] = [prof.get("alu_pipe"), prof.get("fma_pipe")]
-    if "shared_wavefronts_pct_of_peak" in prof:   # the memory level that binds (HBM/L2 are ~0 by design)
-        roof["ncu_shared_mem_pct_of_peak"] = prof["shared_wavefronts_pct_of_peak"]
-        if "duration_ms" in prof and "shared_wavefronts" in prof:   # 128 B per shared-memory wavefront
-            roof["ncu_shared_mem_GBps"] = prof["shared_wavefronts"] * 128 / (prof["duration_ms"] / 1e3) / 1e9
+    rl, sw = move_mix(inst)
+    its_rank = iters_total if world == 1 else iters_all / world
+    roof = onchip_roofline(its_rank * rl, its_rank * sw, t_ms / 1e3, f_mhz, 1, args.workload)
 
     sharded = None if args.no_sharded else sharded_c5(args, A, ctx, comm, world, rank, dev)
     if rank != 0:
@@ -429,21 +484,16 @@ def sharded_c5(args, A, ctx, comm, world, rank, dev):
         t, te = float(tt[0].item()), float(tt[1].item())
     ctx.set_option("SHARD_FUSED", None)
     ctx.set_option("XR_TIMEOUT_MS", None)
-    ops = (inst.n_missions * (inst.n_missions + inst.n_vehicles - 2) * OPS_RELOCATE +
-           inst.n_missions * (inst.n_missions - 1) // 2 * OPS_SWAP)
     f_mhz = clocks.get("sm_mhz") or 1965.0
-    peak = 148 * 128 * f_mhz * 1e6 / 1e9 * world
-    ach = its * ops / t / 1e9
+    rl, sw = move_mix(inst)
+    roof = onchip_roofline(its * rl, its * sw, t, f_mhz, world, "surge")
     return {"workload": f"C5 surge: n={inst.n_missions}, V={inst.n_vehicles}, TS {iters} iters per step, "
                         f"one instance sharded over {world} GPU(s)", "scaling": "strong", "path": path,
             "value": its * VM / t, "unit": UNIT, "tabu_iters_per_s": its / t, "ms_per_step": 1e3 * t / 3,
             "steps": 3, "n_gpus": world, "valid_moves_per_iter": VM, "best_obj": r["best_obj"], "clocks": clocks,
             "e2e": {"value": r["iters_done"] * VM / te, "unit": UNIT, "h2d_bytes_per_step": int(p.nbytes + m.nbytes),
                     "d2h_bytes_per_step": int(40 + (inst.n_vehicles + 1 + inst.n_missions) * 4)},
-            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gop/s", "frac": ach / peak,
-                         "traffic": None,
-                         "peak_basis": f"{world} x 148 SM x 128 INT32 lanes x {f_mhz:.0f} MHz; {OPS_RELOCATE}/{OPS_SWAP} "
-                                       "algorithmic ops per relocate/swap move"}}
+            "roofline": roof}
 
 
 def run_jobs(args):
@@ -509,9 +559,6 @@ def run_jobs(args):
     launches = ctx.kernel_launches - launches0
     res = tres.cpu().numpy().view(A.RESULT_DTYPE).reshape(R)
     moves = sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) * valid_moves(insts[j]) for j in range(n_inst))
-    ops = sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) *
-              (insts[j].n_missions * (insts[j].n_missions + insts[j].n_vehicles - 2) * OPS_RELOCATE +
-               insts[j].n_missions * (insts[j].n_missions - 1) // 2 * OPS_SWAP) for j in range(n_inst))
     t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
     if world > 1:
         tt = torch.tensor([t_ms, 0.0], dtype=torch.float64, device=dev)
@@ -528,8 +575,6 @@ def run_jobs(args):
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_moves = sum(int(hres["iters_done"][j * per:(j + 1) * per].sum()) * valid_moves(insts[j]) for j in range(n_inst))
     f_mhz = clocks.get("sm_mhz") or 1965.0
-    peak = 148 * 128 * f_mhz * 1e6 / 1e9
-    ach = ops * args.steps / (t_ms / 1e3) / 1e9
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -546,9 +591,10 @@ def run_jobs(args):
             "e2e": {"value": e2e_moves * world / (float(np.mean(e2e_ms)) / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(R * 40)},
             "gpu_launches": int(launches), "clocks": clocks,
-            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gop/s", "frac": ach / peak,
-                         "traffic": None,
-                         "peak_basis": f"148 SM x 128 INT32/FP32 lanes x {f_mhz:.0f} MHz (median SM clock under load)"},
+            "roofline": onchip_roofline(
+                sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) * move_mix(insts[j])[0] for j in range(n_inst))
+                * args.steps, sum(int(res["iters_done"][j * per:(j + 1) * per].sum()) * move_mix(insts[j])[1]
+                                  for j in range(n_inst)) * args.steps, t_ms / 1e3, f_mhz, 1, "instances"),
             "cpu_baseline": None}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -558,8 +604,8 @@ def run_jobs(args):
 
 def measured_profile(workload):
     """The committed ncu --set full capture of the dominant kernel for this workload
-    (profiles/r01/traffic.json), or {}."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    (profiles/r02/traffic.json), or {}."""
+    path = os.path.join(PROFILE_DIR, "traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get(workload) or {}
@@ -637,7 +683,9 @@ def run_single(args):
                                    f"{'NS' if args.ns else 'TS'} {iters} iters", "valid_moves_per_iter": VM,
                        "parallelism": f"move space sharded over {world} GPUs" if world > 1 else "1 GPU"},
             "tabu_iters_per_s": its / t, "iters_done_per_step": its / steps, "best_obj": r["best_obj"],
-            "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches}
+            "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches,
+            "roofline": onchip_roofline(its * move_mix(inst)[0], its * move_mix(inst)[1], t,
+                                        clocks.get("sm_mhz") or 1965.0, world, args.workload)}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

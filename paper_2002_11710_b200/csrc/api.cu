@@ -786,9 +786,9 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 if (xr) grid_blocks = std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS, ctx->n_sm)));
                 GA.Tglobal = D.Tpad;
                 void *p;
-                if ((st = scratch(ctx, "g_ll", (size_t)(2 * 2 * grid_blocks + 4) * 8, &p)) != AS_OK) return st;
-                GA.ll = (unsigned long long *)p;          // zeroed by the kernel (own slots) at launch
-                GA.llb = GA.ll + 2 * 2 * grid_blocks;
+                if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
+                GA.gkey = (unsigned long long *)p;
+                CUDA_TRY(cudaMemsetAsync(p, 0xFF, 3 * 8, ctx->stream));
                 if ((st = scratch(ctx, "g_bs", (size_t)S * 4, &p)) != AS_OK) return st;
                 GA.BS = (int32_t *)p;
                 if (tabu && !GA.E_smem) {
@@ -823,6 +823,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     GA.xr_epoch = xr->epoch;
                     GA.xr_timeout_ns = xr->timeout_ns;
                     GA.xr_win = xr->win;
+                    if ((st = scratch(ctx, "g_key2", 3 * 8, &p)) != AS_OK) return st;
+                    GA.gkey2 = (unsigned long long *)p;
                 }
             }
         }

@@ -100,51 +100,6 @@ __device__ __forceinline__ uint64_t rank_exchange(const GridArgs &GA, int q, int
     return kg;
 }
 
-// Grid-wide key exchange without atomics or a grid barrier (LL slots, as NCCL's LL protocol):
-// every CTA publishes its CTA minimum as two 8-byte words {key_hi << 32 | tag, key_lo << 32 | tag}
-// (naturally aligned 64-bit stores are single-copy atomic, so each word carries its own flag and no
-// release/acquire pair is needed), and warp 0 of every CTA polls all CTAs' slots until every tag is
-// this iteration's, then takes the minimum.  One one-way store plus one poll round trip from the
-// last CTA's publish to everyone's key, instead of an arrival atomic, a flag spin and a key read
-// (grid.sync + __ldcg).  Slots are double-buffered by iteration parity: a CTA writes iteration
-// it+2's slot only after it has read every CTA's iteration it+1 key, i.e. after every CTA has
-// finished reading iteration it's slots.  tag = it + 1 (slots are zeroed at launch, before the
-// start-up grid.sync).
-__device__ __forceinline__ void ll_publish(unsigned long long *slot, uint64_t key, uint32_t tag) {
-    const unsigned long long a = (key & 0xFFFFFFFF00000000ull) | tag, b = (key << 32) | tag;
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(a), "l"(b) : "memory");
-}
-
-__device__ __forceinline__ bool ll_read(const unsigned long long *slot, uint32_t tag, uint64_t &key) {
-    unsigned long long a, b;
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(slot) : "memory");
-    key = (a & 0xFFFFFFFF00000000ull) | (b >> 32);
-    return (uint32_t)a == tag && (uint32_t)b == tag;
-}
-
-// Warp-wide: the minimum of the keys in slots [0, n) (stride 2 words) once all carry `tag`.
-constexpr int LL_MAX_PER_LANE = 8;   // up to 256 CTAs
-__device__ __forceinline__ uint64_t ll_gather_min(const unsigned long long *slots, int n, uint32_t tag, int lane) {
-    uint64_t k[LL_MAX_PER_LANE];
-    bool got[LL_MAX_PER_LANE];
-#pragma unroll
-    for (int j = 0; j < LL_MAX_PER_LANE; j++) { got[j] = lane + 32 * j >= n; k[j] = KEY_NONE; }
-    for (;;) {
-        bool all = true;
-#pragma unroll
-        for (int j = 0; j < LL_MAX_PER_LANE; j++)
-            if (!got[j]) {
-                got[j] = ll_read(slots + 2 * (size_t)(lane + 32 * j), tag, k[j]);
-                all &= got[j];
-            }
-        if (__all_sync(0xFFFFFFFFu, all)) break;
-    }
-    uint64_t m = KEY_NONE;
-#pragma unroll
-    for (int j = 0; j < LL_MAX_PER_LANE; j++) m = k[j] < m ? k[j] : m;
-    return wmin(m);
-}
-
 // TR: the table is read from global memory (row-local reads, score.cuh).
 template <bool TABU, class TT, class ET, bool FULL, bool TR>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
@@ -263,9 +218,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     __syncthreads();
     if (blockIdx.x == 0)
         for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
-    if (tid < 4) GA.ll[(size_t)(tid >> 1) * 2 * gridDim.x + 2 * blockIdx.x + (tid & 1)] = 0;   // own LL slots
-    if (blockIdx.x == 0 && tid < 4) GA.llb[tid] = 0;                                         // broadcast slots
-    if (gridDim.x > 1) grid.sync();   // global tabu matrix and LL slots initialised before anyone reads them
+    if (gridDim.x > 1) grid.sync();   // global tabu matrix initialised before anyone reads it
 
     ScoreCtx<TT, ET> SC;
     SC.Ts = Ts; SC.Tt = I.tsym ? Ts : reinterpret_cast<const TT *>(I.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
@@ -281,6 +234,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     const int nwarps_all = gridDim.x * nwarps;
     const int gwarp = GT_spread(GA.thi - GA.tlo, nwarps_all) ? warp * gridDim.x + blockIdx.x : blockIdx.x * nwarps + warp;
     const bool one = gridDim.x == 1;
+    unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
 
     int it = 0;
     for (; it < A.max_iters; it++) {
@@ -289,36 +243,31 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         kmin = wmin(kmin);
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
+        uint64_t kcta = KEY_NONE;
+        if (warp == 0) {   // CTA minimum by one warp (parallel loads + shuffles, not a serial loop)
+            kcta = wmin(lane < nwarps ? red[lane] : KEY_NONE);
+            if (lane == 0 && !one) {
+                if (kcta != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)kcta);
+                if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
+            }
+        }
+        if (!one) grid.sync();   // a single CTA (small instances) needs no grid barrier
+        if (GA.xr) {   // fused sharded run: the all-ranks minimum over NVLink, then every CTA reads it
+            if (blockIdx.x == 0 && tid == 0) {
+                const int q = it % 3;
+                const uint64_t kl = one ? kcta : __ldcg(&gkey[q]);
+                GA.gkey2[q] = rank_exchange(GA, q, it, kl);
+            }
+            if (one) __syncthreads();
+            else grid.sync();
+        }
         if (warp == 0) {
-            // CTA minimum, then (several CTAs) the grid minimum through the LL slots -- warp 0 of
-            // every CTA ends up with the same key, no grid barrier
-            uint64_t kg = wmin(lane < nwarps ? red[lane] : KEY_NONE);
-            const uint32_t tag = (uint32_t)it + 1u;
-            if (!one) {
-                unsigned long long *sl = GA.ll + (size_t)(it & 1) * 2 * gridDim.x;
-                if (lane == 0) ll_publish(sl + 2 * blockIdx.x, kg, tag);
-                kg = ll_gather_min(sl, gridDim.x, tag, lane);
-            }
-            if (GA.xr) {   // fused sharded run: the all-ranks minimum over NVLink, handed to every CTA
-                unsigned long long *bs = GA.llb + 2 * (it & 1);
-                if (blockIdx.x == 0) {
-                    if (lane == 0) {
-                        kg = rank_exchange(GA, it % 3, it, kg);
-                        if (!one) ll_publish(bs, kg, tag);
-                    }
-                    kg = __shfl_sync(0xFFFFFFFFu, kg, 0);
-                } else {
-                    uint64_t v;
-                    while (!__all_sync(0xFFFFFFFFu, ll_read(bs, tag, v))) {}
-                    kg = v;
-                }
-            }
             // apply (every CTA, identical arithmetic): lane 0 splits the delta (from the key: the
             // scorers proved the move valid and feasible), relinks and updates the route totals and
             // the tabu matrix; the touched incoming-link records are then refreshed one per lane
             int nt = 0;
             if (lane == 0) {
-                const uint64_t k = kg;
+                const uint64_t k = GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
                 int stop = 0;
                 if (k == KEY_ABORT) stop = AS_STOP_COMM_ABORT;   // a peer never arrived (bounded wait)
                 else if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;

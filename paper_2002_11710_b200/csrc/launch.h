@@ -76,8 +76,7 @@ struct GridArgs {
     int32_t *Eglobal;              // [n][V] tabu matrix when !E_smem
     int32_t *Etglobal;             // [V][n] its transpose (identical values), when !E_smem
     int32_t *BS;                   // [S] best-schedule successor array
-    unsigned long long *ll;        // [2][gridDim][2] LL key slots (grid.cu ll_publish / ll_gather_min)
-    unsigned long long *llb;       // [2][2] LL broadcast slot of the all-ranks winner (fused sharded run)
+    unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
     int G;                         // rows per tile
     int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
     // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
@@ -87,6 +86,7 @@ struct GridArgs {
     unsigned xr_epoch;             // per-call run epoch (same on every rank), high half of the tags
     unsigned long long xr_timeout_ns;   // bound on the wait for the peers' keys
     ncclWindow_t xr_win;           // symmetric window: [3][nranks] {key, tag} u64 pairs
+    unsigned long long *gkey2;     // [3] the all-ranks winner per slot
 };
 
 // Sharded single-instance run (shard.cu): replica state in global memory.

@@ -583,16 +583,15 @@ __host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
     return T;
 }
 
-// Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
+// One tile of the flat tile list: this lane's best packed key in it.
 template <bool TABU, bool FULL, bool TR, class TT, class ET, class MV, class RV>
-__device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
-                                                const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
-                                                int it, long long cur, long long best, int lane) {
+__device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
+                                               const GridTiles &GT, int tile, int it, long long cur, long long best,
+                                               int lane) {
     const int n = SC.n;
     const int asp = (int)(best - cur);
-    uint64_t kmin = KEY_NONE;
-    for (int tile = tlo + gwarp; tile < thi; tile += nwarps_all) {
-        uint64_t kb = KEY_NONE;
+    uint64_t kb = KEY_NONE;
+    {
         if (tile < GT.n_reloc) {
             const int c = tile % GT.nTC, g = tile / GT.nTC;
             const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
@@ -618,6 +617,18 @@ __device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, cons
                 }
             }
         }
+    }
+    return kb;
+}
+
+// Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
+template <bool TABU, bool FULL, bool TR, class TT, class ET, class MV, class RV>
+__device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
+                                                const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
+                                                int it, long long cur, long long best, int lane) {
+    uint64_t kmin = KEY_NONE;
+    for (int tile = tlo + gwarp; tile < thi; tile += nwarps_all) {
+        const uint64_t kb = score_tile<TABU, FULL, TR>(SC, M, R, GT, tile, it, cur, best, lane);
         kmin = kb < kmin ? kb : kmin;
     }
     return kmin;
