@@ -666,6 +666,14 @@ def run_single(args):
         its += r["iters_done"]
         steps += 1
     clocks = gather_clocks(sampler.stop(), world)
+    # per-iteration device latency by phase of the whole-GPU kernel (one extra, untimed run)
+    phases = None
+    try:
+        with ctx.options(PHASE_TIMES=1):
+            fn()
+            phases = ctx.grid_phases()
+    except A.AirschedError:   # the run did not use the whole-GPU kernel
+        phases = None
     t = sum(ms) / 1e3
     if world > 1:
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
@@ -684,6 +692,7 @@ def run_single(args):
                        "parallelism": f"move space sharded over {world} GPUs" if world > 1 else "1 GPU"},
             "tabu_iters_per_s": its / t, "iters_done_per_step": its / steps, "best_obj": r["best_obj"],
             "stop_reason": r["stop_reason"], "clocks": clocks, "gpu_launches": ctx.kernel_launches,
+            "phases_per_iter": phases,
             "roofline": onchip_roofline(its * move_mix(inst)[0], its * move_mix(inst)[1], t,
                                         clocks.get("sm_mhz") or 1965.0, world, args.workload)}
     print(json.dumps(line), flush=True)

@@ -137,9 +137,16 @@ enum {
     AS_OPT_SHARD_EMULATE,      /* sharded kernels without a comm: emulate this many ranks' slices */
     AS_OPT_SHARD_K,            /* iterations per CUDA graph of the NCCL-graph path */
     AS_OPT_XR_TIMEOUT_MS,      /* fused sharded exchange: bound on the wait for a peer (default 30000) */
+    AS_OPT_PHASE_TIMES,        /* 1: the whole-GPU kernel records its per-iteration phase latencies */
     AS_OPT_COUNT
 };
 as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t value);
+/* Per-iteration device latency of the last whole-GPU (k_grid) run made with AS_OPT_PHASE_TIMES = 1,
+ * measured by CTA 0 with %globaltimer and summed over the iterations: out[0] its own tiles' scoring,
+ * out[1] waiting for the CTA's other warps, out[2] CTA reduction + grid barrier (+ rank exchange),
+ * out[3] apply, in ns; out[4] = iterations.  Synchronises the context's stream.  AS_ERR_INVALID_ARG if
+ * no such run was made. */
+as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out);
 void as_ctx_destroy(as_ctx *ctx);
 /* Upload (and cache on ctx) the instance's device copy.  Optional: every call
  * below uploads on first use; call this to keep the upload out of a timed

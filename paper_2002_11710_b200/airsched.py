@@ -26,7 +26,7 @@ AS_STOP_MAX_ITERS, AS_STOP_LOCAL_OPT, AS_STOP_NO_MOVE, AS_STOP_INFEASIBLE_START,
 # as_ctx_set_option names (include/airsched.h AS_OPT_*), in enum order
 OPTIONS = ["SMEM_LIMIT", "T_SMEM", "WINDOW", "BATCH_KERNEL", "GRID", "GRID_MIN", "ONE_CTA", "GRID_T_GLOBAL",
            "GRID_E_GLOBAL", "GRID_BLOCKS", "GRID_G", "VERBOSE", "RPC", "THREADS", "SHARDED", "GREEDY_GLOBAL",
-           "SHARD_FUSED", "SHARD_FUSED_1", "SHARD_EMULATE", "SHARD_K", "XR_TIMEOUT_MS"]
+           "SHARD_FUSED", "SHARD_FUSED_1", "SHARD_EMULATE", "SHARD_K", "XR_TIMEOUT_MS", "PHASE_TIMES"]
 OPT_UNSET = -(1 << 63)
 
 SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "as_valid_moves_per_iter",
@@ -34,7 +34,7 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
            "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
-           "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option"]
+           "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option", "as_ctx_grid_phases"]
 
 
 class AirschedError(RuntimeError):
@@ -91,6 +91,7 @@ def _load():
         "as_ctx_create": (i32, [i32, vp, vp]),
         "as_ctx_set_stream": (i32, [vp, vp]),
         "as_ctx_set_option": (i32, [vp, i32, i64]),
+        "as_ctx_grid_phases": (i32, [vp, vp]),
         "as_ctx_destroy": (None, [vp]),
         "as_instance_upload": (i32, [vp, vp]),
         "as_init_greedy": (i32, [vp, vp, i32, i32, vp, vp, vp]),
@@ -206,6 +207,14 @@ class Ctx:
     def set_option(self, name: str, value):
         """as_ctx_set_option(AS_OPT_<name>, value); None = back to the automatic choice."""
         _check(lib.as_ctx_set_option(self.handle, OPTIONS.index(name), OPT_UNSET if value is None else int(value)))
+
+    def grid_phases(self):
+        """as_ctx_grid_phases: per-iteration latency (us) of the last whole-GPU run with PHASE_TIMES=1."""
+        out = np.zeros(5, np.int64)
+        _check(lib.as_ctx_grid_phases(self.handle, out.ctypes.data))
+        it = max(int(out[4]), 1)
+        return {"own_tiles_us": out[0] / it / 1e3, "cta_wait_us": out[1] / it / 1e3,
+                "reduce_barrier_us": out[2] / it / 1e3, "apply_us": out[3] / it / 1e3, "iterations": int(out[4])}
 
     def options(self, **kw):
         """Context manager: set options, restore the automatic choice on exit."""

@@ -254,6 +254,7 @@ struct as_ctx {
     size_t max_smem_hw = 0;                 // the device's opt-in limit (max_smem = min(this, AS_OPT_SMEM_LIMIT))
     int64_t opt[AS_OPT_COUNT];              // as_ctx_set_option overrides; OPT_UNSET = automatic
     unsigned long long xr_timeout_ns = 30000000000ull;   // fused sharded exchange: bound on a peer's wait
+    void *phase_dev = nullptr;              // k_grid phase sums of the last timed launch (AS_OPT_PHASE_TIMES)
 };
 
 struct as_comm {
@@ -321,6 +322,16 @@ extern "C" as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t valu
         ctx->max_smem = value == OPT_UNSET ? ctx->max_smem_hw : std::min<size_t>(ctx->max_smem_hw, (size_t)std::max<int64_t>(0, value));
     if (option == AS_OPT_XR_TIMEOUT_MS)
         ctx->xr_timeout_ns = value == OPT_UNSET ? 30000000000ull : (unsigned long long)std::max<int64_t>(1, value) * 1000000ull;
+    return AS_OK;
+}
+
+extern "C" as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out) {
+    if (!ctx || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (!ctx->phase_dev) return fail(AS_ERR_INVALID_ARG, "no whole-GPU run with AS_OPT_PHASE_TIMES yet");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaMemcpy(out, ctx->phase_dev, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     return AS_OK;
 }
 
@@ -786,6 +797,13 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 if (xr) grid_blocks = std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS, ctx->n_sm)));
                 GA.Tglobal = D.Tpad;
                 void *p;
+                GA.phase_ns = nullptr;
+                if (opt_int(ctx, AS_OPT_PHASE_TIMES, 0) == 1) {
+                    if ((st = scratch(ctx, "g_phase", 5 * 8, &p)) != AS_OK) return st;
+                    CUDA_TRY(cudaMemsetAsync(p, 0, 5 * 8, ctx->stream));
+                    GA.phase_ns = (unsigned long long *)p;
+                    ctx->phase_dev = p;
+                }
                 if ((st = scratch(ctx, "g_key", 3 * 8, &p)) != AS_OK) return st;
                 GA.gkey = (unsigned long long *)p;
                 CUDA_TRY(cudaMemsetAsync(p, 0xFF, 3 * 8, ctx->stream));

@@ -237,12 +237,20 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     unsigned long long *gkey = GA.gkey;   // [3], all KEY_NONE at launch
 
     int it = 0;
+    // per-iteration device latency by phase (AS_OPT_PHASE_TIMES): thread 0 of CTA 0 reads %globaltimer
+    // at the phase boundaries -- its own tiles, waiting for the CTA's other warps, CTA reduction + grid
+    // barrier (+ rank exchange), apply -- and the sums go to GA.phase_ns at the end
+    const bool ph = GA.phase_ns && blockIdx.x == 0 && tid == 0;
+    unsigned long long ph_sum[4] = {0, 0, 0, 0}, ph_t = 0, ph_u = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
+        if (ph) ph_t = globaltimer_ns();
         uint64_t kmin = score_tiles<TABU, FULL, TR>(SC, M, R, GT, GA.tlo, GA.thi, gwarp, nwarps_all, it, cur, best, lane);
         kmin = wmin(kmin);
+        if (ph) { ph_u = globaltimer_ns(); ph_sum[0] += ph_u - ph_t; ph_t = ph_u; }
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
+        if (ph) { ph_u = globaltimer_ns(); ph_sum[1] += ph_u - ph_t; ph_t = ph_u; }
         uint64_t kcta = KEY_NONE;
         if (warp == 0) {   // CTA minimum by one warp (parallel loads + shuffles, not a serial loop)
             kcta = wmin(lane < nwarps ? red[lane] : KEY_NONE);
@@ -261,6 +269,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             if (one) __syncthreads();
             else grid.sync();
         }
+        if (ph) { ph_u = globaltimer_ns(); ph_sum[2] += ph_u - ph_t; ph_t = ph_u; }
         if (warp == 0) {
             // apply (every CTA, identical arithmetic): lane 0 splits the delta (from the key: the
             // scorers proved the move valid and feasible), relinks and updates the route totals and
@@ -313,9 +322,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
         }
         __syncthreads();
+        if (ph) ph_sum[3] += globaltimer_ns() - ph_t;
         if (ctrl[0]) break;
         if (ctrl[1] && blockIdx.x == 0)
             for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
+    }
+    if (ph) {
+        for (int k = 0; k < 4; k++) GA.phase_ns[k] = ph_sum[k];
+        GA.phase_ns[4] = (unsigned long long)it;
     }
     if (blockIdx.x == 0 && tid == 0) {
         as_run_result *res = A.results;

@@ -87,6 +87,7 @@ struct GridArgs {
     unsigned long long xr_timeout_ns;   // bound on the wait for the peers' keys
     ncclWindow_t xr_win;           // symmetric window: [3][nranks] {key, tag} u64 pairs
     unsigned long long *gkey2;     // [3] the all-ranks winner per slot
+    unsigned long long *phase_ns;  // [5] per-phase latency sums of CTA 0 + iterations (AS_OPT_PHASE_TIMES), or null
 };
 
 // Sharded single-instance run (shard.cu): replica state in global memory.

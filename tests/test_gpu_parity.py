@@ -763,3 +763,20 @@ def test_jobs_and_greedy_degenerate(A, ctx, oracle_mod):
         for r in range(3):
             o = O.search(p, m, mode=1, tenure=3, max_iters=50, seed=3 * j + r + 1, kick=2)
             assert res[3 * j + r]["best_obj"] == o["best_obj"] and res[3 * j + r]["iters_done"] == o["iters_done"]
+
+
+@pytest.mark.parametrize("cfg,iters", [("ontario", 300), ("large", 40)])
+def test_grid_phase_times(A, ctx, oracle_mod, cfg, iters, ctxopt):
+    """AS_OPT_PHASE_TIMES: the whole-GPU kernel's per-iteration latency breakdown (CTA 0, %globaltimer)
+    covers every iteration, sums to about the kernel time, and leaves the trace unchanged."""
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    ctxopt(PHASE_TIMES=1, GRID=1)
+    g = _compare_run(A, ctx, O, h, p, m, 1, 10, iters)
+    ph = ctx.grid_phases()
+    assert ph["iterations"] == g["iters_done"] == iters
+    per_it = ph["own_tiles_us"] + ph["cta_wait_us"] + ph["reduce_barrier_us"] + ph["apply_us"]
+    assert 0 < per_it * iters / 1e3 <= ctx.last_kernel_ms * 1.05
+    assert min(ph["own_tiles_us"], ph["reduce_barrier_us"], ph["apply_us"]) > 0
