@@ -727,9 +727,11 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     // V <= 32 (tabu bits), bounded tenure (tabu-write ring), not the sweep
     bool win = (P->move_mask & 15u) == 15u && tbytes == 2 && I->tdmax <= 65535 && V <= 32 && !P->sweep &&
                (!tabu || P->tenure <= WIN_MAX_TENURE) && opt_int(ctx, AS_OPT_WINDOW, 1) == 1 &&
-               WIN_P_OK;
+               WIN_P_OK && !I->no_wait;
     size_t sh_b = 0, run_b = 0;
-    batch_smem(n, V, I->NL, I->NC, tbytes, ebytes, tabu, &sh_b, &run_b, win, P->tenure, I->tsym != 0);
+    // the no-wait variant's batched kernel keeps int32 expiries and per-slot arrival/slack records
+    batch_smem(n, V, I->NL, I->NC, tbytes, I->no_wait ? 4 : ebytes, tabu, &sh_b, &run_b, win, P->tenure,
+               I->tsym != 0, I->no_wait != 0);
     int rpc_fit = run_b > 0 && sh_b < ctx->max_smem ? (int)((ctx->max_smem - sh_b) / run_b) : 0;
     if (win) {   // the window path stages more per CTA (node-cost tables): keep it only if it still fits the runs
         const int need = (int)std::min<int64_t>(28, ((int64_t)n_runs + ctx->n_sm - 1) / ctx->n_sm);
@@ -743,12 +745,16 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             rpc_fit = fit0;
         }
     }
-    // the compact-layout kernels (k_batch, k_grid) score the waiting model only;
-    // the no-wait variant (f3) runs on k_search
-    const bool compact_ok = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest && !I->no_wait;
+    // the compact layout (k_batch, k_grid); the no-wait variant (f3) has the batched kernel (exact
+    // per-move evaluation, one run per warp) and, for single runs, the per-CTA kernel k_search
+    const bool compact_fits = I->NL <= 65535 && S <= 65535 && V <= 32767 && I->NC <= 2 && !digest;
+    const bool compact_ok = compact_fits && !I->no_wait;
     if (P->sweep && I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sweep mode (f1) is not built for the no-wait variant");
     const int want_batch = opt_int(ctx, AS_OPT_BATCH_KERNEL, -1);
-    bool use_batch = compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single) || P->sweep);
+    // no-wait batches stay on k_search unless asked for (one run per warp measured slower there:
+    // 4.3e10 vs 6.0e10 move evals/s at 4096 C3 runs, profiles/r02/README.md)
+    bool use_batch = (compact_ok && rpc_fit >= 1 && (want_batch == 1 || (want_batch == -1 && !single) || P->sweep)) ||
+                     (compact_fits && I->no_wait && rpc_fit >= 1 && want_batch == 1);
     if (P->sweep && !use_batch)
         return fail(AS_ERR_UNSUPPORTED, "the sweep mode runs on the batched kernel (compact layout required)");
     // single large instances: one persistent cooperative grid (k_grid)
@@ -817,22 +823,25 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 }
                 // rows per tile: the tiles go round-robin over the warps, so an iteration costs about
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
-                // overhead), the larger G on ties.  A global table caps G at 8 so a row group's table rows
+                // set-up of ~1.5 rows: measured G sweep, profiles/r02/grid_g_sweep_compact.jsonl), the
+                // larger G on ties.  A global table caps G at 8 so a row group's table rows
                 // (~3.4 KB per row at C5) stay L1-resident for the CTA (measured: DESIGN.md §7).
                 const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS * (xr ? xr->nranks : 1);
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
                 const int gmax = GA.T_smem ? 256 : 8;
                 double best_cost = 1e300;
                 GA.G = 1;
+                GA.compact = xr ? 0 : 1;   // one GPU: tile list without the empty swap tiles (score.cuh)
                 for (int g = 1; g <= gmax && g <= std::max(1, n); g++) {
-                    const int64_t tiles = (nTC + nSC) * ((n + g - 1) / g) + nAdj;
+                    const int64_t tiles = GA.compact ? (int64_t)grid_tile_count_compact(n, V, g)
+                                                     : (nTC + nSC) * ((n + g - 1) / g) + nAdj;
                     const int64_t rounds = (tiles + warps_all - 1) / warps_all;
-                    const double cost = (double)rounds * g + 0.3 * (double)rounds;
+                    const double cost = (double)rounds * g + 1.5 * (double)rounds;   // per-tile set-up ~1.5 rows
                     if (cost <= best_cost) { best_cost = cost; GA.G = g; }
                 }
                 GA.G = std::max(1, opt_int(ctx, AS_OPT_GRID_G, GA.G));
                 GA.tlo = 0;
-                GA.thi = grid_tile_count(n, V, GA.G);
+                GA.thi = GA.compact ? grid_tile_count_compact(n, V, GA.G) : grid_tile_count(n, V, GA.G);
                 if (xr) {   // this rank's slice of the tile list (same weighted plan as the sharded kernels)
                     shard_plan(n, V, GA.G, xr->nranks, xr->rank, &GA.tlo, &GA.thi, nullptr, nullptr);
                     GA.xr = 1;

@@ -35,7 +35,7 @@ constexpr int MAXTHREADS = 896;    // <= 28 runs per CTA (one wave of 4096 runs 
 // holds the tabu bits TB[n], the ring of the last tenure + 1 iterations' tabu writes and the
 // warp's window buffer instead.
 __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
-                                                   bool win = false, int tenure = 0, bool tsym = true) {
+                                                   bool win = false, int tenure = 0, bool tsym = true, bool nw = false) {
     BatchLayout L;
     const int S = n + V;
     const int NLp = padded_stride(NL, tbytes);
@@ -63,13 +63,14 @@ __host__ __device__ inline BatchLayout batch_layout(int n, int V, int NL, int NC
     L.TB = r; r = al16(r + (win && tabu ? n * 4 : 0));
     L.RG = r; r = al16(r + (win && tabu ? 2 * (tenure + 1) * 4 : 0));
     L.WB = r; r = al16(r + (win ? WIN_ROWS * WIN_REC_INT4 * 16 : 0));
+    L.NR = r; r = al16(r + (nw ? S * 16 : 0));
     L.run_bytes = r;
     return L;
 }
 
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes, bool win, int tenure, bool tsym) {
-    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure, tsym);
+                size_t *run_bytes, bool win, int tenure, bool tsym, bool nw) {
+    BatchLayout L = batch_layout(n, V, NL, NC, tbytes, ebytes, tabu, win, tenure, tsym, nw);
     *shared_bytes = L.shared_bytes;
     *run_bytes = L.run_bytes;
 }
@@ -77,10 +78,13 @@ void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu,
 // One CTA of the batched executor: stage A.inst, then run this CTA's runs
 // cta_run0 .. cta_run0 + RPC - 1 (one per warp; A's per-run arrays are indexed by
 // that run number).
-template <bool TABU, class TT, class ET, bool FULL, bool WIN>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN, bool NW = false>
 __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const BatchLayout &L, int NLp, int cta_run0) {
-    // WIN: the window scorers (every move kind); FULL then selects their positive-leg (svcpos) form
+    // WIN: the window scorers (every move kind); FULL then selects their positive-leg (svcpos) form.
+    // NW: the no-wait variant (f3, reading #40) -- every move scored by the engine's exact
+    // no-wait evaluation (arrival shifts against suffix slacks; intra-route stretches walked).
     static_assert(!WIN || (sizeof(TT) == 2 && sizeof(ET) == 4), "window scorers: uint16 table, int32 E");
+    static_assert(!NW || (!WIN && !FULL), "the no-wait variant runs the general per-move evaluation");
     extern __shared__ __align__(16) unsigned char smem[];
     const DevInst &I = A.inst;
     const int n = I.n, V = I.V, S = n + V, NC = I.NC, NL = I.NL;
@@ -155,6 +159,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     R.succ.base = rb + L.LK; R.pred.base = rb + L.LK;
     R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
     R.pick_s.base = CS; R.w_s.base = CS;
+    R.arr.base = R.sl.base = R.pos.base = NW ? rb + L.NR : nullptr;
     R.F = F; R.E = E;
     CompactRV<ET> R0 = R;   // evaluation view: the window path takes tabu from TB, not from E in global memory
     if (WIN) R0.E = nullptr;
@@ -190,10 +195,18 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     bad = __any_sync(0xFFFFFFFFu, bad);
     __syncwarp();
     if (!bad) {
-        for (int x = lane; x < S; x += 32) {
+        if constexpr (NW) {   // whole routes: arrivals, positions, suffix slacks (engine.cuh)
+            for (int x = lane; x < n; x += 32)
+                if (R.veh[x] < 0) bad = 1;                                          // unlisted => duplicate
+            bad = __any_sync(0xFFFFFFFFu, bad);
+            if (!bad)
+                for (int v = lane; v < V; v += 32) nw_refresh_route(M, R, v);
+            __syncwarp();
+        }
+        for (int x = lane; x < S && !bad; x += 32) {
             if (x < n && R.veh[x] < 0) { bad = 1; continue; }   // unlisted => a duplicate elsewhere
-            refresh_slot(M, R, x);
-            if (R.depc[x] + R.inc[x] > R.w_s[x]) bad = 1;                          // con7/con8
+            if (!NW) refresh_slot(M, R, x);
+            if (R.depc[x] + R.inc[x] > R.w_s[x]) bad = 1;                          // con7/con8 (no-wait: arrival)
             if (x < n && MH[x] && !M.hok(M.cls(R.veh[x]))) bad = 1;              // con9
         }
         bad = __any_sync(0xFFFFFFFFu, bad);
@@ -234,9 +247,9 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
             for (int k = 0; k < A.kick; k++)
                 for (int tr = 0; tr < 64; tr++) {
                     uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
-                    MoveEval e = eval_index(M, R0, idx, 0xFu, 0);
+                    MoveEval e = eval_index<NW>(M, R0, idx, 0xFu, 0);
                     if (e.valid && e.feasible) {
-                        apply_move(M, R, idx, e, 0, 0, false);
+                        apply_move<NW>(M, R, idx, e, 0, 0, false);
                         kicks++;
                         break;
                     }
@@ -379,6 +392,31 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
             }
         }
 
+        if constexpr (NW) {
+            // no-wait: every move by the engine's exact evaluation -- relocate rows (m warp-uniform,
+            // lanes over target slots), then swap rows (lanes over m2 > m1); adjacent pairs included
+            for (int m = 0; m < n; m++) {
+                const RelocRow r = reloc_row(M, R0, m);
+                if (r.a < 0) continue;
+                for (int t = lane; t < S; t += 32) {
+                    const MoveEval e = reloc_eval<true>(M, R0, r, m, t, mask, it);
+                    const int cls = move_class<TABU>(e, cur, best);
+                    if (cls >= 0) {
+                        const uint64_t key = make_key(cls, e.delta, (uint32_t)m * (uint32_t)S + (uint32_t)t);
+                        kmin = key < kmin ? key : kmin;
+                    }
+                }
+            }
+            for (int m1 = 0; m1 + 1 < n; m1++)
+                for (int m2 = m1 + 1 + lane; m2 < n; m2 += 32) {
+                    const MoveEval e = swap_eval<true>(M, R0, m1, m2, mask, it);
+                    const int cls = move_class<TABU>(e, cur, best);
+                    if (cls >= 0) {
+                        const uint64_t key = make_key(cls, e.delta, Rb + (uint32_t)m1 * (uint32_t)n + (uint32_t)m2);
+                        kmin = key < kmin ? key : kmin;
+                    }
+                }
+        } else {
         // Per-lane best inside a tile (score.cuh); tiles merged through the 64-bit key.
         // ============================ relocate block ============================
         for (int t0 = 0; t0 < S; t0 += 32 * KR) {
@@ -417,6 +455,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
                 }
             }
         }
+        }   // !NW
 
         // ============================ select + apply ============================
         kmin = wmin(kmin);
@@ -426,7 +465,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
             else if (key_cls(kmin) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
             if (!stop) {
                 const uint32_t idx = key_idx(kmin);
-                MoveEval e = eval_index(M, R0, idx, mask, it);
+                MoveEval e = eval_index<NW>(M, R0, idx, mask, it);
                 if (WIN && TABU) {
                     // the 'from' pairs this move writes (O8): relocate (m, veh m); swap (m1, veh m1), (m2, veh m2)
                     uint32_t p0, p1 = 0xFFFFFFFFu;
@@ -446,7 +485,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
                         if (p1 != 0xFFFFFFFFu) TB[p1 & 0xFFFF] |= 0x80000000u >> (p1 >> 16);
                     }
                 }
-                apply_move(M, R, idx, e, it, A.tenure, TABU);
+                apply_move<NW>(M, R, idx, e, it, A.tenure, TABU);
                 cur += e.delta;
                 if (cur < best) {
                     best = cur;
@@ -501,9 +540,9 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
         for (int i = lane; i < n * V; i += 32) A.tabu_out[(size_t)run * n * V + i] = (int32_t)E[i];
 }
 
-template <bool TABU, class TT, class ET, bool FULL, bool WIN>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN, bool NW = false>
 __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch(SearchArgs A, int RPC, BatchLayout L, int NLp) {
-    batch_cta<TABU, TT, ET, FULL, WIN>(A, RPC, L, NLp, blockIdx.x * RPC);
+    batch_cta<TABU, TT, ET, FULL, WIN, NW>(A, RPC, L, NLp, blockIdx.x * RPC);
 }
 
 // Several instances in one launch (as_batch_run_jobs): CTA b runs cta[b] = {job, first run
@@ -531,13 +570,14 @@ __global__ void __launch_bounds__(MAXTHREADS, 1) k_batch_jobs(SearchArgs A, cons
     batch_cta<TABU, TT, ET, FULL, WIN>(B, J.RPC, J.L, J.NLp, 0);
 }
 
-template <bool TABU, class TT, class ET, bool FULL, bool WIN = false>
+template <bool TABU, class TT, class ET, bool FULL, bool WIN = false, bool NW = false>
 static cudaError_t launch_one(const SearchArgs &A, int RPC, size_t smem, cudaStream_t st) {
-    auto kern = k_batch<TABU, TT, ET, FULL, WIN>;
+    auto kern = k_batch<TABU, TT, ET, FULL, WIN, NW>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     const DevInst &I = A.inst;
-    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU, WIN, A.tenure, I.tsym);
+    BatchLayout L = batch_layout(I.n, I.V, I.NL, I.NC, (int)sizeof(TT), (int)sizeof(ET), TABU, WIN, A.tenure, I.tsym,
+                                 NW);
     int NLp = padded_stride(I.NL, (int)sizeof(TT));
     int grid = (A.n_runs + RPC - 1) / RPC;
     kern<<<grid, RPC * 32, smem, st>>>(A, RPC, L, NLp);
@@ -584,6 +624,13 @@ BatchLayout batch_layout_host(int n, int V, int NL, int NC, int tbytes, int ebyt
 
 cudaError_t launch_batch(const SearchArgs &A, int mode, int RPC, int tbytes, int ebytes, size_t smem,
                          cudaStream_t st, bool win) {
+    if (A.inst.no_wait) {   // f3: general evaluation, int32 expiries
+        if (tbytes == 2)
+            return mode == 1 ? launch_one<true, uint16_t, int32_t, false, false, true>(A, RPC, smem, st)
+                             : launch_one<false, uint16_t, int32_t, false, false, true>(A, RPC, smem, st);
+        return mode == 1 ? launch_one<true, int32_t, int32_t, false, false, true>(A, RPC, smem, st)
+                         : launch_one<false, int32_t, int32_t, false, false, true>(A, RPC, smem, st);
+    }
     const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     if (win) {   // window scorers: uint16 table, tabu matrix in global memory (int32); positive legs or general
         if (A.inst.svcpos)

@@ -49,6 +49,7 @@ __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, 
     L.F = o; o = al16(o + V * 4);
     L.E = o; o = al16(o + (tabu && E_smem ? n * V * ebytes : 0));
     L.red = o; o = al16(o + 32 * 8 + 64);
+    L.SP = o; o = al16(o + (n / 1 + 2) * 4);   // compact swap-tile prefix (<= nRG + 1 <= n + 1 entries)
     L.total = o;
     return L;
 }
@@ -227,7 +228,19 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
-    const GridTiles GT = grid_tiles(n, V, GA.G);
+    GridTiles GT = grid_tiles(n, V, GA.G);
+    if (GA.compact) {   // single GPU: the swap tiles below the diagonal are left out of the list
+        int *SP = reinterpret_cast<int *>(smem + L.SP);
+        if (tid == 0) {
+            int c = 0;
+            for (int g = 0; g < GT.nRG; g++) { SP[g] = c; c += swap_chunks_of_group(n, GT.nSC, GT.G, g); }
+            SP[GT.nRG] = c;
+        }
+        __syncthreads();
+        GT.swp = SP;
+        GT.n_swap = SP[GT.nRG];
+        GT.n_total = GT.n_reloc + GT.n_swap + GT.nAdj;
+    }
     // tile -> warp: CTA-major (consecutive tiles = the same row group on one CTA: the table rows
     // of that group are shared in L1) when the tiles fill the grid; spread over the CTAs first when
     // there are fewer tiles than warps, so every SM scores at most ~one tile (latency-bound sizes)

@@ -49,6 +49,7 @@ struct BatchLayout {
     int shared_bytes;
     int RS, LK, BS, F, E, PM, SN;   // per-run part (offsets inside a run block); PM/SN: sweep order (f1)
     int TB, RG, WB;                 // window scorers: tabu bits, tabu-write ring, window buffer
+    int NR;                         // no-wait variant: per-slot {arrival, suffix slack, position} records
     int run_bytes;
 };
 
@@ -64,7 +65,7 @@ struct BatchJob {
 };
 
 struct GridLayout {
-    int T, CS, MH, VC, CH, RS, LK, F, E, red, total;   // shared-memory byte offsets per CTA
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, SP, total;   // shared-memory byte offsets per CTA
 };
 
 struct GridArgs {
@@ -79,6 +80,7 @@ struct GridArgs {
     unsigned long long *gkey;      // [3] triple-buffered grid-wide key, KEY_NONE at launch
     int G;                         // rows per tile
     int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
+    int compact;                   // 1: the list without empty swap tiles (single GPU; score.cuh GridTiles::swp)
     // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
     // and a tag into every peer's symmetric window slot over NVLink and waits (bounded) for the
     // peers' tags of this iteration in its own window (grid.cu rank_exchange)
@@ -116,6 +118,7 @@ cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_
 void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
                 int64_t *weight_rank);
 int grid_tile_count(int n, int V, int G);
+int grid_tile_count_compact(int n, int V, int G);
 
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
@@ -131,7 +134,7 @@ cudaError_t launch_eval_dump(const DevInst &I, const RunViewG &G, int mode, int 
                              int n_sm, cudaStream_t st);
 cudaError_t launch_search(const SearchArgs &A, int mode, int n_runs, int threads, size_t smem, cudaStream_t st);
 void batch_smem(int n, int V, int NL, int NC, int tbytes, int ebytes, bool tabu, size_t *shared_bytes,
-                size_t *run_bytes, bool win = false, int tenure = 0, bool tsym = true);
+                size_t *run_bytes, bool win = false, int tenure = 0, bool tsym = true, bool nw = false);
 // win: the WINDOW scorers (window.cuh): every move kind, svcpos, uint16 table, V <= 32, tenure <= WIN_MAX_TENURE,
 // not the sweep; the tabu matrix is SearchArgs::E_global ([R][n][V] int32)
 constexpr int WIN_MAX_TENURE = 64;

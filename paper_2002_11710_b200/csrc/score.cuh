@@ -567,7 +567,17 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
 struct GridTiles {
     int nTC, nSC, nAdj, nRG, G;   // t-chunks, swap chunks, adjacent tiles, row groups, rows per group
     int n_reloc, n_swap, n_total; // tile counts
+    const int *swp;               // compact swap list (non-empty tiles only): swp[g] = first compact swap tile
+                                  // of row group g, g = 0..nRG (a prefix over the chunk counts); null = full list
 };
+
+// Swap chunks j of row group g holding a pair m1 < m2 (hi = n - 64 j > m_lo + 1): the non-empty ones.
+__host__ __device__ inline int swap_chunks_of_group(int n, int nSC, int G, int g) {
+    const int m_lo = g * G, span = n - 1 - m_lo;
+    if (span <= 0) return 0;
+    const int c = (span + 32 * KS - 1) / (32 * KS);
+    return c < nSC ? c : nSC;
+}
 
 __host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
     GridTiles T;
@@ -580,7 +590,17 @@ __host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
     T.n_reloc = T.nTC * T.nRG;
     T.n_swap = T.nSC * T.nRG;
     T.n_total = T.n_reloc + T.n_swap + T.nAdj;
+    T.swp = nullptr;
     return T;
+}
+
+// The same list without the swap tiles that lie entirely on or below the diagonal (every row of the group
+// at or above the chunk's top): the whole-GPU kernel's tile list on one GPU (fewer, more even tiles per warp).
+__host__ __device__ inline int compact_swap_count(int n, int V, int G) {
+    const GridTiles T = grid_tiles(n, V, G);
+    int c = 0;
+    for (int g = 0; g < T.nRG; g++) c += swap_chunks_of_group(n, T.nSC, G, g);
+    return c;
 }
 
 // One tile of the flat tile list: this lane's best packed key in it.
@@ -599,7 +619,19 @@ __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const
                       : score_reloc<TABU, FULL, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
         } else if (tile < GT.n_reloc + GT.n_swap) {
             const int r = tile - GT.n_reloc;
-            const int j = r % GT.nSC, g = r / GT.nSC;
+            int j, g;
+            if (GT.swp) {   // compact list: the row group by binary search over the prefix, then the chunk
+                int lo_g = 0, hi_g = GT.nRG;   // swp[lo_g] <= r < swp[hi_g]
+                while (hi_g - lo_g > 1) {
+                    const int mid = (lo_g + hi_g) >> 1;
+                    if (GT.swp[mid] <= r) lo_g = mid; else hi_g = mid;
+                }
+                g = lo_g;
+                j = r - GT.swp[g];
+            } else {
+                j = r % GT.nSC;
+                g = r / GT.nSC;
+            }
             const int hi = n - j * 32 * KS;
             const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
             if (m_lo < m_hi)

@@ -329,6 +329,10 @@ cudaError_t launch_batch_best(const as_run_result *res, int n_runs, int64_t run_
 
 // Tile weights (scored moves per tile, approximately) for the rank split.
 int grid_tile_count(int n, int V, int G) { return grid_tiles(n, V, G).n_total; }
+int grid_tile_count_compact(int n, int V, int G) {
+    const GridTiles T = grid_tiles(n, V, G);
+    return T.n_reloc + compact_swap_count(n, V, G) + T.nAdj;
+}
 
 void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, int64_t *weight_total,
                 int64_t *weight_rank) {

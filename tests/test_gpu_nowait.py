@@ -201,3 +201,43 @@ def test_nowait_unsupported_paths(A, ctx, oracle_mod, monkeypatch, ctxopt):
     with pytest.raises(A.AirschedError) as e:
         A.as_tabu_run(ctx, h, p, m, A.params(mode=1, tenure=3, max_iters=10))
     assert e.value.status == A.AS_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("cfg,scale,iters", [("tiny", 1.0, 200), ("tiny", 0.3, 200), ("ontario", 1.0, 800),
+                                             ("batched", 0.5, 400), ("ontario", 0.6, 600)])
+def test_nowait_batch_kernel_single_runs(A, ctx, oracle_mod, cfg, scale, iters, ctxopt):
+    """f3 on the batched kernel (one run per warp, exact no-wait evaluation of every move):
+    single runs forced onto it -- full traces, final tabu matrix, best schedule, TS (plain and
+    kicked) and NS, against the oracle."""
+    ctxopt(BATCH_KERNEL=1)
+    inst = nowait(cfg, scale)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    st, (p, m), _, _ = O.greedy()
+    assert st == 0
+    t = instgen.CONFIGS[cfg].tenure
+    _compare_run(A, ctx, O, h, p, m, 1, t, iters)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    _compare_run(A, ctx, O, h, p, m, 1, t, iters // 2, seed=17, kick=8)
+
+
+def test_nowait_batch_kernel_traces(A, ctx, oracle_mod, ctxopt):
+    """A whole no-wait batch on the batched kernel (option BATCH_KERNEL=1; the default for no-wait
+    batches is the per-run kernel): per-run traces of sampled runs equal the oracle's."""
+    ctxopt(BATCH_KERNEL=1)
+    inst = nowait("ontario", 0.7)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    st, (p, m), _, _ = O.greedy()
+    R, iters = 96, 300
+    seeds = np.arange(1, R + 1, dtype=np.uint64)
+    res = np.zeros(R, A.RESULT_DTYPE)
+    tr = np.zeros((R, iters), A.TRACE_DTYPE)
+    for mode, tenure in ((1, 10), (0, 0)):
+        prm = A.params(mode=mode, tenure=tenure, max_iters=iters, kick=6, trace_level=1)
+        A.as_batch_run(ctx, h, R, p, m, prm, seeds, shared_start=True, results=res, trace_out=tr)
+        for r in (0, 31, 32, 95):
+            o = O.search(p, m, mode=mode, tenure=tenure, max_iters=iters, seed=int(seeds[r]), kick=6)
+            k = o["iters_done"]
+            assert res[r]["iters_done"] == k and res[r]["best_obj"] == o["best_obj"]
+            assert (tr[r]["idx"][:k] == o["trace"]["idx"]).all() and (tr[r]["cur"][:k] == o["trace"]["cur"]).all()
