@@ -277,6 +277,12 @@ struct GridXr {
 
 constexpr int64_t OPT_UNSET = INT64_MIN;
 
+// An as_ctx_set_option override, or the automatic choice dflt.
+static int opt_int(const as_ctx *ctx, int option, int dflt) {
+    const int64_t v = ctx->opt[option];
+    return v == OPT_UNSET ? dflt : (int)v;
+}
+
 #define NCCL_TRY(expr)                                                                              \
     do {                                                                                            \
         ncclResult_t _r = (expr);                                                                   \
@@ -448,6 +454,23 @@ static as_status get_dev_inst(as_ctx *ctx, const as_instance *I, const DevInst *
             CUDA_TRY(launch_pad_table(D.d.T, tt, I->NC, I->NL, NLp, D.tpad_bytes, true, s));
             ctx->launches++;
             D.d.TpadT = tt;
+        }
+    }
+    // node costs for the global-table scorers (score.cuh): only when the table is too large for
+    // shared memory (it is then read from global memory) and every node cost fits 16 bits
+    D.d.TDg = nullptr;
+    {
+        const int NLp = padded_stride_host(I->NL, D.tpad_bytes);
+        const size_t tsm = (size_t)I->NC * I->NL * NLp * D.tpad_bytes;
+        if (D.tpad_bytes == 2 && I->tdmax <= 65535 && tsm > ctx->max_smem_hw / 2 && I->n > 0 &&
+            opt_int(ctx, AS_OPT_NODE_COSTS, 1) == 1) {
+            void *td = nullptr;
+            const size_t bytes = (size_t)I->NC * I->NL * (I->n + I->V) * 2 + 16;
+            CUDA_TRY(cudaMalloc(&td, bytes));
+            D.allocs.push_back(td);
+            CUDA_TRY(launch_build_td(D.d.T, D.d.pick, D.d.del, D.d.vloc, (uint16_t *)td, I->n, I->V, I->NL, I->NC, s));
+            ctx->launches++;
+            D.d.TDg = (const uint16_t *)td;
         }
     }
     auto &slot = ctx->insts[I];
@@ -635,11 +658,6 @@ static as_status pick_layout(as_ctx *ctx, const as_instance *I, bool tabu, int *
     return fail(AS_ERR_UNSUPPORTED, "instance too large for the per-CTA persistent kernel (n=%d, V=%d)", n, V);
 }
 
-// An as_ctx_set_option override, or the automatic choice dflt.
-static int opt_int(const as_ctx *ctx, int option, int dflt) {
-    const int64_t v = ctx->opt[option];
-    return v == OPT_UNSET ? dflt : (int)v;
-}
 
 // The window scorers' general-leg form blocks a row whose removal leaves route a over the
 // flight limit by adding NEG (-2^29) to P - F_b (window.cuh win_reloc_record): exact only while

@@ -47,6 +47,8 @@ struct DevInst {
     int32_t svcpos;          // every pickup->delivery leg > 0 in every class (enables the FAST scorers)
     int32_t tsym;            // every layer of T is symmetric (the transposed table is T itself)
     const void *TpadT;       // padded table transposed per layer (== the padded table when tsym)
+    const uint16_t *TDg;     // node costs TD[c][x][t] = T_c[x][pick_t] + svc_c(t) (END slots: T_c[x][base]),
+                             // rows of n + V, uint16, in global memory for the global-table scorers; or null
 };
 
 // Selection key (O9): class bit 63, biased delta bits 62..32, index bits 31..0.

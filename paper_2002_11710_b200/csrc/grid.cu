@@ -31,6 +31,7 @@
 namespace cg = cooperative_groups;
 
 constexpr int GRID_THREADS = airsched::GRID_WARPS * 32;
+constexpr int GRID_SWT_MAX = 4096;   // compact swap tiles held as a table in shared memory (16 KB)
 
 namespace airsched {
 
@@ -49,7 +50,12 @@ __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, 
     L.F = o; o = al16(o + V * 4);
     L.E = o; o = al16(o + (tabu && E_smem ? n * V * ebytes : 0));
     L.red = o; o = al16(o + 32 * 8 + 64);
-    L.SP = o; o = al16(o + (n / 1 + 2) * 4);   // compact swap-tile prefix (<= nRG + 1 <= n + 1 entries)
+    // compact swap tiles: the prefix over the row groups (<= n + 1 entries) and, when the list is short
+    // (<= GRID_SWT_MAX tiles), the tile table itself (no search per tile)
+    const int nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
+    L.SP = o; o = al16(o + (n + 2) * 4);
+    const int64_t nst = (int64_t)nSC * n;
+    L.ST = o; o = al16(o + (int)(nst < GRID_SWT_MAX ? nst : GRID_SWT_MAX) * 4);
     L.total = o;
     return L;
 }
@@ -225,12 +231,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     SC.Ts = Ts; SC.Tt = I.tsym ? Ts : reinterpret_cast<const TT *>(I.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
     ET *Et = TABU && !GA.E_smem ? reinterpret_cast<ET *>(GA.Etglobal) : nullptr;
     SC.Et = Et;
+    SC.TD = GA.T_smem ? nullptr : I.TDg;   // node costs for the global-table scorers
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
     GridTiles GT = grid_tiles(n, V, GA.G);
     if (GA.compact) {   // single GPU: the swap tiles below the diagonal are left out of the list
         int *SP = reinterpret_cast<int *>(smem + L.SP);
+        int *ST = reinterpret_cast<int *>(smem + L.ST);
         if (tid == 0) {
             int c = 0;
             for (int g = 0; g < GT.nRG; g++) { SP[g] = c; c += swap_chunks_of_group(n, GT.nSC, GT.G, g); }
@@ -240,6 +248,12 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         GT.swp = SP;
         GT.n_swap = SP[GT.nRG];
         GT.n_total = GT.n_reloc + GT.n_swap + GT.nAdj;
+        if (GT.n_swap <= GRID_SWT_MAX) {
+            for (int g = tid; g < GT.nRG; g += blockDim.x)
+                for (int j = 0; j < SP[g + 1] - SP[g]; j++) ST[SP[g] + j] = (g << 16) | j;
+            __syncthreads();
+            GT.swt = ST;
+        }
     }
     // tile -> warp: CTA-major (consecutive tiles = the same row group on one CTA: the table rows
     // of that group are shared in L1) when the tiles fill the grid; spread over the CTAs first when

@@ -509,6 +509,28 @@ __global__ void k_svc(const int32_t *T, const int32_t *pick, const int32_t *del,
     }
 }
 
+// Node-cost table of the global-table scorers: TD[c][x][t] = T_c[x][pick_t] + T_c[pick_t][del_t] for a
+// mission t, T_c[x][base_v] for the END slot t = n + v (the host checked every entry fits 16 bits).
+__global__ void k_build_td(const int32_t *T, const int32_t *pick, const int32_t *del, const int32_t *vloc,
+                           uint16_t *TD, int n, int V, int NL, int NC) {
+    const int S = n + V;
+    const int64_t total = (int64_t)NC * NL * S;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(i % S), x = (int)((i / S) % NL), c = (int)(i / ((int64_t)S * NL));
+        const int32_t *Tc = T + (int64_t)c * NL * NL;
+        int v;
+        if (t < n) v = Tc[(int64_t)x * NL + pick[t]] + Tc[(int64_t)pick[t] * NL + del[t]];
+        else v = Tc[(int64_t)x * NL + vloc[t - n]];
+        TD[i] = (uint16_t)v;
+    }
+}
+
+cudaError_t launch_build_td(const int32_t *T, const int32_t *pick, const int32_t *del, const int32_t *vloc,
+                            uint16_t *TD, int n, int V, int NL, int NC, cudaStream_t st) {
+    k_build_td<<<1024, 256, 0, st>>>(T, pick, del, vloc, TD, n, V, NL, NC);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
                        cudaStream_t st) {
     if (n == 0) return cudaSuccess;

@@ -65,7 +65,7 @@ struct BatchJob {
 };
 
 struct GridLayout {
-    int T, CS, MH, VC, CH, RS, LK, F, E, red, SP, total;   // shared-memory byte offsets per CTA
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, SP, ST, total;   // shared-memory byte offsets per CTA
 };
 
 struct GridArgs {
@@ -150,6 +150,8 @@ size_t greedy_state_bytes(const DevInst &I);
 cudaError_t launch_greedy(const DevInst &I, int n_starts, int insert_mode, int max_repairs, const uint64_t *seeds,
                           int32_t *order_scratch, int32_t *state_global, int warps, bool T_smem, bool state_smem,
                           int32_t *ptr_out, int32_t *ms_out, int32_t *status_out, int32_t *nrep_out, cudaStream_t st);
+cudaError_t launch_build_td(const int32_t *T, const int32_t *pick, const int32_t *del, const int32_t *vloc,
+                            uint16_t *TD, int n, int V, int NL, int NC, cudaStream_t st);
 cudaError_t launch_svc(const int32_t *T, const int32_t *pick, const int32_t *del, int32_t *svc, int n, int NL, int NC,
                        cudaStream_t st);
 

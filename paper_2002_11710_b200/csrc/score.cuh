@@ -76,6 +76,7 @@ struct ScoreCtx {
     const int32_t *F;      // [V] route flight time
     const ET *E;           // [n][V] tabu expiry (TABU only)
     const ET *Et;          // [V][n] its transpose when E is in global memory (row-local E[m2][a] reads), else null
+    const uint16_t *TD;    // global-table scorers (TR): node costs TD[c][x][t] (DevInst::TDg), else null
     int n, V, S, NL, NLp, P;
     uint32_t Rb, mask;
     int one, neg;          // 1 and -1, opaque to the compiler (see madd)
@@ -324,6 +325,12 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
     int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
     // shared table (TR false): cached offsets are byte addresses in the shared window
     const int tsm = TR ? 0 : (int)__cvta_generic_to_shared(Ts), tsz = TR ? 1 : (int)sizeof(TT);
+    // global table with node costs (TR, uint16): d_b(m, t) = T_cb[del_m][pick_t] + svco(t) is ONE read of
+    // TD_cb row del_m at column t -- consecutive lanes, consecutive slots: a coalesced 64-byte read
+    // instead of a gather over the row
+    const bool td = TR && K16 && C.TD != nullptr;
+    const TT *T2p = td ? reinterpret_cast<const TT *>(C.TD) : Ts;
+    const int tdS = td ? S : NLp;
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
@@ -338,10 +345,11 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
                 cb = vc & 0xFF;
                 t1 = TR ? cb * NL * NLp + (rs.w & 0xFFFF)    // column endc(t) of Tt_cb (row pick_m per m)
                         : tsm + tsz * ((cb * NL + (rs.w & 0xFFFF)) * NLp); // row endc(t) of T_cb (column pick_m)
-                t2 = tsm + tsz * (cb * NL * NLp + (cs.y & 0xFFFF)); // column pick(t) of T_cb (row del_m per m)
+                t2 = td ? cb * NL * S + t                          // column t of TD_cb (row del_m per m)
+                        : tsm + tsz * (cb * NL * NLp + (cs.y & 0xFFFF)); // column pick(t) of T_cb (row del_m per m)
                 dw = -rs.x;                                  // -dep(pred t)
-                kk = rs.z - rs.y;                            // svco(t) - inc(t)
-                wsv = cs.x - rs.z;                           // w(t) - svco(t)
+                kk = td ? -rs.y : rs.z - rs.y;               // svco(t) - inc(t) (TD: svco(t) is in the node cost)
+                wsv = td ? cs.x : cs.x - rs.z;               // w(t) - svco(t)
                 slk = (P - F[bb]) - (((vc >> 8) & 1) ? 0 : (1 << 30));   // heli offset (masked off for non-heli rows)
             }
         }
@@ -367,7 +375,7 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
             if (F[a] + rem > P) continue;         // no feasible relocate of m (reading #42)
             const int4 cm = CS4[m];
             const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : tsz * (cm.y & 0xFFFF),
-                      rowD = tsz * (int)((uint32_t)cm.y >> 16) * NLp;
+                      rowD = tsz * (int)((uint32_t)cm.y >> 16) * tdS;
             const int svm0 = cm.z, dsvm = cm.w - cm.z, wm_neg = -cm.x;
             const int hmask = MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
             const int remasp = TABU ? rem - asp : rem;
@@ -378,7 +386,7 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
             for (int k = 0; k < KR; k++) {
                 // T_cb[endc t][pick m], T_cb[del m][pick t]; shared table: byte addresses
                 const int T1 = TR ? (int)__ldg(&Tt[madd(c_t1[k], one, rowP)]) : lds_t<TT>((uint32_t)madd(c_t1[k], one, rowP));
-                const int T2 = TR ? (int)__ldg(&Ts[madd(c_t2[k], one, rowD)]) : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
+                const int T2 = TR ? (int)__ldg(&T2p[madd(c_t2[k], one, rowD)]) : lds_t<TT>((uint32_t)madd(c_t2[k], one, rowD));
                 const int x1 = madd(c_cb[k], dsvm, madd(T1, one, svm0));              // d(c, m)
                 const int ins = x1 + T2 + c_k[k];
                 const int mA = madd(x1, neg, madd(w_m, one, c_dw[k]));               // dep(c) + d(c,m) <= w_m
@@ -437,6 +445,11 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
     int q_cb[KS];
     // shared table (TR false): offsets are byte addresses in the shared window, the base on one side of each pair
     const int tsm = TR ? 0 : (int)__cvta_generic_to_shared(Ts), tsz = TR ? 1 : (int)sizeof(TT);
+    // global table with node costs (TR, uint16): d_a(p1, m2) = T_ca[endc1][pick2] + svc_ca(m2) is ONE read of
+    // TD_ca row endc1 at column m2 -- consecutive lanes: coalesced
+    const bool td = TR && K16 && C.TD != nullptr;
+    const TT *Tyap = td ? reinterpret_cast<const TT *>(C.TD) : Ts;
+    const int S = n + V, tdS = td ? S : NLp;
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
@@ -452,9 +465,9 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 const int s2 = LK[m2] & 0xFFFF;
                 const int4 rs2 = RS4[s2];
                 const int4 cs2 = CS4[s2];
-                p2m = tsz * (c2.y & 0xFFFF);                      // pick2
-                sv0 = c2.z;
-                dsv = c2.w - c2.z;
+                p2m = td ? m2 : tsz * (c2.y & 0xFFFF);            // pick2 (TD: column m2)
+                sv0 = td ? 0 : c2.z;
+                dsv = td ? 0 : c2.w - c2.z;
                 d2 = TR ? (int)((uint32_t)c2.y >> 16)              // column del2 of Tt (row pick(s1) per m1)
                         : tsz * (int)((uint32_t)c2.y >> 16) * NLp; // row del2 of T (column pick(s1) per m1)
                 e2 = TR ? cb * NL * NLp + (r2.w & 0xFFFF)          // column endc2 of Tt_cb (row pick1 per m1)
@@ -487,7 +500,7 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
             const int4 cs1 = CS4[s1];
             const uint32_t vca = VC[a];
             const int ca = vca & 0xFF;
-            const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * NLp);  // T_ca[endc1][.]
+            const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * tdS);  // T_ca[endc1][.] (TD_ca[endc1][.])
             const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp            // Tt_ca[pick(s1)][.]
                                    : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF)); // T_ca[.][pick(s1)]
             const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : tsz * (c1.y & 0xFFFF);
@@ -512,7 +525,7 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 const int b = bf & 0xFFFF;
                 const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
                 const int a_yb1 = madd(q_e2[k], one, rowp1), a_tb2 = madd(q_p2[k], one, row_tb2);
-                const int Tya1 = TR ? (int)__ldg(&Ts[a_ya1]) : lds_t<TT>((uint32_t)a_ya1);
+                const int Tya1 = TR ? (int)__ldg(&Tyap[a_ya1]) : lds_t<TT>((uint32_t)a_ya1);
                 const int Ta2 = TR ? (int)__ldg(&Tt[a_ta2]) : lds_t<TT>((uint32_t)a_ta2);                  // m2 -> s1
                 const int Tyb1 = TR ? (int)__ldg(&Tt[a_yb1]) : lds_t<TT>((uint32_t)a_yb1);
                 const int Tb2 = TR ? (int)__ldg(&Ts[a_tb2]) : lds_t<TT>((uint32_t)a_tb2);                  // m1 -> s2
@@ -569,6 +582,7 @@ struct GridTiles {
     int n_reloc, n_swap, n_total; // tile counts
     const int *swp;               // compact swap list (non-empty tiles only): swp[g] = first compact swap tile
                                   // of row group g, g = 0..nRG (a prefix over the chunk counts); null = full list
+    const int *swt;               // the same list as a table g << 16 | j per compact swap tile (when it is short), or null
 };
 
 // Swap chunks j of row group g holding a pair m1 < m2 (hi = n - 64 j > m_lo + 1): the non-empty ones.
@@ -591,6 +605,7 @@ __host__ __device__ inline GridTiles grid_tiles(int n, int V, int G) {
     T.n_swap = T.nSC * T.nRG;
     T.n_total = T.n_reloc + T.n_swap + T.nAdj;
     T.swp = nullptr;
+    T.swt = nullptr;
     return T;
 }
 
@@ -620,7 +635,11 @@ __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const
         } else if (tile < GT.n_reloc + GT.n_swap) {
             const int r = tile - GT.n_reloc;
             int j, g;
-            if (GT.swp) {   // compact list: the row group by binary search over the prefix, then the chunk
+            if (GT.swt) {   // compact list, short: direct table
+                const int e = GT.swt[r];
+                g = e >> 16;
+                j = e & 0xFFFF;
+            } else if (GT.swp) {   // compact list: the row group by binary search over the prefix, then the chunk
                 int lo_g = 0, hi_g = GT.nRG;   // swp[lo_g] <= r < swp[hi_g]
                 while (hi_g - lo_g > 1) {
                     const int mid = (lo_g + hi_g) >> 1;

@@ -780,3 +780,20 @@ def test_grid_phase_times(A, ctx, oracle_mod, cfg, iters, ctxopt):
     per_it = ph["own_tiles_us"] + ph["cta_wait_us"] + ph["reduce_barrier_us"] + ph["apply_us"]
     assert 0 < per_it * iters / 1e3 <= ctx.last_kernel_ms * 1.05
     assert min(ph["own_tiles_us"], ph["reduce_barrier_us"], ph["apply_us"]) > 0
+
+
+def test_global_node_cost_table(A, oracle_mod):
+    """C5's table is read from global memory; with the node-cost table TD[c][x][t] (default) one gather of
+    each relocate and swap becomes a coalesced row read.  A context without it (AS_OPT_NODE_COSTS=0,
+    set before the upload) must give the same trace, and both equal the oracle's."""
+    inst = instgen.generate("surge")
+    O = oracle_mod.Oracle(inst)
+    p, m = start_of(O, inst)
+    out = []
+    for node_costs in (1, 0):
+        c = A.Ctx(0)
+        c.set_option("NODE_COSTS", node_costs)
+        h = A.Instance(inst)
+        c.upload(h)
+        out.append(_compare_run(A, c, O, h, p, m, 1, 10, 4))
+    assert (out[0]["trace"]["idx"] == out[1]["trace"]["idx"]).all()
