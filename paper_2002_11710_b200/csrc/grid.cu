@@ -108,7 +108,10 @@ __device__ __forceinline__ uint64_t rank_exchange(const GridArgs &GA, int q, int
 }
 
 // TR: the table is read from global memory (row-local reads, score.cuh).
-template <bool TABU, class TT, class ET, bool FULL, bool TR>
+// PH: the per-iteration phase timers (AS_OPT_PHASE_TIMES) -- a separate instantiation, because even
+// untaken, their live accumulators cost the production kernel ~8 % on C1/C2/C4 (register pressure;
+// profiles/r02/kgrid_phase_ab.jsonl).
+template <bool TABU, class TT, class ET, bool FULL, bool TR, bool PH>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     // per-iteration device latency by phase (AS_OPT_PHASE_TIMES): thread 0 of CTA 0 reads %globaltimer
     // at the phase boundaries -- its own tiles, waiting for the CTA's other warps, CTA reduction + grid
     // barrier (+ rank exchange), apply -- and the sums go to GA.phase_ns at the end
-    const bool ph = GA.phase_ns && blockIdx.x == 0 && tid == 0;
+    const bool ph = PH && blockIdx.x == 0 && tid == 0;
     unsigned long long ph_sum[4] = {0, 0, 0, 0}, ph_t = 0, ph_u = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         if (ctrl[1] && blockIdx.x == 0)
             for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
     }
-    if (ph) {
+    if (PH && ph) {
         for (int k = 0; k < 4; k++) GA.phase_ns[k] = ph_sum[k];
         GA.phase_ns[4] = (unsigned long long)it;
     }
@@ -389,7 +392,8 @@ __global__ void k_bs_to_csr(const int32_t *BS, int n, int V, int32_t *bp, int32_
 template <bool TABU, class TT, class ET, bool FULL>
 static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks, int threads, size_t smem,
                             cudaStream_t st) {
-    auto kern = GA.T_smem ? k_grid<TABU, TT, ET, FULL, false> : k_grid<TABU, TT, ET, FULL, true>;
+    auto kern = GA.phase_ns ? (GA.T_smem ? k_grid<TABU, TT, ET, FULL, false, true> : k_grid<TABU, TT, ET, FULL, true, true>)
+                            : (GA.T_smem ? k_grid<TABU, TT, ET, FULL, false, false> : k_grid<TABU, TT, ET, FULL, true, false>);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     SearchArgs a = A;

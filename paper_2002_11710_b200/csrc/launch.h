@@ -41,7 +41,10 @@ struct SearchArgs {
     int32_t *tabu_out;                     // [R][n][V]
 };
 
-constexpr int GRID_WARPS = 24;   // k_grid warps per CTA (one CTA per SM; <= 85 registers per thread; 28 measured slower)
+// k_grid warps per CTA (one CTA per SM): 20 leaves 96 registers per thread (no spills in the scorers);
+// measured against 24 and 16 (profiles/r02/kgrid_warps_ab.jsonl): C1 +7 %, C2 +6 %, C4 +5 %, C5 +-0 vs 24;
+// 16 is slower on C1 (one CTA) and C5 (throughput)
+constexpr int GRID_WARPS = 20;
 
 struct BatchLayout {
     int T, CS, MH, VC, CH, TT, TD, TDT;   // CTA-wide part (window scorers: TT transposed table when
