@@ -90,6 +90,33 @@ __global__ void __launch_bounds__(THREADS, 1) k_lds_seq(int iters, uint32_t *sin
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// LDS.U16 with STRIDE halfwords between lanes (1: 32 lanes read 64 contiguous bytes; 2: one halfword of each of
+// 32 consecutive words): is a sub-word shared load one wavefront, or two?
+template <int STRIDE>
+__global__ void __launch_bounds__(THREADS, 1) k_lds_u16(int iters, uint32_t *sink, long long *cyc) {
+    __shared__ uint16_t buf[16384];
+    for (int i = threadIdx.x; i < 16384; i += blockDim.x) buf[i] = (uint16_t)(i * 40503u);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t acc = 0;
+    uint32_t row = (warp * 8) % 192;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+        uint32_t v[8];
+        const uint16_t *p = buf + row * 64 + lane * STRIDE;   // 64 halfwords per row
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = p[k * 64];
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc += v[k];
+        row += 8 + (acc & 1);
+        if (row >= 192) row -= 192;
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    if (acc == 0x12345678u) sink[threadIdx.x] = acc;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // uint16 gathers at pseudo-random offsets of a 64 KB table: 8 independent gathers per round
 __global__ void __launch_bounds__(THREADS, 1) k_lds_gather(int iters, uint32_t *sink, long long *cyc) {
     extern __shared__ uint16_t tab[];   // 32768 entries
@@ -149,10 +176,12 @@ int main() {
     CK(cudaMalloc(&cyc, nsm * sizeof(long long)));
     const double warps = (double)nsm * THREADS / 32;
     const int it_int = 200000, it_lds = 40000;
-    Meas m_alu, m_mix, m_seq, m_gat;
+    Meas m_alu, m_mix, m_seq, m_gat, m_u1, m_u2;
     if (timed([&] { k_int<0><<<nsm, THREADS>>>(it_int, 1u, sink, cyc); }, nsm, cyc, &m_alu)) return 1;
     if (timed([&] { k_int<1><<<nsm, THREADS>>>(it_int, 1u, sink, cyc); }, nsm, cyc, &m_mix)) return 1;
     if (timed([&] { k_lds_seq<<<nsm, THREADS>>>(it_lds, sink, cyc); }, nsm, cyc, &m_seq)) return 1;
+    if (timed([&] { k_lds_u16<1><<<nsm, THREADS>>>(it_lds, sink, cyc); }, nsm, cyc, &m_u1)) return 1;
+    if (timed([&] { k_lds_u16<2><<<nsm, THREADS>>>(it_lds, sink, cyc); }, nsm, cyc, &m_u2)) return 1;
     CK(cudaFuncSetAttribute(k_lds_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
     if (timed([&] { k_lds_gather<<<nsm, THREADS, 65536>>>(it_lds, sink, cyc); }, nsm, cyc, &m_gat)) return 1;
     // thread-level integer ops: IADD3 counts as one op (two adds in the PTX above fold into one IADD3;
@@ -169,6 +198,8 @@ int main() {
            rate(ops_int, m_mix), per_cyc(ops_int, m_mix), m_mix.ms);
     printf(" \"lds_seq\": {\"bytes_per_s\": %.6g, \"bytes_per_sm_cycle\": %.3f, \"wavefronts_per_sm_cycle\": %.3f, \"ms\": %.3f},\n",
            rate(loads * 128, m_seq), per_cyc(loads * 128, m_seq), per_cyc(loads, m_seq), m_seq.ms);
+    printf(" \"lds_u16_contiguous\": {\"warp_loads_per_sm_cycle\": %.4f, \"ms\": %.3f},\n", per_cyc(loads, m_u1), m_u1.ms);
+    printf(" \"lds_u16_word_stride\": {\"warp_loads_per_sm_cycle\": %.4f, \"ms\": %.3f},\n", per_cyc(loads, m_u2), m_u2.ms);
     printf(" \"lds_gather_u16\": {\"gathers_per_s\": %.6g, \"gathers_per_sm_cycle\": %.3f, \"useful_bytes_per_s\": %.6g, "
            "\"warp_loads_per_sm_cycle\": %.4f, \"ms\": %.3f}}\n",
            rate(loads * 32, m_gat), per_cyc(loads * 32, m_gat), rate(loads * 64, m_gat), per_cyc(loads, m_gat),
