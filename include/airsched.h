@@ -146,8 +146,10 @@ as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t value);
 /* Per-iteration device latency of the last whole-GPU (k_grid) run made with AS_OPT_PHASE_TIMES = 1,
  * measured by CTA 0 with %globaltimer and summed over the iterations: out[0] its own tiles' scoring,
  * out[1] waiting for the CTA's other warps, out[2] CTA reduction + grid barrier (+ rank exchange),
- * out[3] apply, in ns; out[4] = iterations.  Synchronises the context's stream.  AS_ERR_INVALID_ARG if
- * no such run was made. */
+ * out[3] apply, in ns; out[4] = iterations; out[5] the part of out[3] spent reading the winning key
+ * from L2 after the barrier; out[6..9] lane 0's split, relink, totals + bookkeeping, and the warp's record
+ * refresh inside the apply.  out holds 10 entries.  Synchronises the context's stream.
+ * AS_ERR_INVALID_ARG if no such run was made. */
 as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out);
 void as_ctx_destroy(as_ctx *ctx);
 /* Upload (and cache on ctx) the instance's device copy.  Optional: every call

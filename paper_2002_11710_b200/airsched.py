@@ -211,11 +211,14 @@ class Ctx:
 
     def grid_phases(self):
         """as_ctx_grid_phases: per-iteration latency (us) of the last whole-GPU run with PHASE_TIMES=1."""
-        out = np.zeros(5, np.int64)
+        out = np.zeros(10, np.int64)
         _check(lib.as_ctx_grid_phases(self.handle, out.ctypes.data))
         it = max(int(out[4]), 1)
-        return {"own_tiles_us": out[0] / it / 1e3, "cta_wait_us": out[1] / it / 1e3,
-                "reduce_barrier_us": out[2] / it / 1e3, "apply_us": out[3] / it / 1e3, "iterations": int(out[4])}
+        us = lambda k: float(out[k]) / it / 1e3   # noqa: E731
+        return {"own_tiles_us": us(0), "cta_wait_us": us(1), "reduce_barrier_us": us(2), "apply_us": us(3),
+                "apply_parts_us": {"key_read": us(5), "split": us(6), "relink": us(7), "totals": us(8),
+                                   "refresh": us(9)},
+                "iterations": int(out[4])}
 
     def options(self, **kw):
         """Context manager: set options, restore the automatic choice on exit."""

@@ -337,7 +337,7 @@ extern "C" as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out) {
     as_status st = set_device(ctx);
     if (st != AS_OK) return st;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    CUDA_TRY(cudaMemcpy(out, ctx->phase_dev, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out, ctx->phase_dev, 10 * sizeof(int64_t), cudaMemcpyDeviceToHost));
     return AS_OK;
 }
 
@@ -823,8 +823,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 void *p;
                 GA.phase_ns = nullptr;
                 if (opt_int(ctx, AS_OPT_PHASE_TIMES, 0) == 1) {
-                    if ((st = scratch(ctx, "g_phase", 5 * 8, &p)) != AS_OK) return st;
-                    CUDA_TRY(cudaMemsetAsync(p, 0, 5 * 8, ctx->stream));
+                    if ((st = scratch(ctx, "g_phase", 10 * 8, &p)) != AS_OK) return st;
+                    CUDA_TRY(cudaMemsetAsync(p, 0, 10 * 8, ctx->stream));
                     GA.phase_ns = (unsigned long long *)p;
                     ctx->phase_dev = p;
                 }

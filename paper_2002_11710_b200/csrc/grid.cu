@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     // at the phase boundaries -- its own tiles, waiting for the CTA's other warps, CTA reduction + grid
     // barrier (+ rank exchange), apply -- and the sums go to GA.phase_ns at the end
     const bool ph = PH && blockIdx.x == 0 && tid == 0;
-    unsigned long long ph_sum[4] = {0, 0, 0, 0}, ph_t = 0, ph_u = 0;
+    unsigned long long ph_sum[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_t = 0, ph_u = 0, ph_v = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
         if (ph) ph_t = globaltimer_ns();
@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             int nt = 0;
             if (lane == 0) {
                 const uint64_t k = GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
+                if (ph) { asm volatile("" ::"l"(k)); ph_sum[4] += globaltimer_ns() - ph_t; }   // key read (part of apply)
                 int stop = 0;
                 if (k == KEY_ABORT) stop = AS_STOP_COMM_ABORT;   // a peer never arrived (bounded wait)
                 else if (k == KEY_NONE) stop = AS_STOP_NO_MOVE;
@@ -316,8 +317,11 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
                 if (!stop) {
                     const uint32_t idx = key_idx(k);
                     const int32_t delta = key_delta(k);
+                    if (ph) ph_v = globaltimer_ns();
                     const MoveSplit ms = move_split(M, R, idx, delta);
+                    if (ph) { asm volatile("" ::"r"(ms.a), "r"(ms.da)); ph_u = globaltimer_ns(); ph_sum[5] += ph_u - ph_v; ph_v = ph_u; }
                     nt = move_relink(M, R, idx, ms.a, ms.b, ctrl + 4);
+                    if (ph) { asm volatile("" ::"r"(nt)); ph_u = globaltimer_ns(); ph_sum[6] += ph_u - ph_v; ph_v = ph_u; }
                     move_totals(M, R, idx, ms, it, A.tenure, TABU);
                     if (TABU && Et) {   // the transposed copy gets the same expiries (every CTA, identical values)
                         const uint32_t Rb = (uint32_t)n * (uint32_t)S;
@@ -345,11 +349,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
                         tr.it = it;
                         A.trace[it] = tr;
                     }
+                    if (ph) { ph_u = globaltimer_ns(); ph_sum[7] += ph_u - ph_v; ph_v = ph_u; }
                 }
             }
             nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
             __syncwarp();
             if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
+            __syncwarp();
+            if (ph) { ph_u = globaltimer_ns(); ph_sum[8] += ph_u - ph_v; }
         }
         __syncthreads();
         if (ph) ph_sum[3] += globaltimer_ns() - ph_t;
@@ -360,6 +367,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     if (PH && ph) {
         for (int k = 0; k < 4; k++) GA.phase_ns[k] = ph_sum[k];
         GA.phase_ns[4] = (unsigned long long)it;
+        GA.phase_ns[5] = ph_sum[4];
+        for (int k = 5; k < 9; k++) GA.phase_ns[k + 1] = ph_sum[k];
     }
     if (blockIdx.x == 0 && tid == 0) {
         as_run_result *res = A.results;
