@@ -17,7 +17,8 @@ def main():
     n, V = inst.n_missions, inst.n_vehicles
     vm = n * (n + V - 2) + n * (n - 1) // 2
     prm = A.params(mode=1, tenure=10, max_iters=200)
-    for G in [None] + list(range(2, 11)):
+    Gs = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(2, 11))
+    for G in [None] + Gs:
         with ctx.options(GRID_G=G):
             A.as_tabu_run(ctx, h, p, m, prm, want_best=False)
             ms = []
