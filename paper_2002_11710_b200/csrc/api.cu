@@ -1403,472 +1403,6 @@ static as_status comm_device_setup(as_comm *comm) {
 
 static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
                              const int32_t *start_ms, const as_run_params *P, as_run_result *result,
-                             int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out);
-
-extern "C" as_status as_tabu_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
-                                 const int32_t *start_ms, const as_run_params *P, as_run_result *result,
-                                 int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, uint64_t *digest,
-                                 int32_t *tabu_out) {
-    if (!ctx || !I || !P || !result) return fail(AS_ERR_INVALID_ARG, "null argument");
-    HostSched S;
-    as_status st = parse_csr(I, start_ptr, start_ms, false, S);
-    if (st != AS_OK) return st;
-    int32_t feas;
-    int64_t obj;
-    as_schedule_check(I, start_ptr, start_ms, &feas, &obj);
-    if (!feas) return fail(AS_ERR_INFEASIBLE_START, "start schedule is infeasible (SPEC S:348)");
-    if ((comm || opt_int(ctx, AS_OPT_SHARDED, 0) == 1) && !P->sweep) {
-        if (I->no_wait) return fail(AS_ERR_UNSUPPORTED, "the sharded path is not built for the no-wait variant");
-        if (digest && P->trace_level >= 2) return fail(AS_ERR_UNSUPPORTED, "tabu digests are not produced by the sharded path");
-        return sharded_run(ctx, comm, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
-    }
-    st = run_core(ctx, I, 1, start_ptr, start_ms, 0, P, nullptr, result, best_ptr, best_ms, trace, digest, tabu_out, true);
-    if (st == AS_ERR_UNSUPPORTED && !P->sweep && !I->no_wait && !(digest && P->trace_level >= 2) && I->NL <= 65535 &&
-        I->n + I->V <= 65535 && I->NC <= 2) {
-        // no on-chip kernel holds this instance's state: the sharded kernels keep it in global
-        // memory (L2-resident), here with one rank
-        return sharded_run(ctx, nullptr, I, start_ptr, start_ms, P, result, best_ptr, best_ms, trace, tabu_out);
-    }
-    if (st != AS_OK) return st;
-    if (result->stop_reason == AS_STOP_INFEASIBLE_START)
-        return fail(AS_ERR_INFEASIBLE_START, "device rejected the start schedule");
-    return AS_OK;
-}
-
-extern "C" as_status as_nbhd_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
-                                 const int32_t *start_ms, const as_run_params *P, as_run_result *result,
-                                 int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace) {
-    if (!P) return fail(AS_ERR_INVALID_ARG, "null params");
-    as_run_params q = *P;
-    q.mode = AS_MODE_NS;
-    return as_tabu_run(ctx, comm, I, start_ptr, start_ms, &q, result, best_ptr, best_ms, trace, nullptr, nullptr);
-}
-
-extern "C" as_status as_batch_run(as_ctx *ctx, as_comm *comm, const as_instance *I, int32_t n_runs,
-                                  const int32_t *start_ptr, const int32_t *start_ms, int32_t shared_start,
-                                  const as_run_params *P, const uint64_t *seeds, as_run_result *results,
-                                  int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int64_t *best_run_out) {
-    if (!ctx || !I || !P) return fail(AS_ERR_INVALID_ARG, "null argument");
-    if (!start_ptr) return fail(AS_ERR_INVALID_ARG, "null start");
-    // the best-run key packs (best objective << 32 | global run): objective <= V * P and the
-    // global run index must each fit 32 bits
-    if ((int64_t)I->V * I->P >= (1ll << 31))
-        return fail(AS_ERR_UNSUPPORTED, "V * flight_limit_s >= 2^31: the best-run key cannot hold the objective");
-    if ((int64_t)(comm ? comm->nranks : 1) * n_runs >= (1ll << 32))
-        return fail(AS_ERR_INVALID_ARG, "nranks * n_runs >= 2^32");
-    // results are needed on the device for the best-run reduction
-    as_run_result *res = results;
-    if (!res || !is_device_ptr(res)) {
-        void *p;
-        as_status st = scratch(ctx, "batch_res", (size_t)n_runs * sizeof(as_run_result), &p);
-        if (st != AS_OK) return st;
-        res = (as_run_result *)p;
-    }
-    as_status st = run_core(ctx, I, n_runs, start_ptr, start_ms, shared_start, P, seeds, res, best_ptr, best_ms,
-                            trace, nullptr, nullptr, false);
-    if (st != AS_OK) return st;
-    // best (objective, global run) over all ranks: on the device, NCCL MIN across ranks
-    void *kp;
-    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
-    const int64_t offset = comm ? (int64_t)comm->rank * n_runs : 0;
-    CUDA_TRY(launch_batch_best(res, n_runs, offset, (unsigned long long *)kp, ctx->stream));
-    ctx->launches++;
-    if (comm && comm->nranks > 1)
-        NCCL_TRY(ncclAllReduce(kp, kp, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream));
-    ctx->batch_runs = n_runs;
-    ctx->batch_n = I->n;
-    ctx->batch_V = I->V;
-    if (results && res != results) {
-        CUDA_TRY(cudaMemcpyAsync(results, res, (size_t)n_runs * sizeof(as_run_result), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    }
-    if (best_run_out) {
-        unsigned long long k;
-        CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        *best_run_out = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
-    }
-    return AS_OK;
-}
-
-extern "C" as_status as_batch_run_jobs(as_ctx *ctx, as_comm *comm, int32_t n_jobs, const as_job *jobs,
-                                       const as_run_params *P, const uint64_t *seeds, as_run_result *results,
-                                       int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace,
-                                       int64_t *best_run_out) {
-    if (!ctx || !jobs || !P || n_jobs < 1) return fail(AS_ERR_INVALID_ARG, "null argument or no jobs");
-    if (P->mode != AS_MODE_NS && P->mode != AS_MODE_TABU) return fail(AS_ERR_INVALID_ARG, "mode must be NS or TABU");
-    if (P->max_iters < 0 || P->tenure < 0 || P->kick < 0) return fail(AS_ERR_INVALID_ARG, "negative parameter");
-    as_status st = set_device(ctx);
-    if (st != AS_OK) return st;
-    const bool tabu = P->mode == AS_MODE_TABU;
-    int64_t total = 0, bp_total = 0, bm_total = 0;
-    int tbytes = 2;
-    for (int j = 0; j < n_jobs; j++) {
-        const as_instance *I = jobs[j].inst;
-        if (!I || !jobs[j].start_ptr || jobs[j].n_runs < 1) return fail(AS_ERR_INVALID_ARG, "job %d: null instance/start or n_runs < 1", j);
-        if (I->NL > 65535 || I->n + I->V > 65535 || I->V > 32767 || I->NC > 2 || I->no_wait)
-            return fail(AS_ERR_UNSUPPORTED, "job %d: the multi-instance batch needs the compact layout (NL, n+V < 65536, <= 2 classes, waiting model)", j);
-        if (I->maxT > 65535) tbytes = 4;
-        if ((int64_t)I->V * I->P >= (1ll << 31))   // best-run key: objective << 32 (see as_batch_run)
-            return fail(AS_ERR_UNSUPPORTED, "job %d: V * flight_limit_s >= 2^31", j);
-        total += jobs[j].n_runs;
-        bp_total += (int64_t)jobs[j].n_runs * (I->V + 1);
-        bm_total += (int64_t)jobs[j].n_runs * I->n;
-    }
-    if (total >= (1ll << 31) || (int64_t)(comm ? comm->nranks : 1) * total >= (1ll << 32))
-        return fail(AS_ERR_INVALID_ARG, "too many runs");
-    const int ebytes = (int64_t)P->max_iters + P->tenure < 32767 ? 2 : 4;
-    // per-job device instance, layout, runs per CTA, packed start
-    std::vector<BatchJob> J(n_jobs);
-    std::vector<int4> cta;
-    size_t smem = 0;
-    int threads = 32;
-    std::vector<int32_t> packed;           // host starts, uploaded once
-    std::vector<std::pair<int64_t, int64_t>> poff(n_jobs, {-1, -1});
-    // window scorers (window.cuh) for the FAST launch when every FAST job qualifies (V <= 32)
-    bool win = ((P->sweep ? 1u : P->move_mask) & 15u) == 15u && !P->sweep && tbytes == 2 &&
-               (!tabu || P->tenure <= WIN_MAX_TENURE) && opt_int(ctx, AS_OPT_WINDOW, 1) == 1 &&
-               true;
-    for (int j = 0; j < n_jobs && win; j++) {
-        const DevInst *D;
-        if ((st = get_dev_inst(ctx, jobs[j].inst, &D)) != AS_OK) return st;
-        if (jobs[j].inst->V > 32 || jobs[j].inst->tdmax > 65535 || jobs[j].inst->P >= (1 << 28)) win = false;
-    }
-    int64_t run0 = 0, bp0 = 0, bm0 = 0, e0 = 0;
-    for (int j = 0; j < n_jobs; j++) {
-        const as_instance *I = jobs[j].inst;
-        const DevInst *D;
-        if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
-        BatchJob &b = J[j];
-        b.inst = *D;
-        const bool wj = win;
-        b.L = batch_layout_host(I->n, I->V, I->NL, I->NC, tbytes, ebytes, tabu, wj, P->tenure, I->tsym != 0);
-        b.e_off = e0;
-        if (wj && tabu) e0 += (int64_t)jobs[j].n_runs * I->n * I->V;
-        b.NLp = padded_stride_host(I->NL, tbytes);
-        if ((size_t)b.L.shared_bytes + b.L.run_bytes > ctx->max_smem)
-            return fail(AS_ERR_UNSUPPORTED, "job %d: instance too large for the batched kernel", j);
-        const int fit = (int)((ctx->max_smem - b.L.shared_bytes) / b.L.run_bytes);
-        {   // runs per CTA: as few CTAs as fit (<= 28 runs each), the job's runs spread evenly over them
-            const int rmax = std::max(1, std::min(28, fit));
-            const int nct = (jobs[j].n_runs + rmax - 1) / rmax;
-            b.RPC = (jobs[j].n_runs + nct - 1) / nct;
-        }
-        b.run0 = (int)run0;
-        b.bp_off = bp0;
-        b.bm_off = bm0;
-        if (is_device_ptr(jobs[j].start_ptr)) {
-            b.start_ptr = jobs[j].start_ptr;
-            b.start_ms = jobs[j].start_missions;
-        } else {
-            HostSched S;
-            if ((st = parse_csr(I, jobs[j].start_ptr, jobs[j].start_missions, false, S)) != AS_OK) return st;
-            poff[j].first = (int64_t)packed.size();
-            packed.insert(packed.end(), jobs[j].start_ptr, jobs[j].start_ptr + I->V + 1);
-            poff[j].second = (int64_t)packed.size();
-            if (I->n > 0) packed.insert(packed.end(), jobs[j].start_missions, jobs[j].start_missions + I->n);
-        }
-        for (int r = 0; r < jobs[j].n_runs; r += b.RPC)
-            cta.push_back(make_int4(j, r, std::min(b.RPC, jobs[j].n_runs - r), D->svcpos ? 1 : 0));
-        smem = std::max(smem, (size_t)b.L.shared_bytes + (size_t)b.RPC * b.L.run_bytes);
-        threads = std::max(threads, b.RPC * 32);
-        run0 += jobs[j].n_runs;
-        bp0 += (int64_t)jobs[j].n_runs * (I->V + 1);
-        bm0 += (int64_t)jobs[j].n_runs * I->n;
-    }
-    if (!packed.empty()) {
-        const void *dp;
-        if ((st = dev_in(ctx, "jobs_starts", packed.data(), packed.size() * 4, &dp)) != AS_OK) return st;
-        for (int j = 0; j < n_jobs; j++)
-            if (poff[j].first >= 0) {
-                J[j].start_ptr = (const int32_t *)dp + poff[j].first;
-                J[j].start_ms = (const int32_t *)dp + poff[j].second;
-            }
-    }
-    // the FAST scorers need every pickup->delivery leg > 0 (svcpos): with every move kind enabled the
-    // CTAs of such jobs go first in one launch, the others in a second launch on a side stream
-    const bool all_moves = ((P->sweep ? 1u : P->move_mask) & 15u) == 15u;
-    std::stable_sort(cta.begin(), cta.end(), [&](const int4 &x, const int4 &y) { return (all_moves && x.w) > (all_moves && y.w); });
-    int n_fast = 0;
-    for (const int4 &c : cta) n_fast += all_moves && c.w;
-    const void *djobs, *dcta, *ds = nullptr;
-    if ((st = dev_in(ctx, "jobs_table", J.data(), J.size() * sizeof(BatchJob), &djobs)) != AS_OK) return st;
-    if ((st = dev_in(ctx, "jobs_cta", cta.data(), cta.size() * sizeof(int4), &dcta)) != AS_OK) return st;
-    if (seeds && (st = dev_in(ctx, "jobs_seeds", seeds, (size_t)total * 8, &ds)) != AS_OK) return st;
-    as_run_result *res = results;
-    if (!res || !is_device_ptr(res)) {
-        void *p;
-        if ((st = scratch(ctx, "jobs_res", (size_t)total * sizeof(as_run_result), &p)) != AS_OK) return st;
-        res = (as_run_result *)p;
-    }
-    OutBuf o_bp, o_bm, o_tr;
-    if (best_ptr && !best_ms && bm_total > 0) return fail(AS_ERR_INVALID_ARG, "best_ptr_out needs best_missions_out");
-    if ((st = dev_out(ctx, "jobs_bp", best_ptr, (size_t)bp_total * 4, o_bp)) != AS_OK) return st;
-    if ((st = dev_out(ctx, "jobs_bm", best_ptr ? best_ms : nullptr, std::max<size_t>((size_t)bm_total * 4, 4), o_bm)) != AS_OK) return st;
-    const bool want_trace = trace && P->trace_level >= 1 && P->max_iters > 0;
-    if ((st = dev_out(ctx, "jobs_tr", want_trace ? trace : nullptr, (size_t)total * P->max_iters * sizeof(as_trace_rec), o_tr)) != AS_OK) return st;
-    SearchArgs A;
-    memset(&A, 0, sizeof(A));
-    A.one = 1;
-    A.neg = -1;
-    A.n_runs = (int32_t)total;
-    A.seeds = (const uint64_t *)ds;
-    A.seed = P->seed;
-    A.kick = P->kick;
-    A.tenure = P->tenure;
-    A.max_iters = P->max_iters;
-    A.strict_tabu_stop = P->strict_tabu_stop;
-    A.mask = P->sweep ? 1u : P->move_mask;
-    A.sweep = P->sweep ? 1 : 0;
-    A.results = res;
-    A.best_ptr = (int32_t *)o_bp.dev;
-    A.best_ms = best_ptr ? (int32_t *)o_bm.dev : nullptr;
-    A.trace = (as_trace_rec *)o_tr.dev;
-    if (e0 > 0) {   // tabu matrices of the window-path runs (global memory)
-        void *e;
-        if ((st = scratch(ctx, "E_win_jobs", (size_t)e0 * 4 + 4, &e)) != AS_OK) return st;
-        A.E_global = (int32_t *)e;
-    }
-    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    const int n_gen = (int)cta.size() - n_fast;
-    if (n_gen > 0 && n_fast > 0) {   // fork the general-scorer CTAs onto the side stream
-        CUDA_TRY(cudaEventRecord(ctx->evj, ctx->stream));
-        CUDA_TRY(cudaStreamWaitEvent(ctx->cap, ctx->evj, 0));
-        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta + n_fast, n_gen, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->cap, win));
-        ctx->launches++;
-    }
-    if (n_fast > 0) {
-        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_fast, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, true, ctx->stream, win));
-        ctx->launches++;
-    } else {
-        CUDA_TRY(launch_batch_jobs(A, (const BatchJob *)djobs, (const int4 *)dcta, n_gen, threads, smem,
-                                   tabu ? 1 : 0, tbytes, ebytes, false, ctx->stream, win));
-        ctx->launches++;
-    }
-    if (n_gen > 0 && n_fast > 0) {   // join
-        CUDA_TRY(cudaEventRecord(ctx->evj, ctx->cap));
-        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evj, 0));
-    }
-    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
-    ctx->timed = true;
-    void *kp;
-    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
-    const int64_t offset = comm ? (int64_t)comm->rank * total : 0;
-    CUDA_TRY(launch_batch_best(res, (int)total, offset, (unsigned long long *)kp, ctx->stream));
-    ctx->launches++;
-    if (comm && comm->nranks > 1)
-        NCCL_TRY(ncclAllReduce(kp, kp, 1, ncclUint64, ncclMin, comm->nccl, ctx->stream));
-    ctx->batch_runs = -1;   // as_batch_gather_best is for single-instance batches
-    if (results && res != results)
-        CUDA_TRY(cudaMemcpyAsync(results, res, (size_t)total * sizeof(as_run_result), cudaMemcpyDeviceToHost, ctx->stream));
-    if ((st = finish_out(ctx, {&o_bp, &o_bm, &o_tr})) != AS_OK) return st;
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (best_run_out) {
-        unsigned long long k;
-        CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        *best_run_out = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
-    }
-    return AS_OK;
-}
-
-extern "C" as_status as_batch_gather_best(as_ctx *ctx, as_comm *comm, int32_t n_runs, const int32_t *run_best_ptr,
-                                          const int32_t *run_best_ms, int64_t *best_run_out, int64_t *best_obj_out,
-                                          int32_t *ptr_out, int32_t *ms_out) {
-    if (!ctx) return fail(AS_ERR_INVALID_ARG, "null ctx");
-    if (ctx->batch_runs != n_runs) return fail(AS_ERR_INVALID_ARG, "no as_batch_run of %d runs on this context", n_runs);
-    as_status st = set_device(ctx);
-    if (st != AS_OK) return st;
-    void *kp;
-    if ((st = scratch(ctx, "batch_key", 8, &kp)) != AS_OK) return st;
-    unsigned long long k;
-    CUDA_TRY(cudaMemcpyAsync(&k, kp, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    const int64_t run = k == AS_KEY_NONE ? -1 : (int64_t)(k & 0xFFFFFFFFull);
-    if (best_run_out) *best_run_out = run;
-    if (best_obj_out) *best_obj_out = k == AS_KEY_NONE ? -1 : (int64_t)(k >> 32);
-    if (!ptr_out || run < 0) return AS_OK;
-    // owner copies its run's CSR into a buffer, NCCL broadcast to every rank
-    const int rank = comm ? comm->rank : 0;
-    const int owner = (int)(run / n_runs);
-    const int r = (int)(run % n_runs);
-    if (!run_best_ptr || !run_best_ms) return fail(AS_ERR_INVALID_ARG, "run_best_ptr/ms required for the schedule");
-    const int V = ctx->batch_V, n = ctx->batch_n;
-    void *buf;
-    if ((st = scratch(ctx, "gbest", (size_t)(V + 1 + n) * 4 + 4, &buf)) != AS_OK) return st;
-    if (rank == owner) {
-        CUDA_TRY(cudaMemcpyAsync(buf, run_best_ptr + (size_t)r * (V + 1), (size_t)(V + 1) * 4, cudaMemcpyDefault, ctx->stream));
-        if (n > 0)
-            CUDA_TRY(cudaMemcpyAsync((int32_t *)buf + V + 1, run_best_ms + (size_t)r * n, (size_t)n * 4, cudaMemcpyDefault,
-                                     ctx->stream));
-    }
-    if (comm && comm->nranks > 1)
-        NCCL_TRY(ncclBroadcast(buf, buf, (size_t)(V + 1 + n), ncclInt32, owner, comm->nccl, ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(ptr_out, buf, (size_t)(V + 1) * 4, cudaMemcpyDefault, ctx->stream));
-    if (n > 0 && ms_out)
-        CUDA_TRY(cudaMemcpyAsync(ms_out, (int32_t *)buf + V + 1, (size_t)n * 4, cudaMemcpyDefault, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    return AS_OK;
-}
-
-// ------------------------------------------------------------ Algorithm 1 ---
-// Device Algorithm 1 for n_starts starts (greedy.cu, one warp per start).
-extern "C" as_status as_init_greedy_batch(as_ctx *ctx, const as_instance *I, int32_t n_starts, int32_t insert_mode,
-                                          int32_t max_repairs, const uint64_t *seeds, int32_t *route_ptr_out,
-                                          int32_t *route_missions_out, int32_t *status_out, int32_t *n_repairs_out) {
-    if (!ctx || !I || !route_ptr_out) return fail(AS_ERR_INVALID_ARG, "null argument");
-    if (n_starts < 1) return fail(AS_ERR_INVALID_ARG, "n_starts must be >= 1");
-    if (insert_mode != 0 && insert_mode != 1) return fail(AS_ERR_INVALID_ARG, "insert_mode must be 0 (TAIL) or 1 (SORTED)");
-    if (max_repairs < 0) return fail(AS_ERR_INVALID_ARG, "max_repairs must be >= 0");
-    if (I->n > 0 && !route_missions_out) return fail(AS_ERR_INVALID_ARG, "null route_missions_out");
-    as_status st = set_device(ctx);
-    if (st != AS_OK) return st;
-    const DevInst *D;
-    if ((st = get_dev_inst(ctx, I, &D)) != AS_OK) return st;
-    const int n = I->n, V = I->V;
-    const size_t R = (size_t)n_starts;
-    const void *ds = nullptr;
-    if (seeds && (st = dev_in(ctx, "g_seeds", seeds, R * 8, &ds)) != AS_OK) return st;
-    OutBuf op, om, os, onr;
-    if ((st = dev_out(ctx, "g_ptr", route_ptr_out, R * (V + 1) * 4, op)) != AS_OK) return st;
-    if ((st = dev_out(ctx, "g_ms", route_missions_out, std::max<size_t>(R * n * 4, 4), om)) != AS_OK) return st;
-    if ((st = dev_out(ctx, "g_status", status_out, R * 4, os)) != AS_OK) return st;
-    if ((st = dev_out(ctx, "g_nrep", n_repairs_out, R * 4, onr)) != AS_OK) return st;
-    void *ord;
-    if ((st = scratch(ctx, "g_order", (size_t)n * 4 + 4, &ord)) != AS_OK) return st;
-    // layout: T + up to 8 warps of state in shared memory, else state only, else global state
-    const size_t sb = greedy_state_bytes(*D);
-    const size_t lim = ctx->max_smem;
-    int warps = 0;
-    bool T_smem = false, state_smem = false;
-    if (opt_int(ctx, AS_OPT_GREEDY_GLOBAL, 0) == 1) warps = -1;   // test option: state in global memory
-    for (int w = 8; w >= 1 && !warps; w /= 2)
-        if (greedy_smem_bytes(*D, w, true, true) <= lim) { warps = w; T_smem = state_smem = true; }
-    for (int w = 8; w >= 1 && !warps; w /= 2)
-        if (greedy_smem_bytes(*D, w, false, true) <= lim) { warps = w; state_smem = true; }
-    void *sg = nullptr;
-    if (warps <= 0) {
-        warps = 4;
-        T_smem = greedy_smem_bytes(*D, warps, true, false) <= lim;
-        if ((st = scratch(ctx, "g_state", R * sb, &sg)) != AS_OK) return st;
-    }
-    warps = std::max(1, std::min<int>(warps, (int)std::min<size_t>(8, R)));
-    CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
-    CUDA_TRY(launch_greedy(*D, n_starts, insert_mode, max_repairs, (const uint64_t *)ds, (int32_t *)ord,
-                           (int32_t *)sg, warps, T_smem, state_smem, (int32_t *)op.dev, (int32_t *)om.dev,
-                           (int32_t *)os.dev, (int32_t *)onr.dev, ctx->stream));
-    CUDA_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
-    ctx->timed = true;
-    ctx->launches += n > 0 ? 2 : 1;
-    return finish_out(ctx, {&op, &om, &os, &onr});
-}
-
-// Algorithm 1 for one start in the paper's order: the batched device kernel with n_starts = 1, seed 0.
-extern "C" as_status as_init_greedy(as_ctx *ctx, const as_instance *I, int32_t insert_mode, int32_t max_repairs,
-                                    int32_t *route_ptr_out, int32_t *route_missions_out, int32_t *n_repairs_out) {
-    if (!ctx || !I || !route_ptr_out) return fail(AS_ERR_INVALID_ARG, "null argument");
-    int32_t status = AS_OK, nrep = 0;
-    as_status st = as_init_greedy_batch(ctx, I, 1, insert_mode, max_repairs, nullptr, route_ptr_out,
-                                        route_missions_out, &status, &nrep);
-    if (st != AS_OK) return st;
-    if (status != AS_OK)
-        return fail(AS_ERR_INIT_FAILED, "Algorithm 1: a mission could not be placed, even after %d repair(s) (P:166, P:213)", nrep);
-    if (n_repairs_out) *n_repairs_out = nrep;
-    return AS_OK;
-}
-
-// --------------------------------------------------------------- multi-GPU ---
-extern "C" as_status as_comm_unique_id(void *uid_out) {
-    if (!uid_out) return fail(AS_ERR_INVALID_ARG, "null uid_out");
-    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
-    ncclUniqueId id;
-    NCCL_TRY(ncclGetUniqueId(&id));
-    memcpy(uid_out, &id, sizeof(id));
-    return AS_OK;
-}
-
-extern "C" as_status as_comm_init(as_ctx *ctx, int32_t nranks, int32_t rank, const void *uid, as_comm **out) {
-    if (!ctx || !uid || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
-    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(AS_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
-    as_status st = set_device(ctx);
-    if (st != AS_OK) return st;
-    ncclUniqueId id;
-    memcpy(&id, uid, sizeof(id));
-    std::unique_ptr<as_comm> c(new as_comm());
-    c->nranks = nranks;
-    c->rank = rank;
-    c->device = ctx->device;
-    NCCL_TRY(ncclCommInitRank(&c->nccl, nranks, id, rank));
-    *out = c.release();
-    return AS_OK;
-}
-
-extern "C" void as_comm_destroy(as_comm *comm) {
-    if (!comm) return;
-    if (comm->nccl) {
-        cudaSetDevice(comm->device);
-        if (comm->dev_state == 1) ncclCommWindowDeregister(comm->nccl, comm->win);
-        if (comm->xbuf) ncclMemFree(comm->xbuf);
-        ncclCommDestroy(comm->nccl);
-    }
-    delete comm;
-}
-
-static int shard_G(const as_instance *I, int n_sm) {
-    const int n = I->n, V = I->V, S = n + V;
-    const int warps_all = n_sm * 24;
-    const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
-    const int64_t pairs = (int64_t)n * nTC + (int64_t)n * nSC / 2;
-    return (int)std::max<int64_t>(1, pairs / (4 * (int64_t)warps_all));
-}
-
-extern "C" as_status as_shard_plan(const as_instance *I, int32_t nranks, int32_t rank, int32_t n_sm, int32_t *tile_lo,
-                                   int32_t *tile_hi, int32_t *tile_total, int64_t *weight_rank, int64_t *weight_total) {
-    if (!I || nranks < 1 || rank < 0 || rank >= nranks || n_sm < 1) return fail(AS_ERR_INVALID_ARG, "bad argument");
-    const int G = shard_G(I, n_sm);
-    int lo, hi;
-    int64_t wt, wr;
-    shard_plan(I->n, I->V, G, nranks, rank, &lo, &hi, &wt, &wr);
-    int last_lo, total;
-    shard_plan(I->n, I->V, G, 1, 0, &last_lo, &total, nullptr, nullptr);
-    if (tile_lo) *tile_lo = lo;
-    if (tile_hi) *tile_hi = hi;
-    if (tile_total) *tile_total = total;
-    if (weight_rank) *weight_rank = wr;
-    if (weight_total) *weight_total = wt;
-    return AS_OK;
-}
-
-// Sharded single-instance run: replica in global memory, K iterations per CUDA
-// graph of [eval slice -> ncclAllReduce(MIN, 8 B) -> apply].
-// NCCL device-API state of a communicator (collective: every rank calls it in the same order).
-static as_status comm_device_setup(as_comm *comm) {
-    if (comm->dev_state) return AS_OK;
-    comm->dev_state = -1;
-    if (ncclTeamLsa(comm->nccl).nRanks != comm->nranks) return AS_OK;   // not every peer load/store reachable
-    const size_t bytes = std::max<size_t>(4096, (size_t)3 * comm->nranks * 16);
-    NCCL_TRY(ncclMemAlloc(&comm->xbuf, bytes));
-    CUDA_TRY(cudaMemset(comm->xbuf, 0, bytes));   // tags 0: no epoch >= 1 matches them
-    CUDA_TRY(cudaDeviceSynchronize());
-    NCCL_TRY(ncclCommWindowRegister(comm->nccl, comm->xbuf, bytes, &comm->win, NCCL_WIN_COLL_SYMMETRIC));
-    // every rank's window is zeroed before any rank's first fused kernel can store into it:
-    // a one-word all-reduce as a barrier (the memsets above completed before it on each rank)
-    int *bar = nullptr;
-    CUDA_TRY(cudaMalloc(&bar, sizeof(int)));
-    ncclResult_t r = ncclAllReduce(bar, bar, 1, ncclInt32, ncclSum, comm->nccl, 0);
-    cudaError_t e = cudaStreamSynchronize(0);
-    cudaFree(bar);
-    if (r != ncclSuccess) return fail(AS_ERR_COMM, "setup barrier: %s", ncclGetErrorString(r));
-    if (e != cudaSuccess) return fail(AS_ERR_DEVICE, "setup barrier: %s", cudaGetErrorString(e));
-    comm->dev_state = 1;
-    return AS_OK;
-}
-
-static as_status sharded_run(as_ctx *ctx, as_comm *comm, const as_instance *I, const int32_t *start_ptr,
-                             const int32_t *start_ms, const as_run_params *P, as_run_result *result,
                              int32_t *best_ptr, int32_t *best_ms, as_trace_rec *trace, int32_t *tabu_out) {
     as_status st = set_device(ctx);
     if (st != AS_OK) return st;
