@@ -790,10 +790,16 @@ def test_global_node_cost_table(A, oracle_mod):
     O = oracle_mod.Oracle(inst)
     p, m = start_of(O, inst)
     out = []
+    iters = 6
     for node_costs in (1, 0):
         c = A.Ctx(0)
         c.set_option("NODE_COSTS", node_costs)
         h = A.Instance(inst)
         c.upload(h)
-        out.append(_compare_run(A, c, O, h, p, m, 1, 10, 4))
-    assert (out[0]["trace"]["idx"] == out[1]["trace"]["idx"]).all()
+        prm = A.params(mode=1, tenure=10, max_iters=iters, trace_level=1)
+        out.append(A.as_tabu_run(c, h, p, m, prm, want_trace=True, want_tabu=True))
+    o = O.search_par(p, m, mode=1, tenure=10, max_iters=iters, memo=True)
+    for g in out:
+        for k in ("idx", "delta", "cur", "best", "cls"):
+            assert (g["trace"][k] == o["trace"][k]).all(), k
+        assert (g["tabu"] == o["E"]).all() and routes_of(*g["best"]) == routes_of(*o["best"])
