@@ -66,6 +66,14 @@ struct WinCtx {
     int NTDp, LTD;          // TD row stride and class-layer stride (halfwords, compact.cuh td_layer)
 };
 
+// x * p on the FMA pipe (IMAD); with p = 2^s it is x << s.  The tabu-bit shifts are written this way so they
+// leave the ALU pipe, the busier of the two (ncu: ALU 73 %, FMA 30 % of their peaks in k_batch).
+__device__ __forceinline__ uint32_t mul_fma(uint32_t x, uint32_t p) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(x), "r"(p));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {   // x << s, 0 when s >= 32 (PTX shl)
     uint32_t r;
     asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
@@ -136,6 +144,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
     const int tsm = (int)__cvta_generic_to_shared(C.Ts);
     // target-slot side, per lane; c_slk carries the heli offset
     int c_x1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR];
+    uint32_t c_p2[KR];   // 2^b (0 for a lane without a target): the tabu-bit shift as a multiplication
 #pragma unroll
     for (int k = 0; k < KR; k++) {
         const int t = t0 + lane + 32 * k;
@@ -157,6 +166,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
             }
         }
         c_x1[k] = x1; c_t2[k] = t2; c_dw[k] = dw; c_k[k] = kk; c_wsv[k] = wsv; c_slk[k] = slk; c_b[k] = b;
+        c_p2[k] = b < 32 ? 1u << b : 0u;
     }
     uint64_t best = KEY_NONE;
     for (int w0 = m_lo; w0 < m_hi; w0 += WIN_ROWS) {
@@ -198,7 +208,7 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
                 }
                 const int e2 = madd(ins, one, remasp);                                  // delta - asp (TS) / delta (NS)
                 uint32_t nadm;
-                if (TABU) nadm = shl_clamp(tb, (uint32_t)c_b[k]) & ~(uint32_t)e2 & 0x80000000u;
+                if (TABU) nadm = mul_fma(tb, c_p2[k]) & ~(uint32_t)e2 & 0x80000000u;
                 else nadm = ~(uint32_t)e2 & 0x80000000u;
                 const uint32_t k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
@@ -266,6 +276,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
     int q_d2[KS], q_e2[KS], q_p2[KS], q_w2[KS], q_dep2[KS], q_kb[KS], q_ws2[KS], q_slk[KS], q_bf[KS];
     int q_s2[KS];   // general legs only: succ(m2), for the adjacent pairs
     uint32_t q_tb[KS];
+    uint32_t q_pb[KS];   // 2^b (0 for a lane without a mission): the tabu-bit shift as a multiplication
 #pragma unroll
     for (int k = 0; k < KS; k++) {
         const int m2 = lo + lane + 32 * k;
@@ -297,6 +308,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
         }
         q_d2[k] = d2; q_e2[k] = e2; q_p2[k] = p2; q_w2[k] = w2; q_dep2[k] = dep2;
         q_kb[k] = kb; q_ws2[k] = ws2; q_slk[k] = slk; q_bf[k] = bf; q_tb[k] = tb;
+        q_pb[k] = (bf & 0xFFFF) < 32 ? 1u << (bf & 0xFFFF) : 0u;
     }
     const int mlane = lo + lane;   // m2 of sub-chunk 0 (sub-chunk k: + 32 k)
     const int NLp2 = 2 * NLp;
@@ -323,6 +335,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
             const int ndepc1 = q1.x, w1 = q1.y, wsv1 = q1.z, ka = q1.w;
             const int slkA = q2.x, keyb0 = q2.y;
             const uint32_t tb1 = (uint32_t)q2.z;
+            const uint32_t pa = 1u << a;   // a < 32 (window path: V <= 32)
             const int rowM1 = madd(r, NLp2, rowM1_w0);   // TDT row m1 (2 m1 NLp)
             const uint32_t ya_base = (uint32_t)madd(mlane, 2, row_ya1);   // TD_ca[endc1][m2 of sub-chunk 0]
 #pragma unroll
@@ -357,7 +370,7 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                     mg = (l1 | l2 | l3) | (l4 | mf | adj) | tc;
                 }
                 uint32_t nadm;                                                              // delta holds delta - asp
-                if (TABU) nadm = (shl_clamp(tb1, b) | shl_clamp(q_tb[k], (uint32_t)a)) & ~(uint32_t)delta & 0x80000000u;
+                if (TABU) nadm = (mul_fma(tb1, q_pb[k]) | mul_fma(q_tb[k], pa)) & ~(uint32_t)delta & 0x80000000u;
                 else nadm = ~(uint32_t)delta & 0x80000000u;
                 const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
                 bk = min(bk, k32);
