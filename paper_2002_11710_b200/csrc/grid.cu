@@ -108,6 +108,42 @@ __device__ __forceinline__ uint64_t rank_exchange(const GridArgs &GA, int q, int
 }
 
 // TR: the table is read from global memory (row-local reads, score.cuh).
+// The bookkeeping half of the apply (one thread): route totals, tabu expiries (and the transposed copy),
+// objective, best-so-far, trace record.
+template <bool TABU, class MV, class RV, class ET>
+__device__ __forceinline__ void grid_bookkeeping(const SearchArgs &A, const GridArgs &GA, const MV &M, const RV &R, ET *Et,
+                                                 uint32_t idx, int32_t delta, int cls, const MoveSplit &ms, int it,
+                                                 int n, int S, long long &s_cur, long long &s_best, int &s_best_it,
+                                                 int *ctrl) {
+    move_totals(M, R, idx, ms, it, A.tenure, TABU);
+    if (TABU && Et) {   // the transposed copy gets the same expiries (every CTA, identical values)
+        const uint32_t Rb = (uint32_t)n * (uint32_t)S;
+        if (idx < Rb) {
+            Et[(size_t)ms.a * n + idx / S] = (ET)(it + A.tenure);
+        } else {
+            Et[(size_t)ms.a * n + (idx - Rb) / n] = (ET)(it + A.tenure);
+            Et[(size_t)ms.b * n + (idx - Rb) % n] = (ET)(it + A.tenure);
+        }
+    }
+    const long long c = s_cur + delta;
+    s_cur = c;
+    if (c < s_best) {
+        s_best = c;
+        s_best_it = it;
+        ctrl[1] = 1;
+    }
+    if (blockIdx.x == 0 && A.trace) {
+        as_trace_rec tr;
+        tr.cur = c;
+        tr.best = s_best;
+        tr.idx = idx;
+        tr.delta = delta;
+        tr.cls = cls;
+        tr.it = it;
+        A.trace[it] = tr;
+    }
+}
+
 // PH: the per-iteration phase timers (AS_OPT_PHASE_TIMES) -- a separate instantiation, because even
 // untaken, their live accumulators cost the production kernel ~8 % on C1/C2/C4 (register pressure;
 // profiles/r02/kgrid_phase_ab.jsonl).
@@ -203,6 +239,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     // ---- seeded kick (identical in every CTA) ------------------------------
     __shared__ long long s_cur, s_best, s_start;
     __shared__ int s_best_it, s_kicks;
+    __shared__ int s_ap[8];   // the applied move handed from warp 0 to warp 1: idx, delta, a, b, da, db, stop, class
     if (tid == 0) {
         int kicks = 0;
         if (A.seed != 0 && n > 0) {
@@ -300,10 +337,13 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             else grid.sync();
         }
         if (ph) { ph_u = globaltimer_ns(); ph_sum[2] += ph_u - ph_t; ph_t = ph_u; }
+        // apply (every CTA, identical arithmetic), on two warps: warp 0's lane 0 reads the key, tests the
+        // stop conditions and splits the delta per route (the scorers proved the move valid and
+        // feasible), hands (idx, delta, split) to warp 1 through shared memory and a named barrier, then
+        // relinks; warp 0's lanes refresh the touched incoming-link records.  Meanwhile warp 1's lane 0
+        // updates the route totals, the tabu matrix (and its transpose), the objective and the trace --
+        // disjoint state, so the two halves overlap (the split has read everything they change).
         if (warp == 0) {
-            // apply (every CTA, identical arithmetic): lane 0 splits the delta (from the key: the
-            // scorers proved the move valid and feasible), relinks and updates the route totals and
-            // the tabu matrix; the touched incoming-link records are then refreshed one per lane
             int nt = 0;
             if (lane == 0) {
                 const uint64_t k = GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
@@ -314,42 +354,28 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
                 else if (key_cls(k) == 1 && (!TABU || A.strict_tabu_stop)) stop = TABU ? AS_STOP_NO_MOVE : AS_STOP_LOCAL_OPT;
                 ctrl[0] = stop;
                 ctrl[1] = 0;
+                MoveSplit ms{0, 0, 0, 0};
+                const uint32_t idx = key_idx(k);
+                const int32_t delta = key_delta(k);
                 if (!stop) {
-                    const uint32_t idx = key_idx(k);
-                    const int32_t delta = key_delta(k);
                     if (ph) ph_v = globaltimer_ns();
-                    const MoveSplit ms = move_split(M, R, idx, delta);
+                    ms = move_split(M, R, idx, delta);
                     if (ph) { asm volatile("" ::"r"(ms.a), "r"(ms.da)); ph_u = globaltimer_ns(); ph_sum[5] += ph_u - ph_v; ph_v = ph_u; }
-                    nt = move_relink(M, R, idx, ms.a, ms.b, ctrl + 4);
-                    if (ph) { asm volatile("" ::"r"(nt)); ph_u = globaltimer_ns(); ph_sum[6] += ph_u - ph_v; ph_v = ph_u; }
-                    move_totals(M, R, idx, ms, it, A.tenure, TABU);
-                    if (TABU && Et) {   // the transposed copy gets the same expiries (every CTA, identical values)
-                        const uint32_t Rb = (uint32_t)n * (uint32_t)S;
-                        if (idx < Rb) {
-                            Et[(size_t)ms.a * n + idx / S] = (ET)(it + A.tenure);
-                        } else {
-                            Et[(size_t)ms.a * n + (idx - Rb) / n] = (ET)(it + A.tenure);
-                            Et[(size_t)ms.b * n + (idx - Rb) % n] = (ET)(it + A.tenure);
-                        }
-                    }
-                    const long long c = s_cur + delta;
-                    s_cur = c;
-                    if (c < s_best) {
-                        s_best = c;
-                        s_best_it = it;
-                        ctrl[1] = 1;
-                    }
-                    if (blockIdx.x == 0 && A.trace) {
-                        as_trace_rec tr;
-                        tr.cur = c;
-                        tr.best = s_best;
-                        tr.idx = idx;
-                        tr.delta = delta;
-                        tr.cls = key_cls(k);
-                        tr.it = it;
-                        A.trace[it] = tr;
-                    }
-                    if (ph) { ph_u = globaltimer_ns(); ph_sum[7] += ph_u - ph_v; ph_v = ph_u; }
+                }
+                s_ap[0] = (int)idx; s_ap[1] = delta; s_ap[2] = ms.a; s_ap[3] = ms.b; s_ap[4] = ms.da; s_ap[5] = ms.db;
+                s_ap[6] = stop; s_ap[7] = key_cls(k);
+                __threadfence_block();
+            }
+            __syncwarp();
+            if (nwarps > 1) asm volatile("bar.arrive 1, 64;" ::: "memory");   // hand the split to warp 1
+            if (lane == 0 && !ctrl[0]) {
+                const uint32_t idx = (uint32_t)s_ap[0];
+                nt = move_relink(M, R, idx, s_ap[2], s_ap[3], ctrl + 4);
+                if (ph) { asm volatile("" ::"r"(nt)); ph_u = globaltimer_ns(); ph_sum[6] += ph_u - ph_v; ph_v = ph_u; }
+                if (nwarps == 1) {   // (a one-warp CTA does the bookkeeping itself)
+                    const MoveSplit ms{s_ap[2], s_ap[3], s_ap[4], s_ap[5]};
+                    grid_bookkeeping<TABU>(A, GA, M, R, Et, idx, s_ap[1], s_ap[7], ms, it, n, S, s_cur, s_best, s_best_it,
+                                           ctrl);
                 }
             }
             nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
@@ -357,6 +383,13 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
             __syncwarp();
             if (ph) { ph_u = globaltimer_ns(); ph_sum[8] += ph_u - ph_v; }
+        } else if (warp == 1) {
+            asm volatile("bar.sync 1, 64;" ::: "memory");   // the split is in s_ap
+            if (lane == 0 && !s_ap[6]) {
+                const MoveSplit ms{s_ap[2], s_ap[3], s_ap[4], s_ap[5]};
+                grid_bookkeeping<TABU>(A, GA, M, R, Et, (uint32_t)s_ap[0], s_ap[1], s_ap[7], ms, it, n, S, s_cur, s_best,
+                                       s_best_it, ctrl);
+            }
         }
         __syncthreads();
         if (ph) ph_sum[3] += globaltimer_ns() - ph_t;
