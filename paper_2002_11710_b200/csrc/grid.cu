@@ -53,6 +53,7 @@ __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, 
     // compact swap tiles: the prefix over the row groups (<= n + 1 entries) and, when the list is short
     // (<= GRID_SWT_MAX tiles), the tile table itself (no search per tile)
     const int nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
+    L.RR = o; o = al16(o + (T_smem ? 0 : n * 8));   // cached relocate rows (global-table scorers)
     L.SP = o; o = al16(o + (n + 2) * 4);
     const int64_t nst = (int64_t)nSC * n;
     L.ST = o; o = al16(o + (int)(nst < GRID_SWT_MAX ? nst : GRID_SWT_MAX) * 4);
@@ -272,6 +273,15 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     ET *Et = TABU && !GA.E_smem ? reinterpret_cast<ET *>(GA.Etglobal) : nullptr;
     SC.Et = Et;
     SC.TD = GA.T_smem ? nullptr : I.TDg;   // node costs for the global-table scorers
+    // global table + FAST scorers: each CTA caches the relocate rows' removal side (one global-table read
+    // and four dependent shared loads per row and target chunk otherwise); built here, refreshed for the
+    // two changed routes after every apply
+    int2 *RR = (TR && FULL) ? reinterpret_cast<int2 *>(smem + L.RR) : nullptr;
+    if (RR) {
+        for (int m = tid; m < n; m += blockDim.x) RR[m] = reloc_row_record(Ts, CS4, RS4, LK, VC, F, NL, NLp, I.P, m);
+        __syncthreads();
+    }
+    SC.RR = RR;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
@@ -392,6 +402,14 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             }
         }
         __syncthreads();
+        if (RR && !ctrl[0]) {   // the applied move changed routes a and b only: refresh their rows
+            const int ra = s_ap[2], rb = s_ap[3];
+            for (int m = tid; m < n; m += blockDim.x) {
+                const int v = R.veh[m];
+                if (v == ra || v == rb) RR[m] = reloc_row_record(Ts, CS4, RS4, LK, VC, F, NL, NLp, I.P, m);
+            }
+            __syncthreads();
+        }
         if (ph) ph_sum[3] += globaltimer_ns() - ph_t;
         if (ctrl[0]) break;
         if (ctrl[1] && blockIdx.x == 0)

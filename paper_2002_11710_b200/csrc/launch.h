@@ -68,7 +68,7 @@ struct BatchJob {
 };
 
 struct GridLayout {
-    int T, CS, MH, VC, CH, RS, LK, F, E, red, SP, ST, total;   // shared-memory byte offsets per CTA
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, RR, SP, ST, total;   // shared-memory byte offsets per CTA
 };
 
 struct GridArgs {

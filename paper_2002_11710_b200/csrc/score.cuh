@@ -77,6 +77,8 @@ struct ScoreCtx {
     const ET *E;           // [n][V] tabu expiry (TABU only)
     const ET *Et;          // [V][n] its transpose when E is in global memory (row-local E[m2][a] reads), else null
     const uint16_t *TD;    // global-table scorers (TR): node costs TD[c][x][t] (DevInst::TDg), else null
+    const int2 *RR;        // FAST relocate rows cached per CTA (k_grid, global table): {a, or -1 when the row has
+                           // no feasible relocate; removal delta rem} -- see reloc_row_record; or null
     int n, V, S, NL, NLp, P;
     uint32_t Rb, mask;
     int one, neg;          // 1 and -1, opaque to the compiler (see madd)
@@ -362,17 +364,24 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
         const int m_end = min(m_hi, m0 + FB_ROWS);
         if (K16) bk32 = 0xFFFFFFFFu;
         for (int m = m0; m < m_end; m++) {
-            const int4 rm = RS4[m];
-            const int a = (int16_t)((uint32_t)rm.w >> 16);
-            if (a < 0) continue;
-            const int s = LK[m] & 0xFFFF;
-            const int4 rsx = RS4[s];
-            const int4 csx = CS4[s];
-            const int ca = VC[a] & 0xFF;
-            const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
-            if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
-            const int rem = Dps - rm.y - rsx.y;
-            if (F[a] + rem > P) continue;         // no feasible relocate of m (reading #42)
+            int rem;
+            if (TR && C.RR) {   // the row's removal side, cached per CTA and refreshed after every move
+                const int2 rr = C.RR[m];
+                if (rr.x < 0) continue;
+                rem = rr.y;
+            } else {
+                const int4 rm = RS4[m];
+                const int a = (int16_t)((uint32_t)rm.w >> 16);
+                if (a < 0) continue;
+                const int s = LK[m] & 0xFFFF;
+                const int4 rsx = RS4[s];
+                const int4 csx = CS4[s];
+                const int ca = VC[a] & 0xFF;
+                const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+                if (rm.x + Dps > csx.x) continue;     // link p->s infeasible: every relocate of m is
+                rem = Dps - rm.y - rsx.y;
+                if (F[a] + rem > P) continue;         // no feasible relocate of m (reading #42)
+            }
             const int4 cm = CS4[m];
             const int w_m = cm.x, rowP = TR ? (cm.y & 0xFFFF) * NLp : tsz * (cm.y & 0xFFFF),
                       rowD = tsz * (int)((uint32_t)cm.y >> 16) * tdS;
@@ -616,6 +625,26 @@ __host__ __device__ inline int compact_swap_count(int n, int V, int G) {
     int c = 0;
     for (int g = 0; g < T.nRG; g++) c += swap_chunks_of_group(n, T.nSC, G, g);
     return c;
+}
+
+// The FAST relocate scorer's removal side of row m (score_reloc_fast): {route a, removal delta rem}, or
+// {-1, 0} when m is unassigned, the link p -> s it leaves breaks con7/con8, or route a would stay over the
+// flight limit (reading #42: then no relocate of m is feasible).  Depends only on m's route.
+template <class TT>
+__device__ __forceinline__ int2 reloc_row_record(const TT *Ts, const int4 *CS4, const int4 *RS4, const uint32_t *LK,
+                                                 const uint32_t *VC, const int32_t *F, int NL, int NLp, int P, int m) {
+    const int4 rm = RS4[m];
+    const int a = (int16_t)((uint32_t)rm.w >> 16);
+    if (a < 0) return make_int2(-1, 0);
+    const int s = LK[m] & 0xFFFF;
+    const int4 rsx = RS4[s];
+    const int4 csx = CS4[s];
+    const int ca = VC[a] & 0xFF;
+    const int Dps = (int)Ts[(ca * NL + (rm.w & 0xFFFF)) * NLp + (csx.y & 0xFFFF)] + rsx.z;
+    if (rm.x + Dps > csx.x) return make_int2(-1, 0);
+    const int rem = Dps - rm.y - rsx.y;
+    if (F[a] + rem > P) return make_int2(-1, 0);
+    return make_int2(a, rem);
 }
 
 // One tile of the flat tile list: this lane's best packed key in it.
