@@ -388,7 +388,7 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
             const int svm0 = cm.z, dsvm = cm.w - cm.z, wm_neg = -cm.x;
             const int hmask = MH[m] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
             const int remasp = TABU ? rem - asp : rem;
-            const ET *Erow = TABU ? E + m * V : nullptr;
+            const uint32_t erow = (uint32_t)(m * V);   // 32-bit element index: one IMAD.WIDE per tabu read
             const int remk = (rem + (1 << 23)) * 128 + (m - m0) * KR;            // K16 key base
             const uint32_t base = (uint32_t)m * (uint32_t)S + t0 + lane;        // int32-table index
 #pragma unroll
@@ -405,7 +405,7 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
                 const int e2 = madd(ins, one, remasp);                                // delta - asp (TS) / delta (NS)
                 uint32_t nadm;
                 if (TABU) {
-                    const int e1 = madd(it, neg, (int)Erow[c_b[k]]);                  // E[m][b] - it (>= 0: tabu)
+                    const int e1 = madd(it, neg, (int)E[erow + (uint32_t)c_b[k]]);    // E[m][b] - it (>= 0: tabu)
                     nadm = ~(uint32_t)(e1 | e2) & 0x80000000u;
                 } else {
                     nadm = ~(uint32_t)e2 & 0x80000000u;
@@ -521,15 +521,18 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
             const int sv10 = c1.z, dsv1 = c1.w - c1.z;
             const int cmask = ((vca >> 8) & 1) ? 0 : (int)0x80000000;   // route a cannot fly heli-only missions
             const int hmask = MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
-            const ET *Erow = TABU ? E + m1 * V : nullptr;
+            const uint32_t erow = (uint32_t)(m1 * V);   // 32-bit element indices: one IMAD.WIDE per tabu read
             // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
-            const ET *ecol = TABU ? ((TR && C.Et) ? C.Et + (size_t)a * C.n : E + a) : nullptr;
-            const int estr = (TR && C.Et) ? 1 : V;
+            const ET *ecol = TABU ? ((TR && C.Et) ? C.Et : E) : nullptr;
+            const uint32_t ecol0 = (TR && C.Et) ? (uint32_t)a * (uint32_t)C.n : (uint32_t)a;
+            const uint32_t estr = (TR && C.Et) ? 1u : (uint32_t)V;
             const int keyb = (1 << 30) + sa * 128 + (m1 - w0) * KS;               // K16: (2^23 + asp) << 7 | lid
             const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;   // int32 tables
 #pragma unroll
             for (int k = 0; k < KS; k++) {
-                if (lo + 32 * k + 31 <= m1) continue;     // sub-chunk entirely on or below the diagonal
+                // sub-chunk entirely on or below the diagonal: skipped on the shared-table path; the global-table
+                // path scores it masked (trim < 0), so that the loads of both sub-chunks issue back to back
+                if (!TR && lo + 32 * k + 31 <= m1) continue;
                 const int bf = q_bf[k];
                 const int b = bf & 0xFFFF;
                 const int a_ya1 = madd(row_ya1, one, q_p2m[k]), a_ta2 = madd(row_ta2, one, q_d2[k]);
@@ -553,8 +556,8 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
                 const int mg = (l1 | l2 | l3) | (l4 | mfA | mfB) | (trim | (bf & cmask));
                 uint32_t nadm;
                 if (TABU) {
-                    const int t1 = madd(it, neg, (int)Erow[b]);                                  // E[m1][b] - it
-                    const int t2 = madd(it, neg, (int)ecol[max(mlane + 32 * k, 0) * estr]);      // E[m2][a] - it
+                    const int t1 = madd(it, neg, (int)E[erow + (uint32_t)b]);                    // E[m1][b] - it
+                    const int t2 = madd(it, neg, (int)ecol[ecol0 + (uint32_t)max(mlane + 32 * k, 0) * estr]);  // E[m2][a] - it
                     nadm = ~(uint32_t)((t1 & t2) | dl) & 0x80000000u;
                 } else {
                     nadm = ~(uint32_t)dl & 0x80000000u;
