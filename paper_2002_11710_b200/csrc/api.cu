@@ -802,7 +802,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             const bool e_global = opt_int(ctx, AS_OPT_GRID_E_GLOBAL, 0) == 1;
             for (auto o : gopts) {
                 if ((t_global && o.t) || (e_global && o.e)) continue;
-                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu, tabu);
+                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu, tabu,
+                                           false, 0);   // fits for any rows-per-tile G; resized below for the chosen G
                 if (b <= ctx->max_smem) {
                     GA.T_smem = o.t;
                     GA.E_smem = o.e && tabu;
@@ -858,6 +859,17 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                     if (cost <= best_cost) { best_cost = cost; GA.G = g; }
                 }
                 GA.G = std::max(1, opt_int(ctx, AS_OPT_GRID_G, GA.G));
+                // shared memory for this G (the compact-list prefix and table shrink with it); the global-table
+                // scorers add per-warp swap-row records when they fit
+                {
+                    const int eb = tabu && D.tpad_bytes == 2 ? ebytes : 4;
+                    grid_smem = grid_smem_bytes(n, V, I->NL, I->NC, D.tpad_bytes, eb, GA.T_smem, GA.E_smem, tabu, false,
+                                                GA.G);
+                    const size_t bsr = grid_smem_bytes(n, V, I->NL, I->NC, D.tpad_bytes, eb, GA.T_smem, GA.E_smem, tabu,
+                                                       true, GA.G);
+                    GA.swap_rec = !GA.T_smem && bsr <= ctx->max_smem && opt_int(ctx, AS_OPT_GRID_SWAP_REC, 1) == 1;
+                    if (GA.swap_rec) grid_smem = bsr;
+                }
                 GA.tlo = 0;
                 GA.thi = GA.compact ? grid_tile_count_compact(n, V, GA.G) : grid_tile_count(n, V, GA.G);
                 if (xr) {   // this rank's slice of the tile list (same weighted plan as the sharded kernels)

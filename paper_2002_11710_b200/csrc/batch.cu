@@ -269,7 +269,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     const uint32_t mask = A.mask;
     const uint32_t Rb = (uint32_t)n * (uint32_t)S;
     ScoreCtx<TT, ET> SC;
-    SC.Ts = Ts; SC.Tt = A.inst.tsym ? Ts : reinterpret_cast<const TT *>(A.inst.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E; SC.Et = nullptr; SC.TD = nullptr; SC.RR = nullptr;
+    SC.Ts = Ts; SC.Tt = A.inst.tsym ? Ts : reinterpret_cast<const TT *>(A.inst.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E; SC.Et = nullptr; SC.TD = nullptr; SC.RR = nullptr; SC.SR = nullptr;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = Rb; SC.mask = mask;
     SC.one = A.one; SC.neg = A.neg;
     WinCtx W;

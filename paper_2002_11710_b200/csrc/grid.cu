@@ -36,7 +36,7 @@ constexpr int GRID_SWT_MAX = 4096;   // compact swap tiles held as a table in sh
 namespace airsched {
 
 __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, int NLp, int tbytes, int ebytes,
-                                                  bool T_smem, bool E_smem, bool tabu) {
+                                                  bool T_smem, bool E_smem, bool tabu, bool swap_rec, int G) {
     GridLayout L;
     const int S = n + V;
     int o = 0;
@@ -50,19 +50,23 @@ __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, 
     L.F = o; o = al16(o + V * 4);
     L.E = o; o = al16(o + (tabu && E_smem ? n * V * ebytes : 0));
     L.red = o; o = al16(o + 32 * 8 + 64);
-    // compact swap tiles: the prefix over the row groups (<= n + 1 entries) and, when the list is short
-    // (<= GRID_SWT_MAX tiles), the tile table itself (no search per tile)
-    const int nSC = n > 1 ? (n - 1 + 63) / 64 : 0;
+    // compact swap tiles: the prefix over the row groups (nRG + 1 entries) and, when the list is short
+    // (<= GRID_SWT_MAX tiles), the tile table itself (no search per tile).  G = 0: sized for any G (G = 1)
+    const int Gs = G > 0 ? G : 1;
+    const int nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nRG = (n + Gs - 1) / Gs;
+    int nst = 0;
+    for (int g = 0; g < nRG && nst <= GRID_SWT_MAX; g++) nst += swap_chunks_of_group(n, nSC, Gs, g);
     L.RR = o; o = al16(o + (T_smem ? 0 : n * 8));   // cached relocate rows (global-table scorers)
-    L.SP = o; o = al16(o + (n + 2) * 4);
-    const int64_t nst = (int64_t)nSC * n;
-    L.ST = o; o = al16(o + (int)(nst < GRID_SWT_MAX ? nst : GRID_SWT_MAX) * 4);
+    L.SP = o; o = al16(o + (nRG + 2) * 4);
+    L.ST = o; o = al16(o + (nst <= GRID_SWT_MAX ? nst : 0) * 4);
+    L.SR = o; o = al16(o + (swap_rec ? GRID_WARPS * 2 * SR_ROWS * 16 : 0));   // per-warp swap-row records
     L.total = o;
     return L;
 }
 
-size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu) {
-    return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu).total;
+size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu,
+                       bool swap_rec, int G) {
+    return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu, swap_rec, G).total;
 }
 
 __device__ __forceinline__ bool GT_spread(int ntiles, int nwarps_all) { return ntiles < nwarps_all; }
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         __syncthreads();
     }
     SC.RR = RR;
+    SC.SR = (TR && FULL && GA.swap_rec) ? reinterpret_cast<int4 *>(smem + L.SR) : nullptr;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = NL; SC.NLp = NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;
     SC.mask = A.mask;
     SC.one = A.one; SC.neg = -A.one;
@@ -467,7 +472,8 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
     const DevInst &I = A.inst;
     GA.NLp = padded_stride(I.NL, tbytes);
     const int eb = mode == 1 && tbytes == 2 && GA.ebytes == 2 ? 2 : 4;   // int16 expiries: half the tabu traffic
-    GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, eb, GA.T_smem, GA.E_smem, mode == 1);
+    GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, eb, GA.T_smem, GA.E_smem, mode == 1, GA.swap_rec != 0,
+                       GA.G);
     const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
     cudaError_t err;
     if (mode == 1) {

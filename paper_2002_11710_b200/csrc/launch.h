@@ -68,7 +68,7 @@ struct BatchJob {
 };
 
 struct GridLayout {
-    int T, CS, MH, VC, CH, RS, LK, F, E, red, RR, SP, ST, total;   // shared-memory byte offsets per CTA
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, RR, SP, ST, SR, total;   // shared-memory byte offsets per CTA
 };
 
 struct GridArgs {
@@ -84,6 +84,7 @@ struct GridArgs {
     int G;                         // rows per tile
     int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
     int compact;                   // 1: the list without empty swap tiles (single GPU; score.cuh GridTiles::swp)
+    int swap_rec;                  // 1: per-warp swap-row record scratch in shared memory (ScoreCtx::SR)
     // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
     // and a tag into every peer's symmetric window slot over NVLink and waits (bounded) for the
     // peers' tags of this iteration in its own window (grid.cu rank_exchange)
@@ -123,7 +124,8 @@ void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, i
 int grid_tile_count(int n, int V, int G);
 int grid_tile_count_compact(int n, int V, int G);
 
-size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu);
+size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu,
+                       bool swap_rec, int G);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
                         cudaStream_t st);
 cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, bool transpose,

@@ -79,6 +79,8 @@ struct ScoreCtx {
     const uint16_t *TD;    // global-table scorers (TR): node costs TD[c][x][t] (DevInst::TDg), else null
     const int2 *RR;        // FAST relocate rows cached per CTA (k_grid, global table): {a, or -1 when the row has
                            // no feasible relocate; removal delta rem} -- see reloc_row_record; or null
+    int4 *SR;              // FAST swap rows, per-warp scratch (k_grid, global table): SR_ROWS x 2 int4 per warp,
+                           // filled lane-parallel at the start of each tile -- see score_swap_fast; or null
     int n, V, S, NL, NLp, P;
     uint32_t Rb, mask;
     int one, neg;          // 1 and -1, opaque to the compiler (see madd)
@@ -311,6 +313,7 @@ __device__ __forceinline__ uint64_t score_swap(const ScoreCtx<TT, ET> &C, int hi
 // unsigned min per move, the index recovered at the block's end, window.cuh);
 // with an int32 table it keeps (class << 31 | delta + 2^30) and the index.
 constexpr int FB_ROWS = 32;   // rows per key block (uint16 tables)
+constexpr int SR_ROWS = 16;   // swap rows per per-warp record batch (ScoreCtx::SR)
 
 template <bool TABU, bool TR = false, class TT, class ET>
 __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, int t0, int m_lo, int m_hi, int it,
@@ -496,36 +499,68 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
     const int mlane = lo + lane;
     uint64_t best = KEY_NONE;
     uint32_t bk32 = 0xFFFFFFFFu, bidx = 0;
+    // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
+    const ET *ecol = TABU ? ((TR && C.Et) ? C.Et : E) : nullptr;
+    const uint32_t estr = (TR && C.Et) ? 1u : (uint32_t)V;
+    // the row side of m1 (route a, successor s1): its dynamic part either computed here by the whole warp, or
+    // (TR && C.SR) computed once per row by one lane into the warp's record scratch at the start of each batch
+    int4 *SRw = (TR && C.SR) ? C.SR + (threadIdx.x >> 5) * (2 * SR_ROWS) : nullptr;
+    auto row_side = [&](int m1, int &a, int &ca, int &row_ya1, int &row_ta2, int &ndepc1, int &wsv1, int &ka,
+                        int &slkA, int &cmask, int &hmask) {
+        const int4 r1 = RS4[m1];
+        a = (int16_t)((uint32_t)r1.w >> 16);
+        if (a < 0) return;
+        const int s1 = LK[m1] & 0xFFFF;
+        const int4 rs1 = RS4[s1];
+        const int4 cs1 = CS4[s1];
+        const uint32_t vca = VC[a];
+        ca = vca & 0xFF;
+        row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * tdS);      // T_ca[endc1][.] (TD_ca[endc1][.])
+        row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp                // Tt_ca[pick(s1)][.]
+                     : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF));   // T_ca[.][pick(s1)]
+        ndepc1 = -r1.x;
+        wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
+        ka = rs1.z - r1.y - rs1.y - sa;       // svco(s1) - inc1 - inc(s1) - asp
+        slkA = P - F[a] - sa;
+        cmask = ((vca >> 8) & 1) ? 0 : (int)0x80000000;   // route a cannot fly heli-only missions
+        hmask = MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
+    };
     for (int w0 = m1_lo; w0 < m1_hi; w0 += FB_ROWS) {
         const int w_end = min(m1_hi, w0 + FB_ROWS);
         if (K16) bk32 = 0xFFFFFFFFu;
         for (int m1 = w0; m1 < w_end; m1++) {
-            const int4 r1 = RS4[m1];
-            const int a = (int16_t)((uint32_t)r1.w >> 16);
-            if (a < 0) continue;
-            const int s1 = LK[m1] & 0xFFFF;
+            int a = -1, ca = 0, row_ya1 = 0, row_ta2 = 0, ndepc1 = 0, wsv1 = 0, ka = 0, slkA = 0, cmask = 0, hmask = 0;
+            if (TR && SRw) {
+                const int j = (m1 - w0) % SR_ROWS;
+                if (j == 0) {   // next batch of rows: one lane per row
+                    __syncwarp();
+                    const int mr = m1 + lane;
+                    if (lane < SR_ROWS && mr < w_end) {
+                        row_side(mr, a, ca, row_ya1, row_ta2, ndepc1, wsv1, ka, slkA, cmask, hmask);
+                        SRw[2 * lane] = make_int4(row_ya1, row_ta2, ndepc1, wsv1);
+                        SRw[2 * lane + 1] = make_int4(ka, slkA, a, ca | (cmask ? 0x100 : 0) | (hmask == -1 ? 0x200 : 0));
+                    }
+                    __syncwarp();
+                }
+                const int4 x0 = SRw[2 * j], x1 = SRw[2 * j + 1];
+                a = x1.z;
+                if (a < 0) continue;
+                row_ya1 = x0.x; row_ta2 = x0.y; ndepc1 = x0.z; wsv1 = x0.w;
+                ka = x1.x; slkA = x1.y;
+                ca = x1.w & 0xFF;
+                cmask = (x1.w & 0x100) ? (int)0x80000000 : 0;
+                hmask = (x1.w & 0x200) ? (int)0xFFFFFFFF : 0x3FFFFFFF;
+            } else {
+                row_side(m1, a, ca, row_ya1, row_ta2, ndepc1, wsv1, ka, slkA, cmask, hmask);
+                if (a < 0) continue;
+            }
             const int4 c1 = CS4[m1];
-            const int4 rs1 = RS4[s1];
-            const int4 cs1 = CS4[s1];
-            const uint32_t vca = VC[a];
-            const int ca = vca & 0xFF;
-            const int row_ya1 = tsm + tsz * ((ca * NL + (r1.w & 0xFFFF)) * tdS);  // T_ca[endc1][.] (TD_ca[endc1][.])
-            const int row_ta2 = TR ? (ca * NL + (cs1.y & 0xFFFF)) * NLp            // Tt_ca[pick(s1)][.]
-                                   : tsm + tsz * (ca * NL * NLp + (cs1.y & 0xFFFF)); // T_ca[.][pick(s1)]
             const int rowp1 = TR ? (c1.y & 0xFFFF) * NLp : tsz * (c1.y & 0xFFFF);
             const int row_tb2 = tsz * (int)((uint32_t)c1.y >> 16) * NLp;
-            const int ndepc1 = -r1.x, w1 = c1.x;
-            const int wsv1 = cs1.x - rs1.z;                 // w(s1) - svco(s1)
-            const int ka = rs1.z - r1.y - rs1.y - sa;       // svco(s1) - inc1 - inc(s1) - asp
-            const int slkA = P - F[a] - sa;
+            const int w1 = c1.x;
             const int sv10 = c1.z, dsv1 = c1.w - c1.z;
-            const int cmask = ((vca >> 8) & 1) ? 0 : (int)0x80000000;   // route a cannot fly heli-only missions
-            const int hmask = MH[m1] ? (int)0xFFFFFFFF : 0x3FFFFFFF;
             const uint32_t erow = (uint32_t)(m1 * V);   // 32-bit element indices: one IMAD.WIDE per tabu read
-            // E[m2][a] over the lanes: a column of E, or (global tables, TR) a row of its transpose
-            const ET *ecol = TABU ? ((TR && C.Et) ? C.Et : E) : nullptr;
             const uint32_t ecol0 = (TR && C.Et) ? (uint32_t)a * (uint32_t)C.n : (uint32_t)a;
-            const uint32_t estr = (TR && C.Et) ? 1u : (uint32_t)V;
             const int keyb = (1 << 30) + sa * 128 + (m1 - w0) * KS;               // K16: (2^23 + asp) << 7 | lid
             const uint32_t base = Rb + (uint32_t)m1 * (uint32_t)n + lo + lane;   // int32 tables
 #pragma unroll

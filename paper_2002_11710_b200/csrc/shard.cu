@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(768, 1) k_shard_eval(SearchArgs A, ShardViews 
     SC.Tt = A.inst.tsym ? SC.Ts : reinterpret_cast<const TT *>(A.inst.TpadT);
     SC.TD = sizeof(TT) == 2 ? A.inst.TDg : nullptr;
     SC.RR = nullptr;
+    SC.SR = nullptr;
     SC.CS4 = SV.CS4; SC.MH = SV.MH; SC.VC = SV.VC; SC.RS4 = SV.RS4;
     SC.LK = SV.LK; SC.F = SV.F; SC.E = SV.E; SC.Et = nullptr;
     SC.n = n; SC.V = V; SC.S = S; SC.NL = I.NL; SC.NLp = SV.NLp; SC.P = I.P; SC.Rb = (uint32_t)n * (uint32_t)S;

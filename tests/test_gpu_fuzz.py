@@ -97,6 +97,8 @@ PATHS = {
     "k_grid_all": {"GRID": 1},
     "k_grid_tglobal": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_G": 2},
     "k_grid_teglobal": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1},
+    "k_grid_tglobal_g20": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1, "GRID_G": 20},   # > SR_ROWS rows
+    "k_grid_tglobal_norec": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_SWAP_REC": 0},
     "k_batch": {"BATCH_KERNEL": 1},
     "sharded2": {"SHARDED": 1, "SHARD_EMULATE": 2, "SHARD_K": 3},
 }

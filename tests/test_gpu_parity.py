@@ -395,6 +395,8 @@ def test_surge_run_parity_prefix(A, ctx, oracle_mod):
     p, m = start_of(O, inst)
     _compare_run(A, ctx, O, h, p, m, 1, 10, 3)
     _compare_run(A, ctx, O, h, p, m, 0, 0, 2)
+    with ctx.options(GRID_SWAP_REC=0):   # the swap rows' dynamic part computed by the whole warp
+        _compare_run(A, ctx, O, h, p, m, 1, 10, 3)
 
 
 # ------------------------------------------------- sharded single instance (C5) --

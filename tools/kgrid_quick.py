@@ -1,4 +1,5 @@
-"""Quick TS timings of the whole-GPU kernel on C1/C2/C4 (median of 7 runs) -- for A/B of builds."""
+"""Quick TS timings of the whole-GPU kernel on C1/C2/C4/C5 (median of 7 runs) -- for A/B of builds.
+usage: kgrid_quick.py TAG [OPTION=VALUE ...]"""
 import json
 import os
 import sys
@@ -11,6 +12,9 @@ def main():
     from paper_2002_11710_b200 import instgen
     tag = sys.argv[1] if len(sys.argv) > 1 else ""
     ctx = A.Ctx(0)
+    for kv in sys.argv[2:]:   # NAME=VALUE context options (airsched.OPTIONS)
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     for name, iters in (("tiny", 200), ("ontario", 5000), ("large", 3000), ("surge", 200)):
         inst = instgen.generate(name)
         h = A.Instance(inst)
