@@ -326,7 +326,9 @@ __device__ __forceinline__ uint64_t score_reloc_fast(const ScoreCtx<TT, ET> &C, 
     const int32_t *F = C.F;
     const ET *E = C.E;
     const int V = C.V, S = C.S, NL = C.NL, NLp = C.NLp, P = C.P;
-    const int one = C.one, neg = C.neg;
+    // global tables (TR): every table read adds an IMAD.WIDE on the FMA pipe, which then saturates first --
+    // the sums go back to the ALU pipe there (one and neg known to the compiler)
+    const int one = TR ? 1 : C.one, neg = TR ? -1 : C.neg;
     int c_t1[KR], c_t2[KR], c_dw[KR], c_k[KR], c_wsv[KR], c_slk[KR], c_b[KR], c_cb[KR];
     // shared table (TR false): cached offsets are byte addresses in the shared window
     const int tsm = TR ? 0 : (int)__cvta_generic_to_shared(Ts), tsz = TR ? 1 : (int)sizeof(TT);
@@ -448,7 +450,9 @@ __device__ __forceinline__ uint64_t score_swap_fast(const ScoreCtx<TT, ET> &C, i
     const ET *E = C.E;
     const int n = C.n, V = C.V, NL = C.NL, NLp = C.NLp, P = C.P;
     const uint32_t Rb = C.Rb;
-    const int one = C.one, neg = C.neg;
+    // global tables (TR): every table read adds an IMAD.WIDE on the FMA pipe, which then saturates first --
+    // the sums go back to the ALU pipe there (one and neg known to the compiler)
+    const int one = TR ? 1 : C.one, neg = TR ? -1 : C.neg;
     const int lo = hi - 32 * KS;
     const int sa = TABU ? asp : 0;   // aspiration folded into route a's terms: "dl" below is delta - asp
     // m2-side cache; q_bf = b | heli_only(m2) << 31; q_slk carries the heli offset
