@@ -842,12 +842,11 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 }
                 // rows per tile: the tiles go round-robin over the warps, so an iteration costs about
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
-                // set-up of ~1.5 rows: measured G sweep, profiles/r02/grid_g_sweep_compact.jsonl), the
-                // larger G on ties.  A global table caps G at 10 so a row group's table rows
-                // (~3.4 KB per row at C5) stay L1-resident (measured: profiles/r02/kgrid_ab.jsonl).
+                // set-up of ~1.5 rows: measured G sweeps, profiles/r02/grid_g_sweep_*.jsonl), the larger G
+                // on ties; at most 32 rows (one key block).
                 const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS * (xr ? xr->nranks : 1);
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
-                const int gmax = GA.T_smem ? 256 : 10;
+                const int gmax = GA.T_smem ? 256 : 32;
                 double best_cost = 1e300;
                 GA.G = 1;
                 GA.compact = xr ? 0 : opt_int(ctx, AS_OPT_GRID_COMPACT, 1);   // one GPU: no empty swap tiles (score.cuh)
