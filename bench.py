@@ -95,7 +95,8 @@ def onchip_roofline(relocs, swaps, t_s, f_mhz, n_gpus=1, workload=None):
     prof = measured_profile(workload) if workload else {}
     if prof:   # hardware counters of the committed ncu capture of this workload's dominant kernel
         hw = {"source": prof.get("source"), "issue_slots_busy": prof.get("issue_slots_busy"),
-              "alu_fma_pipe": [prof.get("alu_pipe"), prof.get("fma_pipe")]}
+              "alu_fma_pipe": [prof.get("alu_pipe"), prof.get("fma_pipe")],
+              "fmaheavy_pipe": prof.get("fmaheavy_pipe")}   # IMAD's half-rate pipe
         if "shared_wavefronts" in prof and "duration_ms" in prof:
             gbps = prof["shared_wavefronts"] * 128 / (prof["duration_ms"] / 1e3) / 1e9
             hw["shared_wavefront_GBps"] = gbps

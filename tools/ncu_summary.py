@@ -34,6 +34,8 @@ def main(rep, key, label, note, details_out):
            "issue_slots_busy": pct("sm__inst_issued.avg.pct_of_peak_sustained_active"),
            "alu_pipe": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
            "fma_pipe": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+           # IMAD / IMAD.WIDE issue to the FMA-heavy half at half rate: the busier FMA half
+           "fmaheavy_pipe": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
            "warp_instructions_per_launch": d["smsp__inst_executed.sum"][0],
            "shared_wavefronts": d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][0],
            "shared_bank_conflict_wavefronts": d["l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"][0],
