@@ -783,7 +783,8 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     int grid_blocks = 0;
     if (xr && !(single && compact_ok && !P->sweep))
         return fail(AS_ERR_UNSUPPORTED, "fused sharded run needs the compact layout");
-    if (single && compact_ok && !P->sweep) {
+    // the whole-GPU kernel also runs the no-wait variant (general scorers, engine.cuh's exact evaluation)
+    if (single && (compact_ok || (compact_fits && I->no_wait && !xr)) && !P->sweep) {
         const int want_grid = xr ? 1 : opt_int(ctx, AS_OPT_GRID, -1);
         const bool kfits = kfit;
         // CTAs: one per single-row tile up to the SM count (an iteration's floor is one tile's
@@ -800,16 +801,22 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
             struct Opt { bool t, e; } gopts[4] = {{true, true}, {true, false}, {false, true}, {false, false}};
             const bool t_global = opt_int(ctx, AS_OPT_GRID_T_GLOBAL, 0) == 1;   // test options
             const bool e_global = opt_int(ctx, AS_OPT_GRID_E_GLOBAL, 0) == 1;
-            for (auto o : gopts) {
-                if ((t_global && o.t) || (e_global && o.e)) continue;
-                size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu, tabu,
-                                           false, 0);   // fits for any rows-per-tile G; resized below for the chosen G
-                if (b <= ctx->max_smem) {
-                    GA.T_smem = o.t;
-                    GA.E_smem = o.e && tabu;
-                    grid_smem = b;
-                    use_grid = true;
-                    break;
+            // fits for any rows-per-tile G (the compact-list prefix sized for G = 1), else for G >= 16 (the G
+            // chosen below is then at least 16); resized below for the chosen G
+            int gfit = 1;
+            for (int pass = 0; pass < 2 && !use_grid; pass++) {
+                gfit = pass ? 16 : 1;
+                for (auto o : gopts) {
+                    if ((t_global && o.t) || (e_global && o.e)) continue;
+                    size_t b = grid_smem_bytes(n, V, I->NL, I->NC, tb, tabu && tb == 2 ? ebytes : 4, o.t, o.e && tabu,
+                                               tabu, false, gfit, I->no_wait != 0);
+                    if (b <= ctx->max_smem) {
+                        GA.T_smem = o.t;
+                        GA.E_smem = o.e && tabu;
+                        grid_smem = b;
+                        use_grid = true;
+                        break;
+                    }
                 }
             }
             if (use_grid) {
@@ -823,7 +830,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 GA.Tglobal = D.Tpad;
                 void *p;
                 GA.phase_ns = nullptr;
-                if (opt_int(ctx, AS_OPT_PHASE_TIMES, 0) == 1) {
+                if (opt_int(ctx, AS_OPT_PHASE_TIMES, 0) == 1 && !I->no_wait) {   // (no phase timers for no-wait)
                     if ((st = scratch(ctx, "g_phase", 10 * 8, &p)) != AS_OK) return st;
                     CUDA_TRY(cudaMemsetAsync(p, 0, 10 * 8, ctx->stream));
                     GA.phase_ns = (unsigned long long *)p;
@@ -848,25 +855,26 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
                 const int gmax = GA.T_smem ? 256 : 32;
                 double best_cost = 1e300;
-                GA.G = 1;
                 GA.compact = xr ? 0 : opt_int(ctx, AS_OPT_GRID_COMPACT, 1);   // one GPU: no empty swap tiles (score.cuh)
-                for (int g = 1; g <= gmax && g <= std::max(1, n); g++) {
+                GA.G = gfit;
+                for (int g = gfit; g <= std::max(gmax, gfit) && g <= std::max(gfit, n); g++) {
                     const int64_t tiles = GA.compact ? (int64_t)grid_tile_count_compact(n, V, g)
                                                      : (nTC + nSC) * ((n + g - 1) / g) + nAdj;
                     const int64_t rounds = (tiles + warps_all - 1) / warps_all;
                     const double cost = (double)rounds * g + 1.5 * (double)rounds;   // per-tile set-up ~1.5 rows
                     if (cost <= best_cost) { best_cost = cost; GA.G = g; }
                 }
-                GA.G = std::max(1, opt_int(ctx, AS_OPT_GRID_G, GA.G));
+                GA.G = std::max(gfit, opt_int(ctx, AS_OPT_GRID_G, GA.G));
                 // shared memory for this G (the compact-list prefix and table shrink with it); the global-table
                 // scorers add per-warp swap-row records when they fit
                 {
                     const int eb = tabu && D.tpad_bytes == 2 ? ebytes : 4;
+                    const bool nw = I->no_wait != 0;
                     grid_smem = grid_smem_bytes(n, V, I->NL, I->NC, D.tpad_bytes, eb, GA.T_smem, GA.E_smem, tabu, false,
-                                                GA.G);
+                                                GA.G, nw);
                     const size_t bsr = grid_smem_bytes(n, V, I->NL, I->NC, D.tpad_bytes, eb, GA.T_smem, GA.E_smem, tabu,
-                                                       true, GA.G);
-                    GA.swap_rec = !GA.T_smem && bsr <= ctx->max_smem && opt_int(ctx, AS_OPT_GRID_SWAP_REC, 1) == 1;
+                                                       true, GA.G, nw);
+                    GA.swap_rec = !GA.T_smem && !nw && bsr <= ctx->max_smem && opt_int(ctx, AS_OPT_GRID_SWAP_REC, 1) == 1;
                     if (GA.swap_rec) grid_smem = bsr;
                 }
                 GA.tlo = 0;

@@ -36,7 +36,8 @@ constexpr int GRID_SWT_MAX = 4096;   // compact swap tiles held as a table in sh
 namespace airsched {
 
 __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, int NLp, int tbytes, int ebytes,
-                                                  bool T_smem, bool E_smem, bool tabu, bool swap_rec, int G) {
+                                                  bool T_smem, bool E_smem, bool tabu, bool swap_rec, int G,
+                                                  bool nw) {
     GridLayout L;
     const int S = n + V;
     int o = 0;
@@ -56,17 +57,19 @@ __host__ __device__ inline GridLayout grid_layout(int n, int V, int NL, int NC, 
     const int nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nRG = (n + Gs - 1) / Gs;
     int nst = 0;
     for (int g = 0; g < nRG && nst <= GRID_SWT_MAX; g++) nst += swap_chunks_of_group(n, nSC, Gs, g);
-    L.RR = o; o = al16(o + (T_smem ? 0 : n * 8));   // cached relocate rows (global-table scorers)
+    L.RR = o; o = al16(o + (T_smem || nw ? 0 : n * 8));   // cached relocate rows (global-table FAST scorers)
     L.SP = o; o = al16(o + (nRG + 2) * 4);
     L.ST = o; o = al16(o + (nst <= GRID_SWT_MAX ? nst : 0) * 4);
     L.SR = o; o = al16(o + (swap_rec ? GRID_WARPS * 2 * SR_ROWS * 16 : 0));   // per-warp swap-row records
+    L.NR = o; o = al16(o + (nw ? S * 16 : 0));   // no-wait: {arrival, suffix slack, position} per slot
     L.total = o;
     return L;
 }
 
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu,
-                       bool swap_rec, int G) {
-    return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu, swap_rec, G).total;
+                       bool swap_rec, int G, bool nw) {
+    return grid_layout(n, V, NL, NC, padded_stride(NL, tbytes), tbytes, ebytes, T_smem, E_smem, tabu, swap_rec, G,
+                       nw).total;
 }
 
 __device__ __forceinline__ bool GT_spread(int ntiles, int nwarps_all) { return ntiles < nwarps_all; }
@@ -152,8 +155,11 @@ __device__ __forceinline__ void grid_bookkeeping(const SearchArgs &A, const Grid
 // PH: the per-iteration phase timers (AS_OPT_PHASE_TIMES) -- a separate instantiation, because even
 // untaken, their live accumulators cost the production kernel ~8 % on C1/C2/C4 (register pressure;
 // profiles/r02/kgrid_phase_ab.jsonl).
-template <bool TABU, class TT, class ET, bool FULL, bool TR, bool PH>
+// NW: the no-wait variant (f3, reading #40): every move by the engine's exact evaluation (general
+// scorers), per-slot {arrival, suffix slack, position} records, whole-route refresh of the two changed routes.
+template <bool TABU, class TT, class ET, bool FULL, bool TR, bool PH, bool NW = false>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
+    static_assert(!NW || (!FULL && !PH), "the no-wait variant runs the general scorers, without phase timers");
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
     const DevInst &I = A.inst;
@@ -209,6 +215,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
     R.pick_s.base = reinterpret_cast<unsigned char *>(CS4); R.w_s.base = reinterpret_cast<unsigned char *>(CS4);
     R.F = F; R.E = E;
+    R.arr.base = R.sl.base = R.pos.base = NW ? smem + L.NR : nullptr;
 
     // ---- start schedule -> replica (every CTA) -----------------------------
     for (int x = tid; x < S; x += blockDim.x) R.veh[x] = x < n ? (int16_t)-1 : (int16_t)(x - n);
@@ -232,7 +239,11 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         R.pred[n + v] = (uint16_t)prev;
     }
     __syncthreads();
-    for (int x = tid; x < S; x += blockDim.x) refresh_slot(M, R, x);
+    if constexpr (NW) {   // whole routes: incoming links, arrivals, positions, suffix slacks (engine.cuh)
+        for (int v = tid; v < V; v += blockDim.x) nw_refresh_route(M, R, v);
+    } else {
+        for (int x = tid; x < S; x += blockDim.x) refresh_slot(M, R, x);
+    }
     __syncthreads();
     for (int v = tid; v < V; v += blockDim.x) {
         int f = 0, x = R.succ[n + v];
@@ -253,9 +264,9 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             for (int k = 0; k < A.kick; k++)
                 for (int tr = 0; tr < 64; tr++) {
                     uint32_t idx = (uint32_t)(splitmix64_next(s) % Rb);
-                    MoveEval e = eval_index(M, R, idx, 0xFu, 0);
+                    MoveEval e = eval_index<NW>(M, R, idx, 0xFu, 0);
                     if (e.valid && e.feasible) {
-                        apply_move(M, R, idx, e, 0, 0, false);
+                        apply_move<NW>(M, R, idx, e, 0, 0, false);
                         kicks++;
                         break;
                     }
@@ -327,7 +338,8 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
         if (ph) ph_t = globaltimer_ns();
-        uint64_t kmin = score_tiles<TABU, FULL, TR>(SC, M, R, GT, GA.tlo, GA.thi, gwarp, nwarps_all, it, cur, best, lane);
+        uint64_t kmin = score_tiles<TABU, FULL, TR, NW>(SC, M, R, GT, GA.tlo, GA.thi, gwarp, nwarps_all, it, cur, best,
+                                                        lane);
         kmin = wmin(kmin);
         if (ph) { ph_u = globaltimer_ns(); ph_sum[0] += ph_u - ph_t; ph_t = ph_u; }
         if (lane == 0) red[warp] = kmin;
@@ -395,7 +407,11 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
             }
             nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
             __syncwarp();
-            if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
+            if constexpr (NW) {   // the two changed routes, one lane each (s_ap: routes a, b)
+                if (!ctrl[0] && lane < 2 && (lane == 0 || s_ap[3] != s_ap[2])) nw_refresh_route(M, R, s_ap[2 + lane]);
+            } else {
+                if (lane < nt) refresh_slot(M, R, ctrl[4 + lane]);
+            }
             __syncwarp();
             if (ph) { ph_u = globaltimer_ns(); ph_sum[8] += ph_u - ph_v; }
         } else if (warp == 1) {
@@ -459,6 +475,9 @@ static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks,
                             cudaStream_t st) {
     auto kern = GA.phase_ns ? (GA.T_smem ? k_grid<TABU, TT, ET, FULL, false, true> : k_grid<TABU, TT, ET, FULL, true, true>)
                             : (GA.T_smem ? k_grid<TABU, TT, ET, FULL, false, false> : k_grid<TABU, TT, ET, FULL, true, false>);
+    if constexpr (!FULL)   // the no-wait variant (general scorers; no phase-timer instantiation)
+        if (A.inst.no_wait)
+            kern = GA.T_smem ? k_grid<TABU, TT, ET, false, false, false, true> : k_grid<TABU, TT, ET, false, true, false, true>;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     SearchArgs a = A;
@@ -473,8 +492,8 @@ cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, 
     GA.NLp = padded_stride(I.NL, tbytes);
     const int eb = mode == 1 && tbytes == 2 && GA.ebytes == 2 ? 2 : 4;   // int16 expiries: half the tabu traffic
     GA.L = grid_layout(I.n, I.V, I.NL, I.NC, GA.NLp, tbytes, eb, GA.T_smem, GA.E_smem, mode == 1, GA.swap_rec != 0,
-                       GA.G);
-    const bool full = (A.mask & 15u) == 15u && A.inst.svcpos;
+                       GA.G, I.no_wait != 0);
+    const bool full = (A.mask & 15u) == 15u && A.inst.svcpos && !A.inst.no_wait;
     cudaError_t err;
     if (mode == 1) {
         if (tbytes == 2 && eb == 2)

@@ -68,7 +68,7 @@ struct BatchJob {
 };
 
 struct GridLayout {
-    int T, CS, MH, VC, CH, RS, LK, F, E, red, RR, SP, ST, SR, total;   // shared-memory byte offsets per CTA
+    int T, CS, MH, VC, CH, RS, LK, F, E, red, RR, SP, ST, SR, NR, total;   // shared-memory byte offsets per CTA
 };
 
 struct GridArgs {
@@ -125,7 +125,7 @@ int grid_tile_count(int n, int V, int G);
 int grid_tile_count_compact(int n, int V, int G);
 
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu,
-                       bool swap_rec, int G);
+                       bool swap_rec, int G, bool nw);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,
                         cudaStream_t st);
 cudaError_t launch_pad_table(const int32_t *T, void *out, int NC, int NL, int NLp, int tbytes, bool transpose,

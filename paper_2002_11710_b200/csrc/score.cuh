@@ -689,8 +689,55 @@ __device__ __forceinline__ int2 reloc_row_record(const TT *Ts, const int4 *CS4, 
     return make_int2(a, rem);
 }
 
+// No-wait variant (f3) tiles: every move by the engine's exact evaluation (engine.cuh reloc_eval /
+// swap_eval with NW), m warp-uniform, lanes over the targets t of the chunk / the m2 of the swap chunk
+// (m2 > m1, adjacent pairs included: swap_eval is exact for them, so no adjacent-pair tiles are needed).
+template <bool TABU, class TT, class ET, class MV, class RV>
+__device__ __forceinline__ uint64_t score_reloc_nw(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R, int t0,
+                                                   int m_lo, int m_hi, int it, long long cur, long long best,
+                                                   int lane) {
+    uint64_t kb = KEY_NONE;
+    for (int m = m_lo; m < m_hi; m++) {
+        const RelocRow r = reloc_row(M, R, m);
+        if (r.a < 0) continue;
+#pragma unroll
+        for (int k = 0; k < KR; k++) {
+            const int t = t0 + lane + 32 * k;
+            if (t >= SC.S) continue;
+            const MoveEval e = reloc_eval<true>(M, R, r, m, t, SC.mask, it);
+            const int cls = move_class<TABU>(e, cur, best);
+            if (cls >= 0) {
+                const uint64_t key = make_key(cls, e.delta, (uint32_t)m * (uint32_t)SC.S + (uint32_t)t);
+                kb = key < kb ? key : kb;
+            }
+        }
+    }
+    return kb;
+}
+
+template <bool TABU, class TT, class ET, class MV, class RV>
+__device__ __forceinline__ uint64_t score_swap_nw(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R, int hi,
+                                                  int m1_lo, int m1_hi, int it, long long cur, long long best,
+                                                  int lane) {
+    uint64_t kb = KEY_NONE;
+    for (int m1 = m1_lo; m1 < m1_hi; m1++) {
+#pragma unroll
+        for (int k = 0; k < KS; k++) {
+            const int m2 = hi - 32 * KS + lane + 32 * k;
+            if (m2 <= m1) continue;
+            const MoveEval e = swap_eval<true>(M, R, m1, m2, SC.mask, it);
+            const int cls = move_class<TABU>(e, cur, best);
+            if (cls >= 0) {
+                const uint64_t key = make_key(cls, e.delta, SC.Rb + (uint32_t)m1 * (uint32_t)SC.n + (uint32_t)m2);
+                kb = key < kb ? key : kb;
+            }
+        }
+    }
+    return kb;
+}
+
 // One tile of the flat tile list: this lane's best packed key in it.
-template <bool TABU, bool FULL, bool TR, class TT, class ET, class MV, class RV>
+template <bool TABU, bool FULL, bool TR, bool NW = false, class TT, class ET, class MV, class RV>
 __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
                                                const GridTiles &GT, int tile, int it, long long cur, long long best,
                                                int lane) {
@@ -701,8 +748,9 @@ __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const
         if (tile < GT.n_reloc) {
             const int c = tile % GT.nTC, g = tile / GT.nTC;
             const int m_lo = g * GT.G, m_hi = min(n, m_lo + GT.G);
-            kb = FULL ? score_reloc_fast<TABU, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane)
-                      : score_reloc<TABU, FULL, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
+            if constexpr (NW) kb = score_reloc_nw<TABU>(SC, M, R, c * 32 * KR, m_lo, m_hi, it, cur, best, lane);
+            else kb = FULL ? score_reloc_fast<TABU, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane)
+                           : score_reloc<TABU, FULL, TR>(SC, c * 32 * KR, m_lo, m_hi, it, asp, lane);
         } else if (tile < GT.n_reloc + GT.n_swap) {
             const int r = tile - GT.n_reloc;
             int j, g;
@@ -724,10 +772,12 @@ __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const
             }
             const int hi = n - j * 32 * KS;
             const int m_lo = g * GT.G, m_hi = min(hi - 1, m_lo + GT.G);
-            if (m_lo < m_hi)
-                kb = FULL ? score_swap_fast<TABU, TR>(SC, hi, m_lo, m_hi, it, asp, lane)
-                          : score_swap<TABU, FULL, TR>(SC, hi, m_lo, m_hi, it, asp, lane);
-        } else {
+            if (m_lo < m_hi) {
+                if constexpr (NW) kb = score_swap_nw<TABU>(SC, M, R, hi, m_lo, m_hi, it, cur, best, lane);
+                else kb = FULL ? score_swap_fast<TABU, TR>(SC, hi, m_lo, m_hi, it, asp, lane)
+                               : score_swap<TABU, FULL, TR>(SC, hi, m_lo, m_hi, it, asp, lane);
+            }
+        } else if (!NW) {
             const int x = (tile - GT.n_reloc - GT.n_swap) * 32 + lane;
             if (x < n && (FULL || (SC.mask & 8u))) {
                 const int gg = SC.LK[x] & 0xFFFF;
@@ -744,13 +794,13 @@ __device__ __forceinline__ uint64_t score_tile(const ScoreCtx<TT, ET> &SC, const
 }
 
 // Score tiles [tlo, thi) of the flat tile list with stride over the warps of the grid.
-template <bool TABU, bool FULL, bool TR, class TT, class ET, class MV, class RV>
+template <bool TABU, bool FULL, bool TR, bool NW = false, class TT, class ET, class MV, class RV>
 __device__ __forceinline__ uint64_t score_tiles(const ScoreCtx<TT, ET> &SC, const MV &M, const RV &R,
                                                 const GridTiles &GT, int tlo, int thi, int gwarp, int nwarps_all,
                                                 int it, long long cur, long long best, int lane) {
     uint64_t kmin = KEY_NONE;
     for (int tile = tlo + gwarp; tile < thi; tile += nwarps_all) {
-        const uint64_t kb = score_tile<TABU, FULL, TR>(SC, M, R, GT, tile, it, cur, best, lane);
+        const uint64_t kb = score_tile<TABU, FULL, TR, NW>(SC, M, R, GT, tile, it, cur, best, lane);
         kmin = kb < kmin ? kb : kmin;
     }
     return kmin;

@@ -241,3 +241,51 @@ def test_nowait_batch_kernel_traces(A, ctx, oracle_mod, ctxopt):
             k = o["iters_done"]
             assert res[r]["iters_done"] == k and res[r]["best_obj"] == o["best_obj"]
             assert (tr[r]["idx"][:k] == o["trace"]["idx"]).all() and (tr[r]["cur"][:k] == o["trace"]["cur"]).all()
+
+
+@pytest.mark.parametrize("cfg,scale,iters,opts", [
+    ("tiny", 1.0, 200, {"GRID": 1}),
+    ("tiny", 0.3, 200, {"GRID": 1, "GRID_BLOCKS": 1}),
+    ("ontario", 1.0, 800, {"GRID": 1}),
+    ("ontario", 0.6, 600, {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_G": 3}),
+    ("batched", 0.5, 400, {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1}),
+    ("batched", 0.5, 300, {"GRID": 1, "GRID_COMPACT": 0, "GRID_G": 7}),
+    ("large", 1.0, 40, {"GRID": 1}),
+])
+def test_nowait_grid_runs(A, ctx, oracle_mod, cfg, scale, iters, opts, ctxopt):
+    """f3 on the whole-GPU kernel (k_grid<..., NW>: general scorers with the engine's exact
+    no-wait evaluation, whole-route refresh of the two changed routes): full traces, final tabu
+    matrix, best schedule, TS (plain and kicked) and NS, against the oracle -- shared and global
+    tables, one CTA and the whole grid, compact and full tile lists."""
+    ctxopt(**opts)
+    inst = nowait(cfg, scale)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    st, (p, m), _, _ = O.greedy()
+    assert st == 0
+    t = instgen.CONFIGS[cfg].tenure
+    _compare_run(A, ctx, O, h, p, m, 1, t, iters)
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    _compare_run(A, ctx, O, h, p, m, 1, t, max(iters // 2, 1), seed=17, kick=8)
+
+
+def test_nowait_grid_surge_prefix(A, ctx, oracle_mod):
+    """C5-sized no-wait instance (n=4000, V=100) on the whole-GPU kernel (it holds no on-chip copy
+    for the per-CTA kernel): the first TS and NS iterations equal the oracle's (chunk-parallel
+    driver of the same arithmetic, tests/test_oracle_driver.py)."""
+    import os
+    inst = nowait("surge")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    st, (p, m), _, _ = O.greedy()
+    assert st == 0
+    for mode, tenure, iters in ((1, 10, 4), (0, 0, 3)):
+        prm = A.params(mode=mode, tenure=tenure, max_iters=iters, trace_level=1)
+        g = A.as_tabu_run(ctx, h, p, m, prm, want_trace=True, want_tabu=(mode == 1))
+        o = O.search_par(p, m, mode=mode, tenure=tenure, max_iters=iters, threads=os.cpu_count(), memo=True)
+        assert g["iters_done"] == o["iters_done"] and g["stop_reason"] == o["stop_reason"]
+        for k in ("idx", "delta", "cur", "best", "cls"):
+            assert (g["trace"][k] == o["trace"][k]).all(), k
+        if mode == 1:
+            assert (g["tabu"] == o["E"]).all()
+        assert routes_of(*g["best"]) == routes_of(*o["best"])

@@ -49,3 +49,21 @@ def test_par_driver_masks_and_tiny_instances(oracle_mod):
                 ref = O.search(p, m, mode=mode, tenure=2, max_iters=40, mask=mask)
                 got = O.search_par(p, m, mode=mode, tenure=2, max_iters=40, mask=mask, threads=4, memo=True)
                 same(got, ref)
+
+
+@pytest.mark.parametrize("name,scale,iters", [("ontario", 0.6, 300), ("batched", 0.5, 120)])
+def test_par_driver_nowait(oracle_mod, name, scale, iters):
+    """The no-wait variant (f3): a move's feasibility then depends on the whole of its two routes
+    (arrival shifts), still only on those -- the memo stays valid; traces equal the plain driver's."""
+    import dataclasses
+    inst = instgen.generate(name)
+    w = np.maximum(1, np.floor(inst.deadline_s * scale)).astype(np.int32)
+    inst = dataclasses.replace(inst, no_wait=1, deadline_s=w)
+    O = oracle_mod.Oracle(inst)
+    st, (p, m), _, _ = O.greedy()
+    assert st == 0
+    for kw in (dict(mode=1, tenure=instgen.CONFIGS[name].tenure), dict(mode=0),
+               dict(mode=1, tenure=5, seed=3, kick=6)):
+        ref = O.search(p, m, max_iters=iters, **kw)
+        for threads, memo in ((3, True), (8, False)):
+            same(O.search_par(p, m, max_iters=iters, threads=threads, memo=memo, **kw), ref)
