@@ -417,25 +417,43 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
                     }
                 }
         } else {
-        // Per-lane best inside a tile (score.cuh); tiles merged through the 64-bit key.
-        // ============================ relocate block ============================
-        for (int t0 = 0; t0 < S; t0 += 32 * KR) {
-            uint64_t kb;
-            if constexpr (WIN) kb = score_reloc_win<TABU, FULL>(SC, W, t0, 0, n, it, asp, lane);
-            else kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
-                           : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
-            kmin = kb < kmin ? kb : kmin;
+        // Per-lane best inside a tile (score.cuh); tiles merged through the 64-bit key.  The window scorers
+        // with positive legs run their one-sign-bit form first (F1, window.cuh) and the exact form only when
+        // that finds no admissible feasible move (class 1 or none: the by-default move, a local optimum)
+        auto score_blocks = [&](auto f1) {
+            constexpr bool F1 = decltype(f1)::value;
+            uint64_t km = KEY_NONE;
+            // ============================ relocate block ============================
+            for (int t0 = 0; t0 < S; t0 += 32 * KR) {
+                uint64_t kb;
+                if constexpr (WIN) kb = score_reloc_win<TABU, FULL, F1>(SC, W, t0, 0, n, it, asp, lane);
+                else kb = FULL ? score_reloc_fast<TABU>(SC, t0, 0, n, it, asp, lane)
+                               : score_reloc<TABU, FULL>(SC, t0, 0, n, it, asp, lane);
+                km = kb < km ? kb : km;
+            }
+            // ============================== swap block ==============================
+            // m2 chunks of 32*KS aligned to the top (hi = n, n - 64, ...) so only the
+            // lowest chunk is ragged; adjacent pairs are excluded there and scored exactly
+            // by the generic three-link formula below.
+            for (int hi = n; hi > 1; hi -= 32 * KS) {
+                uint64_t kb;
+                if constexpr (WIN) kb = score_swap_win<TABU, FULL, F1>(SC, W, hi, 0, hi - 1, it, asp, lane);
+                else kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
+                               : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
+                km = kb < km ? kb : km;
+            }
+            return km;
+        };
+        constexpr bool F1 = WIN && FULL;
+        {
+            const uint64_t km = score_blocks(std::integral_constant<bool, F1>{});
+            kmin = km < kmin ? km : kmin;
         }
-        // ============================== swap block ==============================
-        // m2 chunks of 32*KS aligned to the top (hi = n, n - 64, ...) so only the
-        // lowest chunk is ragged; adjacent pairs are excluded there and scored exactly
-        // by the generic three-link formula below.
-        for (int hi = n; hi > 1; hi -= 32 * KS) {
-            uint64_t kb;
-            if constexpr (WIN) kb = score_swap_win<TABU, FULL>(SC, W, hi, 0, hi - 1, it, asp, lane);
-            else kb = FULL ? score_swap_fast<TABU>(SC, hi, 0, hi - 1, it, asp, lane)
-                           : score_swap<TABU, FULL>(SC, hi, 0, hi - 1, it, asp, lane);
-            kmin = kb < kmin ? kb : kmin;
+        if constexpr (F1) {
+            if (key_cls(wmin(kmin)) == 1) {   // warp-uniform: no admissible feasible move -- re-score exactly
+                const uint64_t km = score_blocks(std::integral_constant<bool, false>{});
+                kmin = km;
+            }
         }
         // adjacent pairs (x, succ x): the exact three-link formula (engine.cuh)
         if (mask & 8u) {

@@ -134,7 +134,12 @@ __device__ __forceinline__ void win_reloc_record(const ScoreCtx<uint16_t, int32_
     if (!SV) rec[2] = q2;
 }
 
-template <bool TABU, bool SV>
+// F1 (positive legs only): one sign bit for "not admissible OR infeasible" -- k32 = key | ((nadm | margins) & 2^31),
+// one ALU instruction fewer per move than the exact form (nadm << 31 | key, all ones when infeasible).  A window
+// minimum below 2^31 is then exactly the exact form's (the same admissible feasible moves, the same order); a
+// minimum at or above 2^31 says only that no admissible feasible move exists, and the caller re-scores the
+// iteration with the exact form (batch.cu) -- rare in TS, once per NS run.
+template <bool TABU, bool SV, bool F1 = false>
 __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int t0,
                                                     int m_lo, int m_hi, int it, int asp, int lane) {
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
@@ -207,10 +212,16 @@ __device__ __forceinline__ uint64_t score_reloc_win(const ScoreCtx<uint16_t, int
                     mg = mA | mB | (lim - ins) | noop;
                 }
                 const int e2 = madd(ins, one, remasp);                                  // delta - asp (TS) / delta (NS)
-                uint32_t nadm;
-                if (TABU) nadm = mul_fma(tb, c_p2[k]) & ~(uint32_t)e2 & 0x80000000u;
-                else nadm = ~(uint32_t)e2 & 0x80000000u;
-                const uint32_t k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk + k) | nadm | (uint32_t)(mg >> 31);
+                uint32_t k32;
+                if (F1 && SV) {
+                    const uint32_t nz = TABU ? mul_fma(tb, c_p2[k]) & ~(uint32_t)e2 : ~(uint32_t)e2;
+                    k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk + k) | ((nz | (uint32_t)mg) & 0x80000000u);
+                } else {
+                    uint32_t nadm;
+                    if (TABU) nadm = mul_fma(tb, c_p2[k]) & ~(uint32_t)e2 & 0x80000000u;
+                    else nadm = ~(uint32_t)e2 & 0x80000000u;
+                    k32 = (uint32_t)madd(ins, 1 << WIN_KEY_SHIFT, remk + k) | nadm | (uint32_t)(mg >> 31);
+                }
                 bk = min(bk, k32);
             }
         }
@@ -261,7 +272,7 @@ __device__ __forceinline__ void win_swap_record(const ScoreCtx<uint16_t, int32_t
     rec[0] = q0; rec[1] = q1; rec[2] = q2;
 }
 
-template <bool TABU, bool SV>
+template <bool TABU, bool SV, bool F1 = false>
 __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int32_t> &C, const WinCtx &W, int hi,
                                                    int m1_lo, int m1_hi, int it, int asp, int lane) {
     const int4 *CS4 = C.CS4, *RS4 = C.RS4;
@@ -369,10 +380,17 @@ __device__ __forceinline__ uint64_t score_swap_win(const ScoreCtx<uint16_t, int3
                     const int adj = (s1 == m2) | (q_s2[k] == m1) ? -1 : 0;
                     mg = (l1 | l2 | l3) | (l4 | mf | adj) | tc;
                 }
-                uint32_t nadm;                                                              // delta holds delta - asp
-                if (TABU) nadm = (mul_fma(tb1, q_pb[k]) | mul_fma(q_tb[k], pa)) & ~(uint32_t)delta & 0x80000000u;
-                else nadm = ~(uint32_t)delta & 0x80000000u;
-                const uint32_t k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
+                uint32_t k32;                                                               // delta holds delta - asp
+                if (F1 && SV) {   // see score_reloc_win
+                    const uint32_t nz = TABU ? (mul_fma(tb1, q_pb[k]) | mul_fma(q_tb[k], pa)) & ~(uint32_t)delta
+                                             : ~(uint32_t)delta;
+                    k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | ((nz | (uint32_t)mg) & 0x80000000u);
+                } else {
+                    uint32_t nadm;
+                    if (TABU) nadm = (mul_fma(tb1, q_pb[k]) | mul_fma(q_tb[k], pa)) & ~(uint32_t)delta & 0x80000000u;
+                    else nadm = ~(uint32_t)delta & 0x80000000u;
+                    k32 = (uint32_t)madd(delta, 1 << WIN_KEY_SHIFT, keyb0 + k) | nadm | (uint32_t)(mg >> 31);
+                }
                 bk = min(bk, k32);
             }
         };
