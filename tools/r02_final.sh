@@ -16,8 +16,9 @@ $B > $OUT/plain_batch2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:^k_batch$ -c 1 -o $OUT/k_batch $B > $OUT/ncu_batch.log 2>&1
 echo "full_rc=$?" >> $OUT/ncu_rc.txt
 bash tools/quick_single.sh $OUT
+# the k_grid captures (~15 MB each) only when asked: gpurun copies back at most 64 MiB
 declare -A IT=( [ontario]=500 [large]=300 [surge]=20 )
-for w in ontario large surge; do
+for w in ${KGRID_NCU:-}; do
   cmd="python bench.py --workload $w --iters ${IT[$w]} --steps 1 --warmup 0 --no-cpu-baseline"
   $cmd > $OUT/plain_$w.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_grid -c 1 -o $OUT/k_grid_$w $cmd > $OUT/ncu_$w.log 2>&1
