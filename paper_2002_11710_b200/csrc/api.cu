@@ -550,7 +550,7 @@ struct GState {
 static as_status alloc_gstate(as_ctx *ctx, const as_instance *I, bool with_E, RunViewG &G) {
     const size_t S = (size_t)I->n + I->V;
     void *p;
-    size_t words = 13 * S + (size_t)I->V + (with_E ? (size_t)I->n * I->V : 0) + 16;
+    size_t words = 14 * S + (size_t)I->V + (with_E ? (size_t)I->n * I->V : 0) + 16;
     as_status st = scratch(ctx, "gstate", words * 4, &p);
     if (st != AS_OK) return st;
     int32_t *b = (int32_t *)p;
@@ -567,6 +567,7 @@ static as_status alloc_gstate(as_ctx *ctx, const as_instance *I, bool with_E, Ru
     G.arr = b; b += S;
     G.sl = b; b += S;
     G.pos = b; b += S;
+    G.slp = b; b += S;
     G.E = with_E ? b : nullptr;
     return AS_OK;
 }

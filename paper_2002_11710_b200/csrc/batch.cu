@@ -159,7 +159,7 @@ __device__ __forceinline__ void batch_cta(const SearchArgs &A, int RPC, const Ba
     R.succ.base = rb + L.LK; R.pred.base = rb + L.LK;
     R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
     R.pick_s.base = CS; R.w_s.base = CS;
-    R.arr.base = R.sl.base = R.pos.base = NW ? rb + L.NR : nullptr;
+    R.arr.base = R.sl.base = R.pos.base = R.slp.base = NW ? rb + L.NR : nullptr;
     R.F = F; R.E = E;
     CompactRV<ET> R0 = R;   // evaluation view: the window path takes tabu from TB, not from E in global memory
     if (WIN) R0.E = nullptr;

@@ -60,10 +60,11 @@ struct CompactRV {
     Field<int32_t, 16, 8> svco;
     Field<uint16_t, 16, 4> pick_s;
     Field<int32_t, 16, 0> w_s;
-    // no-wait variant (f3, batched kernel): NR[x] (16 B) = {arrival, suffix slack, position, 0}
+    // no-wait variant (f3): NR[x] (16 B) = {arrival, suffix slack, position, position of the suffix minimum}
     Field<int32_t, 16, 0> arr;
     Field<int32_t, 16, 4> sl;
     Field<int32_t, 16, 8> pos;
+    Field<int32_t, 16, 12> slp;
     int32_t *F;
     ET *E;
 };

@@ -109,6 +109,7 @@ struct RunViewT {
     int32_t *arr;                   // [S] arrival at the slot (END: return to base)
     int32_t *sl;                    // [S] min over the route suffix from the slot of (w - arr)
     int32_t *pos;                   // [S] position in the route (missions 1..L, END L+1)
+    int32_t *slp;                   // [S] first position of the suffix where that minimum is attained
 };
 
 using MissionView = MissionViewT<int32_t, int32_t>;
@@ -195,8 +196,19 @@ __device__ __forceinline__ int nw_range_slack(const RV &R, int x, int y) {
     return s;
 }
 
+// Does every slot of the stretch x..y (x at or before y along succ) keep slack >= d?
+// O(1) unless the suffix minimum from x is below d and lies after y: then the
+// stretch's own minimum decides (walk).  Same answer as d <= nw_range_slack.
+template <class RV>
+__device__ __forceinline__ bool nw_stretch_ok(const RV &R, int x, int y, int d) {
+    if (d <= R.sl[x]) return true;                 // the whole suffix from x has the slack
+    if (R.slp[x] <= R.pos[y]) return false;        // its minimum (< d) lies inside x..y
+    return d <= nw_range_slack(R, x, y);
+}
+
 // Recompute the whole route of vehicle v (incoming-link records, arrivals,
-// positions, suffix slacks) from its linked list.  Single thread, O(L).
+// positions, suffix slacks and where they are attained) from its linked list.
+// Single thread, O(L).
 template <class MV, class RV>
 __device__ inline void nw_refresh_route(const MV &M, const RV &R, int v) {
     const int n = M.n, term = n + v, c = M.cls(v);
@@ -216,12 +228,13 @@ __device__ inline void nw_refresh_route(const MV &M, const RV &R, int v) {
         dep += inc;
         x = R.succ[x];
     }
-    int s = 0x7FFFFFFF;
+    int s = 0x7FFFFFFF, sp = 0;
     x = term;
     do {
         int v2 = R.w_s[x] - R.arr[x];
-        s = v2 < s ? v2 : s;
+        if (v2 <= s) { s = v2; sp = R.pos[x]; }   // ties: the earlier position
         R.sl[x] = s;
+        R.slp[x] = sp;
         x = R.pred[x];
     } while (x != term);
 }
@@ -240,7 +253,7 @@ __device__ __forceinline__ bool nw_reloc_time(const MV &M, const RV &R, const Re
     if (R.pos[t] > R.pos[m]) {               // p s .. c m t ..
         int c = R.pred[t];
         int d1 = R.depc[m] + r.Dps - R.arr[s];
-        if (d1 > nw_range_slack(R, s, c)) return false;
+        if (!nw_stretch_ok(R, s, c, d1)) return false;
         int Am = R.arr[c] + d1 + x1;
         return Am <= r.w_m && Am + x2 - R.arr[t] <= R.sl[t];
     }
@@ -248,7 +261,7 @@ __device__ __forceinline__ bool nw_reloc_time(const MV &M, const RV &R, const Re
     int Am = R.depc[t] + x1;
     if (Am > r.w_m) return false;
     int d1 = Am + x2 - R.arr[t];
-    if (d1 > nw_range_slack(R, t, p)) return false;
+    if (!nw_stretch_ok(R, t, p, d1)) return false;
     return R.arr[p] + d1 + r.Dps - R.arr[s] <= R.sl[s];
 }
 
@@ -342,7 +355,7 @@ __device__ __forceinline__ MoveEval swap_eval(const MV &M, const RV &R, int m1, 
                 const int wf = first1 ? w1 : w2, wg = first1 ? w2 : w1;
                 int Ag = R.depc[f] + d_pf_g;
                 int d1 = Ag + d_g_sf - R.arr[sf];
-                ok = ok && (Ag <= wg) && (d1 <= nw_range_slack(R, sf, pg));
+                ok = ok && (Ag <= wg) && nw_stretch_ok(R, sf, pg, d1);
                 int Af = R.arr[pg] + d1 + d_pg_f;
                 ok = ok && (Af <= wf) && (Af + d_f_sg - R.arr[sg] <= R.sl[sg]);
             }

@@ -58,7 +58,7 @@ struct GreedyArgs {
 // int32 words of one start's state
 __host__ __device__ inline int greedy_state_words(int n, int V, bool nw) {
     const int S = n + V;
-    return (9 + (nw ? 3 : 0)) * S + V + n + 2;
+    return (9 + (nw ? 4 : 0)) * S + V + n + 2;
 }
 
 template <bool NW>
@@ -96,8 +96,8 @@ __global__ void k_greedy(GreedyArgs G) {
     int32_t *w_w = p; R.w_s = p; p += S;
     R.F = p; p += V;
     int32_t *order = p; p += n;
-    if (NW) { R.arr = p; p += S; R.sl = p; p += S; R.pos = p; p += S; }
-    else { R.arr = R.sl = R.pos = nullptr; }
+    if (NW) { R.arr = p; p += S; R.sl = p; p += S; R.pos = p; p += S; R.slp = p; p += S; }
+    else { R.arr = R.sl = R.pos = R.slp = nullptr; }
     R.E = nullptr;
 
     // ---- empty schedule ----------------------------------------------------

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     R.veh.base = RSb; R.endc.base = RSb; R.depc.base = RSb; R.inc.base = RSb; R.svco.base = RSb;
     R.pick_s.base = reinterpret_cast<unsigned char *>(CS4); R.w_s.base = reinterpret_cast<unsigned char *>(CS4);
     R.F = F; R.E = E;
-    R.arr.base = R.sl.base = R.pos.base = NW ? smem + L.NR : nullptr;
+    R.arr.base = R.sl.base = R.pos.base = R.slp.base = NW ? smem + L.NR : nullptr;
 
     // ---- start schedule -> replica (every CTA) -----------------------------
     for (int x = tid; x < S; x += blockDim.x) R.veh[x] = x < n ? (int16_t)-1 : (int16_t)(x - n);

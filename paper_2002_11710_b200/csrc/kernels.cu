@@ -73,11 +73,11 @@ __global__ void k_build_state(DevInst I, const int32_t *ptr, const int32_t *ms, 
     RunView R;
     R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
     R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = nullptr;
-    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos;
+    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos; R.slp = G.slp;
     for (int x = threadIdx.x; x < S; x += blockDim.x) {
         if (x < n && G.veh[x] < 0) {
             G.endc[x] = G.depc[x] = G.inc[x] = G.svco[x] = 0;
-            if (I.no_wait) G.arr[x] = G.sl[x] = G.pos[x] = 0;
+            if (I.no_wait) G.arr[x] = G.sl[x] = G.pos[x] = G.slp[x] = 0;
             continue;
         }
         if (!I.no_wait) refresh_slot(M, R, x);
@@ -102,7 +102,7 @@ __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long l
     RunView R;
     R.succ = G.succ; R.pred = G.pred; R.veh = G.veh; R.endc = G.endc; R.depc = G.depc; R.inc = G.inc;
     R.svco = G.svco; R.pick_s = G.pick_s; R.w_s = G.w_s; R.F = G.F; R.E = TABU ? G.E : nullptr;
-    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos;
+    R.arr = G.arr; R.sl = G.sl; R.pos = G.pos; R.slp = G.slp;
     uint64_t kmin = KEY_NONE;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < N;
          idx += (uint64_t)gridDim.x * blockDim.x) {
@@ -132,7 +132,7 @@ __global__ void k_eval_dump(DevInst I, RunViewG G, int it, long long cur, long l
 struct SmemLayout {
     // byte offsets, 16-byte aligned
     int T, del, heli, svc, vcls, vloc, clsheli;
-    int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc, arr, sl, pos;
+    int succ, pred, veh, endc, depc, inc, svco, pick_s, w_s, F, E, bsucc, arr, sl, pos, slp;
     int red, ctrl, total;
 };
 
@@ -164,6 +164,7 @@ __host__ __device__ inline SmemLayout make_layout(int n, int V, int NL, int NC, 
     L.arr = o; o = align16(o + (nw ? S * 4 : 0));
     L.sl = o; o = align16(o + (nw ? S * 4 : 0));
     L.pos = o; o = align16(o + (nw ? S * 4 : 0));
+    L.slp = o; o = align16(o + (nw ? S * 4 : 0));
     L.E = E_smem ? o : -1;
     o = align16(o + (E_smem ? n * V * 4 : 0));
     L.red = o; o = align16(o + 32 * 8);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(1024) k_search(SearchArgs A) {
     R.succ = SM32(L.succ); R.pred = SM32(L.pred); R.veh = SM32(L.veh); R.endc = SM32(L.endc); R.depc = SM32(L.depc);
     R.inc = SM32(L.inc); R.svco = SM32(L.svco); R.pick_s = SM32(L.pick_s); R.w_s = SM32(L.w_s); R.F = SM32(L.F);
     R.E = TABU ? Eg : nullptr;
-    R.arr = SM32(L.arr); R.sl = SM32(L.sl); R.pos = SM32(L.pos);
+    R.arr = SM32(L.arr); R.sl = SM32(L.sl); R.pos = SM32(L.pos); R.slp = SM32(L.slp);
     int32_t *bsucc = SM32(L.bsucc);
     unsigned long long *red = reinterpret_cast<unsigned long long *>(smem_raw + L.red);
     int32_t *ctrl = SM32(L.ctrl);   // 0: stop, 1: copy-best, 2: infeasible flag

@@ -18,7 +18,7 @@ namespace airsched {
 // One run's state in global memory (dump path).
 struct RunViewG {
     int32_t *succ, *pred, *veh, *endc, *depc, *inc, *svco, *pick_s, *w_s, *F, *E;
-    int32_t *arr, *sl, *pos;   // no-wait variant only (f3)
+    int32_t *arr, *sl, *pos, *slp;   // no-wait variant only (f3)
 };
 
 struct SearchArgs {

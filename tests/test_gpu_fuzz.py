@@ -191,6 +191,10 @@ def test_fuzz_nowait_and_greedy(A, ctx, oracle_mod):
         p, m = start
         compare_run(A, ctx, O, h, p, m, 1, 3, 40, seed=5, kick=2, digest=True)
         compare_run(A, ctx, O, h, p, m, 0, 0, 40)
+        with ctx.options(GRID=1):   # the whole-GPU kernel's no-wait form (compact layouts)
+            compare_run(A, ctx, O, h, p, m, 1, 3, 40, seed=7, kick=2)
+        with ctx.options(GRID=1, GRID_T_GLOBAL=1, GRID_E_GLOBAL=1, GRID_G=3):
+            compare_run(A, ctx, O, h, p, m, 1, 2, 30)
         d, f, key = A.as_eval_moves(ctx, h, p, m, mode=0)
         od, of, ok = O.eval_moves(p, m, mode=0)
         assert (d == od).all() and (f == of).all()
