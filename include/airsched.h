@@ -152,6 +152,9 @@ as_status as_ctx_set_option(as_ctx *ctx, int32_t option, int64_t value);
  * refresh inside the apply.  out holds 10 entries.  Synchronises the context's stream.
  * AS_ERR_INVALID_ARG if no such run was made. */
 as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out);
+/* Per CTA of that run (at most 256): tile_ns[c] = the sum over iterations of CTA c's own tile phase (loop
+ * top to all of its warps done), smid[c] = the SM it ran on; *n_ctas = the CTA count.  Host buffers of 256. */
+as_status as_ctx_grid_cta_phases(as_ctx *ctx, int64_t *tile_ns, int32_t *smid, int32_t *n_ctas);
 void as_ctx_destroy(as_ctx *ctx);
 /* Upload (and cache on ctx) the instance's device copy.  Optional: every call
  * below uploads on first use; call this to keep the upload out of a timed

@@ -35,7 +35,8 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_init_greedy", "as_eval_moves", "as_tabu_run", "as_nbhd_run", "as_batch_run",
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
            "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
-           "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option", "as_ctx_grid_phases"]
+           "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option", "as_ctx_grid_phases",
+           "as_ctx_grid_cta_phases"]
 
 
 class AirschedError(RuntimeError):
@@ -93,6 +94,7 @@ def _load():
         "as_ctx_set_stream": (i32, [vp, vp]),
         "as_ctx_set_option": (i32, [vp, i32, i64]),
         "as_ctx_grid_phases": (i32, [vp, vp]),
+        "as_ctx_grid_cta_phases": (i32, [vp, vp, vp, vp]),
         "as_ctx_destroy": (None, [vp]),
         "as_instance_upload": (i32, [vp, vp]),
         "as_init_greedy": (i32, [vp, vp, i32, i32, vp, vp, vp]),
@@ -219,6 +221,15 @@ class Ctx:
                 "apply_parts_us": {"key_read": us(5), "split": us(6), "relink": us(7), "totals": us(8),
                                    "refresh": us(9)},
                 "iterations": int(out[4])}
+
+    def grid_cta_phases(self):
+        """as_ctx_grid_cta_phases: per CTA of that run, its tile phase per iteration (us) and its SM id."""
+        t = np.zeros(256, np.int64)
+        sm = np.zeros(256, np.int32)
+        nc = C.c_int32(0)
+        _check(lib.as_ctx_grid_cta_phases(self.handle, t.ctypes.data, sm.ctypes.data, C.byref(nc)))
+        it = max(self.grid_phases()["iterations"], 1)
+        return t[:nc.value] / it / 1e3, sm[:nc.value].copy()
 
     def options(self, **kw):
         """Context manager: set options, restore the automatic choice on exit."""

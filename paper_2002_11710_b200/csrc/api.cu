@@ -255,6 +255,7 @@ struct as_ctx {
     int64_t opt[AS_OPT_COUNT];              // as_ctx_set_option overrides; OPT_UNSET = automatic
     unsigned long long xr_timeout_ns = 30000000000ull;   // fused sharded exchange: bound on a peer's wait
     void *phase_dev = nullptr;              // k_grid phase sums of the last timed launch (AS_OPT_PHASE_TIMES)
+    int phase_ctas = 0;                     // its CTA count (per-CTA records, as_ctx_grid_cta_phases)
 };
 
 struct as_comm {
@@ -338,6 +339,20 @@ extern "C" as_status as_ctx_grid_phases(as_ctx *ctx, int64_t *out) {
     if (st != AS_OK) return st;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     CUDA_TRY(cudaMemcpy(out, ctx->phase_dev, 10 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return AS_OK;
+}
+
+extern "C" as_status as_ctx_grid_cta_phases(as_ctx *ctx, int64_t *tile_ns, int32_t *smid, int32_t *n_ctas) {
+    if (!ctx || !tile_ns || !smid || !n_ctas) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (!ctx->phase_dev) return fail(AS_ERR_INVALID_ARG, "no whole-GPU run with AS_OPT_PHASE_TIMES yet");
+    as_status st = set_device(ctx);
+    if (st != AS_OK) return st;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    int64_t buf[2 * 256];
+    CUDA_TRY(cudaMemcpy(buf, (int64_t *)ctx->phase_dev + 16, sizeof(buf), cudaMemcpyDeviceToHost));
+    const int nc = std::min(ctx->phase_ctas, 256);
+    for (int c = 0; c < nc; c++) { tile_ns[c] = buf[c]; smid[c] = (int32_t)buf[256 + c]; }
+    *n_ctas = nc;
     return AS_OK;
 }
 
@@ -832,8 +847,9 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 void *p;
                 GA.phase_ns = nullptr;
                 if (opt_int(ctx, AS_OPT_PHASE_TIMES, 0) == 1 && !I->no_wait) {   // (no phase timers for no-wait)
-                    if ((st = scratch(ctx, "g_phase", 10 * 8, &p)) != AS_OK) return st;
-                    CUDA_TRY(cudaMemsetAsync(p, 0, 10 * 8, ctx->stream));
+                    if ((st = scratch(ctx, "g_phase", (16 + 2 * 256) * 8, &p)) != AS_OK) return st;
+                    CUDA_TRY(cudaMemsetAsync(p, 0, (16 + 2 * 256) * 8, ctx->stream));
+                    ctx->phase_ctas = grid_blocks;
                     GA.phase_ns = (unsigned long long *)p;
                     ctx->phase_dev = p;
                 }

@@ -32,6 +32,7 @@ namespace cg = cooperative_groups;
 
 constexpr int GRID_THREADS = airsched::GRID_WARPS * 32;
 constexpr int GRID_SWT_MAX = 4096;   // compact swap tiles held as a table in shared memory (16 KB)
+constexpr int GRID_PH_CTAS = 256;    // per-CTA phase records (AS_OPT_PHASE_TIMES)
 
 namespace airsched {
 
@@ -334,16 +335,19 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     // at the phase boundaries -- its own tiles, waiting for the CTA's other warps, CTA reduction + grid
     // barrier (+ rank exchange), apply -- and the sums go to GA.phase_ns at the end
     const bool ph = PH && blockIdx.x == 0 && tid == 0;
-    unsigned long long ph_sum[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_t = 0, ph_u = 0, ph_v = 0;
+    const bool phc = PH && tid == 0;   // every CTA: its own tile phase (loop top -> all its warps done)
+    unsigned long long ph_sum[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ph_t = 0, ph_u = 0, ph_v = 0, phc_t = 0, phc_sum = 0;
     for (; it < A.max_iters; it++) {
         const long long cur = s_cur, best = s_best;
         if (ph) ph_t = globaltimer_ns();
+        if (phc) phc_t = globaltimer_ns();
         uint64_t kmin = score_tiles<TABU, FULL, TR, NW>(SC, M, R, GT, GA.tlo, GA.thi, gwarp, nwarps_all, it, cur, best,
                                                         lane);
         kmin = wmin(kmin);
         if (ph) { ph_u = globaltimer_ns(); ph_sum[0] += ph_u - ph_t; ph_t = ph_u; }
         if (lane == 0) red[warp] = kmin;
         __syncthreads();
+        if (phc) phc_sum += globaltimer_ns() - phc_t;
         if (ph) { ph_u = globaltimer_ns(); ph_sum[1] += ph_u - ph_t; ph_t = ph_u; }
         uint64_t kcta = KEY_NONE;
         if (warp == 0) {   // CTA minimum by one warp (parallel loads + shuffles, not a serial loop)
@@ -435,6 +439,12 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         if (ctrl[0]) break;
         if (ctrl[1] && blockIdx.x == 0)
             for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
+    }
+    if (PH && phc && blockIdx.x < GRID_PH_CTAS) {   // per CTA: tile-phase sum and the SM it ran on
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        GA.phase_ns[16 + blockIdx.x] = phc_sum;
+        GA.phase_ns[16 + GRID_PH_CTAS + blockIdx.x] = smid;
     }
     if (PH && ph) {
         for (int k = 0; k < 4; k++) GA.phase_ns[k] = ph_sum[k];
