@@ -782,6 +782,10 @@ def test_grid_phase_times(A, ctx, oracle_mod, cfg, iters, ctxopt):
     per_it = ph["own_tiles_us"] + ph["cta_wait_us"] + ph["reduce_barrier_us"] + ph["apply_us"]
     assert 0 < per_it * iters / 1e3 <= ctx.last_kernel_ms * 1.05
     assert min(ph["own_tiles_us"], ph["reduce_barrier_us"], ph["apply_us"]) > 0
+    # per CTA: every CTA's tile phase is measured and fits in the iteration; SM ids distinct and in range
+    t, sm = ctx.grid_cta_phases()
+    assert len(t) >= 1 and (t > 0).all() and (t <= per_it * 1.05).all()
+    assert len(set(sm.tolist())) == len(sm) and sm.min() >= 0
 
 
 def test_global_node_cost_table(A, oracle_mod):
