@@ -843,6 +843,26 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 grid_blocks = one_cta ? 1 : std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS,
                                                                                       want_grid == 1 ? ctx->n_sm : need_blocks)));
                 if (xr) grid_blocks = std::max(1, std::min(std::min(ctx->n_sm, 256), opt_int(ctx, AS_OPT_GRID_BLOCKS, ctx->n_sm)));
+                // small instances: ONE cluster of up to 16 CTAs (every CTA's key stored into every CTA's shared
+                // memory + one cluster barrier, instead of a global atomic, the grid barrier and a global read)
+                // when its warps take every tile within two rounds
+                GA.cluster = 0;
+                {
+                    const int clo = opt_int(ctx, AS_OPT_GRID_CLUSTER, -1);
+                    const bool ok = !xr && !one_cta && GA.T_smem && (GA.E_smem || !tabu) && !I->no_wait &&
+                                    opt_int(ctx, AS_OPT_PHASE_TIMES, 0) != 1;
+                    int cl = 0;
+                    if (ok && clo >= 2) cl = (int)std::min<int64_t>(clo, 16);
+                    else if (ok && clo == -1 && want_grid != 1 && tiles1 <= 2 * 16 * GRID_WARPS) cl = 16;
+                    const bool full = (P->move_mask & 15u) == 15u && D.d.svcpos;
+                    while (cl >= 2 &&
+                           grid_cluster_capacity(tabu ? 1 : 0, tb, ebytes, full, cl, GRID_WARPS * 32, grid_smem) < 1)
+                        cl /= 2;
+                    if (cl >= 2) {
+                        GA.cluster = cl;
+                        grid_blocks = cl;
+                    }
+                }
                 GA.Tglobal = D.Tpad;
                 void *p;
                 GA.phase_ns = nullptr;
@@ -913,7 +933,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     if (xr && !use_grid) return fail(AS_ERR_UNSUPPORTED, "fused sharded run: the state does not fit the grid kernel");
     if (opt_int(ctx, AS_OPT_VERBOSE, 0))
         fprintf(stderr, "[airsched] n=%d V=%d runs=%d single=%d -> %s (blocks %d, G %d, T_smem %d, E_smem %d, smem %zu)\n",
-                n, V, n_runs, (int)single, use_grid ? (xr ? "k_grid fused-sharded" : grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
+                n, V, n_runs, (int)single, use_grid ? (xr ? "k_grid fused-sharded" : GA.cluster > 1 ? "k_grid/cluster" : grid_blocks == 1 ? "k_grid/1CTA" : "k_grid") :
                 use_batch ? (win ? "k_batch/window" : "k_batch") : "k_search", grid_blocks, GA.G, GA.T_smem, GA.E_smem,
                 use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));

@@ -33,6 +33,7 @@ namespace cg = cooperative_groups;
 constexpr int GRID_THREADS = airsched::GRID_WARPS * 32;
 constexpr int GRID_SWT_MAX = 4096;   // compact swap tiles held as a table in shared memory (16 KB)
 constexpr int GRID_PH_CTAS = 256;    // per-CTA phase records (AS_OPT_PHASE_TIMES)
+constexpr int GRID_CL_MAX = 16;      // CTAs of the cluster mode (non-portable cluster size)
 
 namespace airsched {
 
@@ -158,9 +159,13 @@ __device__ __forceinline__ void grid_bookkeeping(const SearchArgs &A, const Grid
 // profiles/r02/kgrid_phase_ab.jsonl).
 // NW: the no-wait variant (f3, reading #40): every move by the engine's exact evaluation (general
 // scorers), per-slot {arrival, suffix slack, position} records, whole-route refresh of the two changed routes.
-template <bool TABU, class TT, class ET, bool FULL, bool TR, bool PH, bool NW = false>
+// CL: the grid is ONE thread-block cluster (small instances, GridArgs::cluster): the per-iteration exchange is
+// every CTA's key stored into every CTA's shared memory (DSMEM) and one cluster barrier, instead of a global
+// atomicMin, a grid barrier and a global read (~0.3 instead of ~1.5 us per iteration).
+template <bool TABU, class TT, class ET, bool FULL, bool TR, bool PH, bool NW = false, bool CL = false>
 __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs GA) {
     static_assert(!NW || (!FULL && !PH), "the no-wait variant runs the general scorers, without phase timers");
+    static_assert(!CL || (!TR && !NW), "cluster mode: shared-memory tables, waiting model");
     extern __shared__ __align__(16) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
     const DevInst &I = A.inst;
@@ -282,7 +287,10 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
     __syncthreads();
     if (blockIdx.x == 0)
         for (int x = tid; x < S; x += blockDim.x) GA.BS[x] = (int32_t)(LK[x] & 0xFFFF);
-    if (gridDim.x > 1) grid.sync();   // global tabu matrix initialised before anyone reads it
+    if constexpr (CL) cg::this_cluster().sync();
+    else if (gridDim.x > 1) grid.sync();   // global tabu matrix initialised before anyone reads it
+    __shared__ unsigned long long s_ckey[2][GRID_CL_MAX];   // CL: every CTA's key of iterations of each parity
+    __shared__ unsigned long long s_kcl;                     // CL: the cluster minimum
 
     ScoreCtx<TT, ET> SC;
     SC.Ts = Ts; SC.Tt = I.tsym ? Ts : reinterpret_cast<const TT *>(I.TpadT); SC.CS4 = CS4; SC.MH = MH; SC.VC = VC; SC.RS4 = RS4; SC.LK = LK; SC.F = F; SC.E = E;
@@ -352,12 +360,28 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         uint64_t kcta = KEY_NONE;
         if (warp == 0) {   // CTA minimum by one warp (parallel loads + shuffles, not a serial loop)
             kcta = wmin(lane < nwarps ? red[lane] : KEY_NONE);
-            if (lane == 0 && !one) {
+            if constexpr (CL) {   // lane r stores this CTA's key into CTA r's slot (DSMEM)
+                if (lane < (int)gridDim.x) {
+                    unsigned long long *dst = cg::this_cluster().map_shared_rank(&s_ckey[it & 1][blockIdx.x], lane);
+                    *dst = kcta;
+                }
+            } else if (lane == 0 && !one) {
                 if (kcta != KEY_NONE) atomicMin(&gkey[it % 3], (unsigned long long)kcta);
                 if (blockIdx.x == 0) gkey[(it + 1) % 3] = KEY_NONE;   // safe: last read in iteration it-2
             }
         }
-        if (!one) grid.sync();   // a single CTA (small instances) needs no grid barrier
+        if constexpr (CL) {
+            // slots of parity it & 1: written before this barrier, read after it; the next writes of this
+            // parity (iteration it + 2) come after every CTA passed the barrier of iteration it + 1
+            cg::this_cluster().sync();
+            if (warp == 0) {
+                const uint64_t kc = wmin(lane < (int)gridDim.x ? s_ckey[it & 1][lane] : KEY_NONE);
+                if (lane == 0) s_kcl = kc;
+            }
+            __syncwarp();
+        } else if (!one) {
+            grid.sync();   // a single CTA (small instances) needs no grid barrier
+        }
         if (GA.xr) {   // fused sharded run: the all-ranks minimum over NVLink, then every CTA reads it
             if (blockIdx.x == 0 && tid == 0) {
                 const int q = it % 3;
@@ -377,7 +401,7 @@ __global__ void __launch_bounds__(GRID_THREADS, 1) k_grid(SearchArgs A, GridArgs
         if (warp == 0) {
             int nt = 0;
             if (lane == 0) {
-                const uint64_t k = GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
+                const uint64_t k = CL ? s_kcl : GA.xr ? __ldcg(&GA.gkey2[it % 3]) : one ? kcta : __ldcg(&gkey[it % 3]);
                 if (ph) { asm volatile("" ::"l"(k)); ph_sum[4] += globaltimer_ns() - ph_t; }   // key read (part of apply)
                 int stop = 0;
                 if (k == KEY_ABORT) stop = AS_STOP_COMM_ABORT;   // a peer never arrived (bounded wait)
@@ -480,6 +504,54 @@ __global__ void k_bs_to_csr(const int32_t *BS, int n, int V, int32_t *bp, int32_
     bp[V] = pos;
 }
 
+// Launch configuration of the cluster mode (one cluster of cl CTAs); gridDim.x == 0 on error.
+static cudaLaunchConfig_t cluster_config(const void *kc, int cl, int threads, size_t smem, cudaStream_t st,
+                                         cudaLaunchAttribute *at) {
+    cudaLaunchConfig_t cfg = {};
+    cudaError_t err = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess && cl > 8) err = cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return cfg;
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+// How many clusters of cl CTAs of the cluster-mode kernel for (mode, table and tabu widths, FAST scorers) fit
+// the GPU at once (0: none -- the caller keeps the cooperative grid).
+int grid_cluster_capacity(int mode, int tbytes, int ebytes, bool full, int cl, int threads, size_t smem) {
+    if (cl < 2 || cl > GRID_CL_MAX) return 0;
+    const int eb = mode == 1 && tbytes == 2 && ebytes == 2 ? 2 : 4;
+    const void *kc;
+    if (mode == 1) {
+        if (tbytes == 2 && eb == 2)
+            kc = full ? (const void *)k_grid<true, uint16_t, int16_t, true, false, false, false, true>
+                      : (const void *)k_grid<true, uint16_t, int16_t, false, false, false, false, true>;
+        else if (tbytes == 2)
+            kc = full ? (const void *)k_grid<true, uint16_t, int32_t, true, false, false, false, true>
+                      : (const void *)k_grid<true, uint16_t, int32_t, false, false, false, false, true>;
+        else kc = (const void *)k_grid<true, int32_t, int32_t, false, false, false, false, true>;
+    } else {
+        if (tbytes == 2)
+            kc = full ? (const void *)k_grid<false, uint16_t, int32_t, true, false, false, false, true>
+                      : (const void *)k_grid<false, uint16_t, int32_t, false, false, false, false, true>;
+        else kc = (const void *)k_grid<false, int32_t, int32_t, false, false, false, false, true>;
+    }
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = cluster_config(kc, cl, threads, smem, 0, at);
+    if (cfg.gridDim.x == 0) { cudaGetLastError(); return 0; }
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kc, &cfg) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return n;
+}
+
 template <bool TABU, class TT, class ET, bool FULL>
 static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks, int threads, size_t smem,
                             cudaStream_t st) {
@@ -488,11 +560,18 @@ static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks,
     if constexpr (!FULL)   // the no-wait variant (general scorers; no phase-timer instantiation)
         if (A.inst.no_wait)
             kern = GA.T_smem ? k_grid<TABU, TT, ET, false, false, false, true> : k_grid<TABU, TT, ET, false, true, false, true>;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
     SearchArgs a = A;
     GridArgs g = GA;
     void *args[] = {&a, &g};
+    if (GA.cluster > 1) {   // one cluster of GA.cluster CTAs (shared-memory tables, waiting model, no timers)
+        const void *kc = (const void *)k_grid<TABU, TT, ET, FULL, false, false, false, true>;
+        cudaLaunchAttribute at[1];
+        cudaLaunchConfig_t cfg = cluster_config(kc, GA.cluster, threads, smem, st, at);
+        if (cfg.gridDim.x == 0) return cudaGetLastError();
+        return cudaLaunchKernelExC(&cfg, kc, args);
+    }
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
     return cudaLaunchCooperativeKernel((void *)kern, blocks, threads, args, smem, st);
 }
 

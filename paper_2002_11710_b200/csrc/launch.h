@@ -85,6 +85,7 @@ struct GridArgs {
     int tlo, thi;                  // this launch's slice of the flat tile list (all tiles: 0, n_total)
     int compact;                   // 1: the list without empty swap tiles (single GPU; score.cuh GridTiles::swp)
     int swap_rec;                  // 1: per-warp swap-row record scratch in shared memory (ScoreCtx::SR)
+    int cluster;                   // > 1: the grid is ONE cluster of this many CTAs (k_grid<..., CL>)
     // fused sharded run (one k_grid per rank): after the grid minimum, CTA 0 stores the rank's key
     // and a tag into every peer's symmetric window slot over NVLink and waits (bounded) for the
     // peers' tags of this iteration in its own window (grid.cu rank_exchange)
@@ -124,6 +125,7 @@ void shard_plan(int n, int V, int G, int nranks, int rank, int *tlo, int *thi, i
 int grid_tile_count(int n, int V, int G);
 int grid_tile_count_compact(int n, int V, int G);
 
+int grid_cluster_capacity(int mode, int tbytes, int ebytes, bool full, int cl, int threads, size_t smem);
 size_t grid_smem_bytes(int n, int V, int NL, int NC, int tbytes, int ebytes, bool T_smem, bool E_smem, bool tabu,
                        bool swap_rec, int G, bool nw);
 cudaError_t launch_grid(const SearchArgs &A, GridArgs GA, int mode, int tbytes, int blocks, int threads, size_t smem,

@@ -809,3 +809,28 @@ def test_global_node_cost_table(A, oracle_mod):
         for k in ("idx", "delta", "cur", "best", "cls"):
             assert (g["trace"][k] == o["trace"][k]).all(), k
         assert (g["tabu"] == o["E"]).all() and routes_of(*g["best"]) == routes_of(*o["best"])
+
+
+@pytest.mark.parametrize("cfg,iters,opts,blocks", [
+    ("ontario", 600, {}, 16),                                   # the automatic choice for C2
+    ("ontario", 400, {"GRID_CLUSTER": 8}, 8),
+    ("tiny", 200, {"GRID": 1, "GRID_CLUSTER": 2}, 2),
+    ("batched", 200, {}, 16),
+    ("batched", 150, {"GRID_CLUSTER": 4, "GRID_G": 3}, 4),
+])
+def test_cluster_mode_parity(A, ctx, oracle_mod, cfg, iters, opts, blocks, ctxopt, capfd):
+    """The whole-GPU kernel as ONE thread-block cluster (small instances: every CTA's key stored into every
+    CTA's shared memory, one cluster barrier per iteration): TS (plain and kicked) and NS traces, tabu
+    matrix and best schedule equal the oracle's; the verbose line names the path and its CTA count."""
+    inst = instgen.generate(cfg)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start_of(O, inst)
+    c = instgen.CONFIGS[cfg]
+    ctxopt(VERBOSE=1, **opts)
+    capfd.readouterr()
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters)
+    err = capfd.readouterr().err
+    assert "k_grid/cluster" in err and f"blocks {blocks}," in err, err
+    _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
+    _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters // 2, seed=11, kick=6)
