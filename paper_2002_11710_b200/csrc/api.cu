@@ -849,8 +849,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 GA.cluster = 0;
                 {
                     const int clo = opt_int(ctx, AS_OPT_GRID_CLUSTER, -1);
-                    const bool ok = !xr && !one_cta && GA.T_smem && (GA.E_smem || !tabu) && !I->no_wait &&
-                                    opt_int(ctx, AS_OPT_PHASE_TIMES, 0) != 1;
+                    const bool ok = !xr && !one_cta && GA.T_smem && (GA.E_smem || !tabu) && !I->no_wait;
                     int cl = 0;
                     if (ok && clo >= 2) cl = (int)std::min<int64_t>(clo, 16);
                     else if (ok && clo == -1 && want_grid != 1 && tiles1 <= 2 * 16 * GRID_WARPS) cl = 16;

@@ -563,8 +563,9 @@ static cudaError_t launch_g(const SearchArgs &A, const GridArgs &GA, int blocks,
     SearchArgs a = A;
     GridArgs g = GA;
     void *args[] = {&a, &g};
-    if (GA.cluster > 1) {   // one cluster of GA.cluster CTAs (shared-memory tables, waiting model, no timers)
-        const void *kc = (const void *)k_grid<TABU, TT, ET, FULL, false, false, false, true>;
+    if (GA.cluster > 1) {   // one cluster of GA.cluster CTAs (shared-memory tables, waiting model)
+        const void *kc = GA.phase_ns ? (const void *)k_grid<TABU, TT, ET, FULL, false, true, false, true>
+                                     : (const void *)k_grid<TABU, TT, ET, FULL, false, false, false, true>;
         cudaLaunchAttribute at[1];
         cudaLaunchConfig_t cfg = cluster_config(kc, GA.cluster, threads, smem, st, at);
         if (cfg.gridDim.x == 0) return cudaGetLastError();

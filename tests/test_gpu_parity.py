@@ -834,3 +834,9 @@ def test_cluster_mode_parity(A, ctx, oracle_mod, cfg, iters, opts, blocks, ctxop
     assert "k_grid/cluster" in err and f"blocks {blocks}," in err, err
     _compare_run(A, ctx, O, h, p, m, 0, 0, iters)
     _compare_run(A, ctx, O, h, p, m, 1, c.tenure, iters // 2, seed=11, kick=6)
+    with ctx.options(PHASE_TIMES=1):   # the phase timers on the same path: every CTA of the cluster recorded
+        g = _compare_run(A, ctx, O, h, p, m, 1, c.tenure, 50)
+        ph = ctx.grid_phases()
+        t, sm = ctx.grid_cta_phases()
+    assert ph["iterations"] == g["iters_done"] == 50 and ph["own_tiles_us"] > 0
+    assert len(t) == blocks and (t > 0).all()
