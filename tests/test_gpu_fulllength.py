@@ -127,3 +127,18 @@ def test_bench_configuration_64_runs(A, ctx, oracle_mod):
         assert res[r]["best_obj"] == o["best_obj"] and res[r]["final_obj"] == o["final_obj"], r
         assert res[r]["best_iter"] == o["best_iter"] and res[r]["kicks_applied"] == o["kicks_applied"], r
         assert routes_of(bp[r], bm[r]) == routes_of(*o["best"]), r
+
+
+def test_large_c4_nowait_full_length(A, ctx, oracle_mod):
+    """f3 at C4's full length: the no-wait variant of C4 on the whole-GPU kernel (k_grid<..., NW>), TS for
+    all 20,000 iterations and NS to its local optimum, against the oracle's no-wait trajectory."""
+    import dataclasses
+    inst = dataclasses.replace(instgen.generate("large"), no_wait=1)
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    p, m = start(A, ctx, h, O)
+    c = instgen.CONFIGS["large"]
+    g, _ = compare_full(A, ctx, O, h, p, m, 1, c.tenure, c.max_iters)
+    assert g["iters_done"] == c.max_iters
+    g, _ = compare_full(A, ctx, O, h, p, m, 0, 0, c.max_iters)
+    assert g["stop_reason"] == 1
