@@ -445,9 +445,9 @@ __device__ __forceinline__ int move_relink(const MV &M, const RV &R, uint32_t id
     if (idx < Rb) {
         const int m = idx / S, t = idx % S;
         const int p = R.pred[m], s = R.succ[m];
+        const int c = R.pred[t];   // t's predecessor after the removal too: a valid t is neither m nor succ(m)
         R.succ[p] = s;
         R.pred[s] = p;
-        const int c = R.pred[t];
         R.succ[c] = m;
         R.pred[m] = c;
         R.succ[m] = t;
