@@ -102,6 +102,21 @@ int64_t as_valid_moves_per_iter(const as_instance *inst);
 as_status as_schedule_check(const as_instance *inst, const int32_t *route_ptr, const int32_t *route_missions,
                             int32_t *feasible, int64_t *objective);
 
+/* An owned, validated copy of a schedule: one ordered route per vehicle
+ * in CSR form.  Creation copies the arrays and applies as_schedule_check's rules (route_ptr[0] = 0 and
+ * non-decreasing, mission ids in range and listed at most once; every mission listed unless allow_partial),
+ * then stores the objective (Eq. obj_s) and feasibility (con6-con9).  The run calls take
+ * the CSR arrays directly (as_schedule_get hands them out); the handle is the caller's, freed with
+ * as_schedule_destroy.  Pointers: host. */
+typedef struct as_schedule as_schedule;
+as_status as_schedule_from_routes(const as_instance *inst, const int32_t *route_ptr, const int32_t *route_missions,
+                                  int32_t allow_partial, as_schedule **out);
+/* Any output may be NULL: route_ptr[V + 1], route_missions[n_assigned] (n_assigned = route_ptr[V]),
+ * objective (seconds), feasible (1 iff complete and feasible), n_assigned. */
+as_status as_schedule_get(const as_schedule *s, int32_t *route_ptr, int32_t *route_missions, int64_t *objective,
+                          int32_t *feasible, int32_t *n_assigned);
+void as_schedule_destroy(as_schedule *s);
+
 /* ----------------------------------------------------------------- context --
  * device: CUDA ordinal.  cuda_stream: a cudaStream_t (e.g. torch's current
  * stream); NULL = the legacy default stream. */

@@ -37,7 +37,7 @@ SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "a
            "as_ctx_last_kernel_ms", "as_ctx_kernel_launches", "as_last_error", "as_version",
            "as_comm_unique_id", "as_comm_init", "as_comm_destroy", "as_shard_plan", "as_batch_gather_best",
            "as_init_greedy_batch", "as_batch_run_jobs", "as_ctx_set_option", "as_ctx_grid_phases",
-           "as_ctx_grid_cta_phases"]
+           "as_ctx_grid_cta_phases", "as_schedule_from_routes", "as_schedule_get", "as_schedule_destroy"]
 
 
 class AirschedError(RuntimeError):
@@ -91,6 +91,9 @@ def _load():
         "as_move_space_size": (i64, [vp]),
         "as_valid_moves_per_iter": (i64, [vp]),
         "as_schedule_check": (i32, [vp, vp, vp, vp, vp]),
+        "as_schedule_from_routes": (i32, [vp, vp, vp, i32, vp]),
+        "as_schedule_get": (i32, [vp, vp, vp, vp, vp, vp]),
+        "as_schedule_destroy": (None, [vp]),
         "as_ctx_create": (i32, [i32, vp, vp]),
         "as_ctx_set_stream": (i32, [vp, vp]),
         "as_ctx_set_option": (i32, [vp, i32, i64]),
@@ -183,6 +186,33 @@ class Instance:
         ms = np.ascontiguousarray(ms, np.int32)
         _check(lib.as_schedule_check(self.handle, _ptr(ptr), _ptr(ms), C.byref(f), C.byref(o)))
         return bool(f.value), int(o.value)
+
+
+class Schedule:
+    """as_schedule: an owned, validated copy of a CSR schedule with its objective and feasibility."""
+
+    def __init__(self, inst, ptr, ms, allow_partial=False):
+        ptr = np.ascontiguousarray(ptr, np.int32)
+        ms = np.ascontiguousarray(ms, np.int32)
+        h = C.c_void_p()
+        _check(lib.as_schedule_from_routes(inst.handle, _ptr(ptr), _ptr(ms) if ms.size else None,
+                                           1 if allow_partial else 0, C.byref(h)))
+        self.handle = h
+        self.V = inst.V
+
+    def get(self):
+        """(route_ptr, route_missions, objective, feasible)."""
+        na, o, f = C.c_int32(), C.c_int64(), C.c_int32()
+        _check(lib.as_schedule_get(self.handle, None, None, None, None, C.byref(na)))
+        ptr = np.zeros(self.V + 1, np.int32)
+        ms = np.zeros(max(na.value, 1), np.int32)
+        _check(lib.as_schedule_get(self.handle, _ptr(ptr), _ptr(ms), C.byref(o), C.byref(f), None))
+        return ptr, ms[:na.value], int(o.value), bool(f.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.as_schedule_destroy(self.handle)
+            self.handle = None
 
 
 class Ctx:

@@ -224,6 +224,41 @@ extern "C" as_status as_schedule_check(const as_instance *I, const int32_t *ptr,
     return AS_OK;
 }
 
+struct as_schedule {
+    std::vector<int32_t> ptr, ms;
+    int64_t objective = 0;
+    int32_t feasible = 0;
+};
+
+extern "C" as_status as_schedule_from_routes(const as_instance *I, const int32_t *ptr, const int32_t *ms,
+                                             int32_t allow_partial, as_schedule **out) {
+    if (!I || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+    if (allow_partial != 0 && allow_partial != 1) return fail(AS_ERR_INVALID_ARG, "allow_partial must be 0 or 1");
+    HostSched S;
+    as_status st = parse_csr(I, ptr, ms, allow_partial != 0, S);
+    if (st != AS_OK) return st;
+    as_schedule *s = new (std::nothrow) as_schedule;
+    if (!s) return fail(AS_ERR_OOM, "host allocation");
+    s->ptr.assign(ptr, ptr + I->V + 1);
+    s->ms.assign(ms ? ms : ptr, ms ? ms + ptr[I->V] : ptr);
+    as_schedule_check(I, ptr, ms, &s->feasible, &s->objective);
+    *out = s;
+    return AS_OK;
+}
+
+extern "C" as_status as_schedule_get(const as_schedule *s, int32_t *ptr, int32_t *ms, int64_t *objective,
+                                     int32_t *feasible, int32_t *n_assigned) {
+    if (!s) return fail(AS_ERR_INVALID_ARG, "null schedule");
+    if (ptr) std::copy(s->ptr.begin(), s->ptr.end(), ptr);
+    if (ms) std::copy(s->ms.begin(), s->ms.end(), ms);
+    if (objective) *objective = s->objective;
+    if (feasible) *feasible = s->feasible;
+    if (n_assigned) *n_assigned = (int32_t)s->ms.size();
+    return AS_OK;
+}
+
+extern "C" void as_schedule_destroy(as_schedule *s) { delete s; }
+
 // ------------------------------------------------------------------ context --
 struct DevBuf {
     void *p = nullptr;

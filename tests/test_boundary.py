@@ -136,3 +136,39 @@ def test_library_reads_no_environment():
     import glob
     for f in glob.glob(os.path.join(ROOT, "paper_2002_11710_b200", "csrc", "*")):
         assert "getenv" not in open(f).read(), f
+
+
+def test_schedule_handles(A, oracle_mod):
+    """as_schedule_from_routes / as_schedule_get / as_schedule_destroy (host only): a validated copy of the
+    routes with the objective and feasibility the oracle gives (Eq. obj_s, con6-con9); partial schedules
+    only on request; the rules of as_schedule_check on bad input."""
+    inst = instgen.generate("ontario")
+    O = oracle_mod.Oracle(inst)
+    h = A.Instance(inst)
+    st, (p, m), _, _ = O.greedy()
+    s = A.Schedule(h, p, m)
+    gp, gm, obj, feas = s.get()
+    assert (gp == p).all() and (gm == m).all()
+    assert feas and obj == O.objective(p, m) and h.check(p, m) == (True, obj)
+    # a partial schedule: the last mission of the last non-empty route left out
+    V = inst.n_vehicles
+    v = max(u for u in range(V) if p[u + 1] > p[u])
+    pp = p.copy()
+    pp[v + 1:] -= 1
+    mm = np.delete(m, p[v + 1] - 1)
+    with pytest.raises(A.AirschedError):
+        A.Schedule(h, pp, mm)
+    s2 = A.Schedule(h, pp, mm, allow_partial=True)
+    gp2, gm2, obj2, feas2 = s2.get()
+    assert (gp2 == pp).all() and (gm2 == mm).all() and not feas2
+    assert obj2 == h.check(pp, mm)[1]
+    # a mission listed twice
+    bad = m.copy()
+    bad[1] = bad[0]
+    with pytest.raises(A.AirschedError) as e:
+        A.Schedule(h, p, bad)
+    assert e.value.status == A.AS_ERR_INVALID_ARG
+    # every route empty: a partial schedule with objective 0
+    empty = np.zeros(V + 1, np.int32)
+    s3 = A.Schedule(h, empty, np.zeros(0, np.int32), allow_partial=True)
+    assert s3.get()[2] == 0
