@@ -99,6 +99,7 @@ PATHS = {
     "k_grid_teglobal": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1},
     "k_grid_tglobal_g20": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_E_GLOBAL": 1, "GRID_G": 20},   # > SR_ROWS rows
     "k_grid_tglobal_norec": {"GRID": 1, "GRID_T_GLOBAL": 1, "GRID_SWAP_REC": 0},
+    "k_grid_cluster4": {"GRID": 1, "GRID_CLUSTER": 4},
     "k_batch": {"BATCH_KERNEL": 1},
     "sharded2": {"SHARDED": 1, "SHARD_EMULATE": 2, "SHARD_K": 3},
 }
