@@ -156,6 +156,7 @@ enum {
     AS_OPT_NODE_COSTS,         /* 0: no global node-cost table for the global-table scorers (set before upload) */
     AS_OPT_GRID_COMPACT,       /* 0: the whole-GPU kernel keeps the empty swap tiles in its tile list */
     AS_OPT_GRID_SWAP_REC,      /* 0: no per-warp swap-row records in the whole-GPU kernel's global-table scorers */
+    AS_OPT_GRID_WARPS,         /* warps per CTA of the whole-GPU kernel (1..20; default 20, 8 as one cluster) */
     AS_OPT_GRID_CLUSTER,       /* whole-GPU kernel as ONE thread-block cluster of this many CTAs (2..16; 0: never;
                                   automatic: 16 for small instances with shared-memory tables) */
     AS_OPT_COUNT

@@ -28,7 +28,7 @@ OPTIONS = ["SMEM_LIMIT", "T_SMEM", "WINDOW", "BATCH_KERNEL", "GRID", "GRID_MIN",
            "GRID_E_GLOBAL", "GRID_BLOCKS", "GRID_G", "VERBOSE", "RPC", "THREADS", "SHARDED", "GREEDY_GLOBAL",
            "SHARD_FUSED", "SHARD_FUSED_1", "SHARD_EMULATE", "SHARD_K", "XR_TIMEOUT_MS", "PHASE_TIMES",
            "NODE_COSTS", "GRID_COMPACT", "GRID_SWAP_REC",
-           "GRID_CLUSTER"]
+           "GRID_WARPS", "GRID_CLUSTER"]
 OPT_UNSET = -(1 << 63)
 
 SYMBOLS = ["as_instance_create", "as_instance_destroy", "as_move_space_size", "as_valid_moves_per_iter",

@@ -832,6 +832,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
     memset(&GA, 0, sizeof(GA));
     size_t grid_smem = 0;
     int grid_blocks = 0;
+    int grid_warps = GRID_WARPS;   // warps per CTA of the whole-GPU kernel (AS_OPT_GRID_WARPS)
     if (xr && !(single && compact_ok && !P->sweep))
         return fail(AS_ERR_UNSUPPORTED, "fused sharded run needs the compact layout");
     // the whole-GPU kernel also runs the no-wait variant (general scorers, engine.cuh's exact evaluation)
@@ -922,7 +923,11 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 // ceil(tiles / warps) rounds of G rows; take the G that minimises that (plus a per-round
                 // set-up of ~1.5 rows: measured G sweeps, profiles/r02/grid_g_sweep_*.jsonl), the larger G
                 // on ties; at most 32 rows (one key block).
-                const int64_t warps_all = (int64_t)grid_blocks * GRID_WARPS * (xr ? xr->nranks : 1);
+                // warps per CTA: 20, or 8 on one cluster (its 16 CTAs then hold a tile per warp, and the CTA barriers of
+                // the apply wait for fewer warps: C2 +6 %, the C3 instance alone +5 %, kgrid_warps_cluster.jsonl)
+                grid_warps = (int)std::max<int64_t>(1, std::min<int64_t>(GRID_WARPS, opt_int(ctx, AS_OPT_GRID_WARPS,
+                                                                                     GA.cluster > 1 ? 8 : GRID_WARPS)));
+                const int64_t warps_all = (int64_t)grid_blocks * grid_warps * (xr ? xr->nranks : 1);
                 const int64_t nTC = (S + 127) / 128, nSC = n > 1 ? (n - 1 + 63) / 64 : 0, nAdj = (n + 31) / 32;
                 const int gmax = GA.T_smem ? 256 : 32;
                 double best_cost = 1e300;
@@ -972,7 +977,7 @@ static as_status run_core(as_ctx *ctx, const as_instance *I, int32_t n_runs, con
                 use_grid ? grid_smem : smem);
     CUDA_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_grid) {
-        CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, GRID_WARPS * 32, grid_smem,
+        CUDA_TRY(launch_grid(A, GA, tabu ? 1 : 0, ctx->insts[I].tpad_bytes, grid_blocks, grid_warps * 32, grid_smem,
                              ctx->stream));
         ctx->launches += A.best_ptr ? 2 : 1;
         ctx->launches--;   // counted once below
